@@ -1,0 +1,111 @@
+/*
+ * zipfks_b200 — C ABI of the B200 (sm_100a) Monte Carlo engine for KS cutoff tables of the
+ * discrete power law (Zipf).  Plain pointers and sizes only; no torch types.
+ *
+ * The reference (zipfks 1.0.0, /root/reference/pkg) is a Python package with no FFI of its
+ * own.  These entry points replace the bodies of its Python functions at the batch seam
+ * (SURVEY.md §8b); the Python shim paper_1305_6738_b200 binds them with ctypes.  Each
+ * declaration cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - Return 0 on success.  ZKS_EINVAL: argument validation (the shim raises ValueError);
+ *     ZKS_ECUDA: CUDA failure (RuntimeError).  zks_last_error() gives the thread's message.
+ *   - "_dev" pointers are device memory owned by the caller; "_host" pointers host memory.
+ *   - Work is enqueued on the engine's stream (zks_engine_set_stream); calls that return host
+ *     results synchronise that stream.
+ */
+#ifndef ZIPFKS_B200_H
+#define ZIPFKS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZKS_OK 0
+#define ZKS_EINVAL 1
+#define ZKS_ECUDA 2
+
+#define ZKS_STATUS_OK 0         /* first stream succeeded                                */
+#define ZKS_STATUS_RETRIED 1    /* NoRootError on the first stream, retry at idx + 2^32 ok */
+#define ZKS_STATUS_FAILED 2     /* both streams failed (SimulationError in the shim)      */
+
+typedef struct zks_engine zks_engine;
+typedef struct zks_table zks_table;
+
+/* One (cell, repetition) slice of replicate indices [first, first + count).
+ * Mirrors SimulationConfig (montecarlo.py:50-72) plus the repetition / index range that
+ * run_repetition (montecarlo.py:174-191) and _pool_span (montecarlo.py:151-159) iterate. */
+typedef struct {
+  int32_t support_k;   /* Support.k; 0 = unbounded (draws from 1..65535, distribution.py:26) */
+  int32_t reserved;
+  double gamma;        /* generating exponent                                             */
+  int64_t n;           /* sample size per replicate                                       */
+  uint64_t base_seed;  /* stream key (base_seed, repetition, index), distribution.py:182-184 */
+  uint64_t repetition;
+  uint64_t first;      /* first replicate index                                            */
+  uint64_t count;      /* number of replicates                                             */
+} zks_cell;
+
+/* ABI version (bumped on any signature change). */
+int zks_version(void);
+
+/* Thread-local message for the last non-zero return. */
+const char* zks_last_error(void);
+
+/* Create an engine on `device`.  `logs_host[k] = ln k` for k = 0..logs_len-1 (entry 0 = 0),
+ * built by the shim with numpy exactly as series.natural_logs (series.py:31-44);
+ * logs_len must be >= 65537. */
+int zks_engine_create(int device, const double* logs_host, int64_t logs_len, zks_engine** out);
+void zks_engine_destroy(zks_engine* engine);
+
+/* Enqueue subsequent work on `stream` (a cudaStream_t; NULL = the legacy default stream).
+ * A new engine starts on its own non-blocking stream. */
+int zks_engine_set_stream(zks_engine* engine, void* stream);
+int zks_engine_sync(zks_engine* engine);
+
+/* Upload a host-built sampling CDF (ZipfModel._sampling_cdf, distribution.py:99-105):
+ * cdf_host[k-1] = P(X <= k) for k = 1..len, len = K or 65535, and build its guide table.
+ * Replaces the per-process lru_cache'd table build of _generating_model (montecarlo.py:82-86). */
+int zks_table_create(zks_engine* engine, const double* cdf_host, int64_t len, zks_table** out);
+void zks_table_destroy(zks_table* table);
+
+/* Replicates [first, first+count) of one cell and repetition: per replicate the KS statistic
+ * against the refitted model, the refitted exponent and a status byte.  Replaces
+ * run_replicate (montecarlo.py:98-116) looped by run_repetition / _pool_span
+ * (montecarlo.py:151-191).  Outputs are indexed by (index - first).  For status
+ * ZKS_STATUS_FAILED, ks is NaN and gamma_hat holds the mean log of the retry sample
+ * (the "mean log of data" in the NoRootError message, estimate.py:102-105).  Asynchronous. */
+int zks_run_replicates(zks_engine* engine, const zks_table* table, const zks_cell* cell, double* ks_dev,
+                       double* gamma_hat_dev, uint8_t* status_dev);
+
+/* Order statistics at zero-based `ranks_host[i]` of `count` non-negative doubles, written to
+ * out_host[i].  Replaces the np.sort + index of order_quantiles (montecarlo.py:119-136); the
+ * Decimal rank rule stays in the shim.  nranks <= 16.  Synchronous. */
+int zks_select_ranks(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,
+                     int32_t nranks, double* out_host);
+
+/* Same selection, asynchronous: the selected values land in out_dev[0..nranks) (device). */
+int zks_select_ranks_async(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,
+                           int32_t nranks, double* out_dev);
+
+/* normalization(gamma, support) (distribution.py:71-85): the finite power sum over 1..K
+ * (support_k > 0) or the zeta series with its Euler-Maclaurin tail (support_k == 0,
+ * series.py:126-138).  Synchronous. */
+int zks_normaliser(zks_engine* engine, double gamma, int32_t support_k, double* out_host);
+
+/* First `count` values of RandomStream.for_replicate(seed, rep, idx).uniforms(count)
+ * (distribution.py:182-187), bit-exact.  Asynchronous. */
+int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, uint64_t index, int64_t count,
+                        double* out_dev);
+
+/* Inverse-transform draws for given uniforms: searchsorted(cdf, u, 'left') + 1 clamped to the
+ * table length (sample, distribution.py:190-201).  Asynchronous. */
+int zks_draw(zks_engine* engine, const zks_table* table, const double* u_dev, int64_t count, int64_t* out_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZIPFKS_B200_H */

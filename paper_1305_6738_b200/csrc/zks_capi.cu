@@ -1,0 +1,321 @@
+// C ABI of the engine (include/zipfks_b200.h): engine / table lifetime, launches, errors.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/zipfks_b200.h"
+#include "zks_replicate.cuh"
+#include "zks_select.cuh"
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+#define ZKS_CUDA(call)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(ZKS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
+constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
+constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
+constexpr int64_t kStagingLen = 65536;                // doubles per slot
+
+}  // namespace
+
+struct zks_engine {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  double* logs = nullptr;
+  unsigned long long* work = nullptr;
+  uint16_t* slab = nullptr;
+  size_t slab_bytes = 0;
+  zks::SelectState* sel = nullptr;
+  double* sel_out = nullptr;
+  int blocks_per_sm = 0;
+  size_t smem_bytes_cached = 0;
+  // pinned staging ring: table uploads stay asynchronous w.r.t. queued kernels
+  double* staging = nullptr;
+  cudaEvent_t staging_done[kStagingSlots] = {};
+  int staging_next = 0;
+};
+
+struct zks_table {
+  zks_engine* engine = nullptr;
+  double* cdf = nullptr;
+  uint16_t* guide = nullptr;
+  uint32_t len = 0;
+};
+
+extern "C" {
+
+int zks_version(void) { return 1; }
+
+const char* zks_last_error(void) { return g_error.c_str(); }
+
+int zks_engine_create(int device, const double* logs_host, int64_t logs_len, zks_engine** out) {
+  if (!out) return fail(ZKS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!logs_host || logs_len < kLogsLen) return fail(ZKS_EINVAL, "log table needs >= %lld entries", (long long)kLogsLen);
+  int ndev = 0;
+  ZKS_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ZKS_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  ZKS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  ZKS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) return fail(ZKS_EINVAL, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+  zks_engine* e = new zks_engine();
+  e->device = device;
+  e->sms = prop.multiProcessorCount;
+  cudaError_t err = cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaMalloc(&e->logs, kLogsLen * sizeof(double));
+  if (err == cudaSuccess) err = cudaMemcpy(e->logs, logs_host, kLogsLen * sizeof(double), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMalloc(&e->work, sizeof(unsigned long long));
+  if (err == cudaSuccess) err = cudaMalloc(&e->sel, sizeof(zks::SelectState));
+  if (err == cudaSuccess) err = cudaMallocHost(&e->staging, kStagingSlots * kStagingLen * sizeof(double));
+  for (int i = 0; i < kStagingSlots && err == cudaSuccess; ++i)
+    err = cudaEventCreateWithFlags(&e->staging_done[i], cudaEventDisableTiming);
+  if (err != cudaSuccess) {
+    zks_engine_destroy(e);
+    return fail(ZKS_ECUDA, "engine allocation failed: %s", cudaGetErrorString(err));
+  }
+  e->stream = e->own;
+  *out = e;
+  return ZKS_OK;
+}
+
+void zks_engine_destroy(zks_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  cudaFree(e->logs);
+  cudaFree(e->work);
+  cudaFree(e->slab);
+  cudaFree(e->sel);
+  cudaFree(e->sel_out);
+  if (e->staging) cudaFreeHost(e->staging);
+  for (int i = 0; i < kStagingSlots; ++i)
+    if (e->staging_done[i]) cudaEventDestroy(e->staging_done[i]);
+  if (e->own) cudaStreamDestroy(e->own);
+  delete e;
+}
+
+int zks_engine_set_stream(zks_engine* e, void* stream) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  e->stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
+  return ZKS_OK;
+}
+
+int zks_engine_sync(zks_engine* e) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_table** out) {
+  if (!e || !out) return fail(ZKS_EINVAL, "engine/out is NULL");
+  *out = nullptr;
+  if (!cdf_host || len < 2 || len > 65535) return fail(ZKS_EINVAL, "cdf length %lld outside [2, 65535]", (long long)len);
+  ZKS_CUDA(cudaSetDevice(e->device));
+  zks_table* t = new zks_table();
+  t->engine = e;
+  t->len = static_cast<uint32_t>(len);
+  cudaError_t err = cudaMalloc(&t->cdf, len * sizeof(double));
+  if (err == cudaSuccess) err = cudaMalloc(&t->guide, (zks::kGuide + 2) * sizeof(uint16_t));
+  if (err == cudaSuccess) {
+    // stage through a pinned slot so the copy never waits for kernels already queued
+    const int slot = e->staging_next;
+    e->staging_next = (slot + 1) % kStagingSlots;
+    err = cudaEventSynchronize(e->staging_done[slot]);
+    double* stage = e->staging + slot * kStagingLen;
+    if (err == cudaSuccess) {
+      std::memcpy(stage, cdf_host, len * sizeof(double));
+      err = cudaMemcpyAsync(t->cdf, stage, len * sizeof(double), cudaMemcpyHostToDevice, e->stream);
+    }
+    if (err == cudaSuccess) err = cudaEventRecord(e->staging_done[slot], e->stream);
+  }
+  if (err == cudaSuccess) {
+    zks::guide_kernel<<<(zks::kGuide + 2 + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
+    err = cudaGetLastError();
+  }
+  if (err != cudaSuccess) {
+    zks_table_destroy(t);
+    return fail(ZKS_ECUDA, "table upload failed: %s", cudaGetErrorString(err));
+  }
+  *out = t;
+  return ZKS_OK;
+}
+
+void zks_table_destroy(zks_table* t) {
+  if (!t) return;
+  if (t->engine) {
+    cudaSetDevice(t->engine->device);
+    cudaStreamSynchronize(t->engine->stream);
+  }
+  cudaFree(t->cdf);
+  cudaFree(t->guide);
+  delete t;
+}
+
+int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
+                       uint8_t* st_dev) {
+  if (!e || !t || !c) return fail(ZKS_EINVAL, "engine/table/cell is NULL");
+  if (c->n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)c->n);
+  if (c->support_k < 0 || c->support_k == 1 || c->support_k > 32766)
+    return fail(ZKS_EINVAL, "finite support bound must be in [2, 32766], got %d", c->support_k);
+  const uint32_t L = c->support_k ? static_cast<uint32_t>(c->support_k) : 65535u;
+  if (t->len != L) return fail(ZKS_EINVAL, "table length %u does not match support (%u)", t->len, L);
+  if (c->count == 0) return ZKS_OK;
+  if (!ks_dev || !gh_dev || !st_dev) return fail(ZKS_EINVAL, "output pointer is NULL");
+  ZKS_CUDA(cudaSetDevice(e->device));
+
+  zks::ReplicateArgs a;
+  a.cdf = t->cdf;
+  a.guide = t->guide;
+  a.logs = e->logs;
+  a.L = L;
+  a.K = c->support_k;
+  a.H = static_cast<int32_t>(std::min<uint32_t>(L, zks::kHistMax));
+  a.hist_words = zks::round_up(std::max(a.H, 4) + 1, 4);
+  a.gamma = c->gamma;
+  a.n = c->n;
+  a.seed = c->base_seed;
+  a.rep = c->repetition;
+  a.first = c->first;
+  a.count = c->count;
+  a.ks_out = ks_dev;
+  a.gh_out = gh_dev;
+  a.st_out = st_dev;
+  a.work = e->work;
+
+  const size_t smem = zks::round_up((zks::kGuide + 2) * 2, 16) + size_t(zks::kWarps) * a.hist_words * 4;
+  if (smem != e->smem_bytes_cached) {
+    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zks::replicate_kernel, zks::kThreads, smem));
+    if (per_sm < 1) return fail(ZKS_ECUDA, "replicate kernel does not fit (smem %zu)", smem);
+    e->blocks_per_sm = per_sm;
+    e->smem_bytes_cached = smem;
+  }
+  int64_t blocks = int64_t(e->sms) * e->blocks_per_sm;
+  blocks = std::min<int64_t>(blocks, (int64_t)((c->count + zks::kWarps - 1) / zks::kWarps));
+  a.slab = nullptr;
+  a.slab_cap = 0;
+  if (L > static_cast<uint32_t>(a.H)) {
+    // worst case every draw of a replicate lands above the histogram: capacity n per warp
+    const size_t per_warp = size_t(c->n) * sizeof(uint16_t);
+    int64_t max_blocks = int64_t(kSlabBudget / (per_warp * zks::kWarps));
+    if (max_blocks < 1) return fail(ZKS_EINVAL, "sample size %lld too large for the overflow slab", (long long)c->n);
+    blocks = std::min(blocks, max_blocks);
+    const size_t need = per_warp * zks::kWarps * size_t(blocks);
+    if (need > e->slab_bytes) {
+      ZKS_CUDA(cudaStreamSynchronize(e->stream));
+      cudaFree(e->slab);
+      e->slab = nullptr;
+      e->slab_bytes = 0;
+      ZKS_CUDA(cudaMalloc(&e->slab, need));
+      e->slab_bytes = need;
+    }
+    a.slab = e->slab;
+    a.slab_cap = c->n;
+  }
+  ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+  zks::replicate_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
+                           int32_t nranks, double* out_dev) {
+  if (!e || !values_dev || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (count < 1) return fail(ZKS_EINVAL, "cannot take quantiles of an empty array");
+  if (nranks < 1 || nranks > zks::kMaxRanks) return fail(ZKS_EINVAL, "nranks %d outside [1, %d]", nranks, zks::kMaxRanks);
+  zks::RankList rl;
+  std::memset(&rl, 0, sizeof rl);
+  for (int i = 0; i < nranks; ++i) {
+    if (ranks_host[i] < 0 || ranks_host[i] >= count)
+      return fail(ZKS_EINVAL, "rank %lld out of range for %lld values", (long long)ranks_host[i], (long long)count);
+    rl.rank[i] = static_cast<unsigned long long>(ranks_host[i]);
+  }
+  ZKS_CUDA(cudaSetDevice(e->device));
+  zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->sel, rl, nranks);
+  ZKS_CUDA(cudaGetLastError());
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    zks::select_pass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(
+        reinterpret_cast<const unsigned long long*>(values_dev), count, shift, e->sel, nranks, out_dev);
+    ZKS_CUDA(cudaGetLastError());
+  }
+  return ZKS_OK;
+}
+
+int zks_select_ranks(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
+                     int32_t nranks, double* out_host) {
+  if (!e || !out_host) return fail(ZKS_EINVAL, "NULL argument");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
+  const int rc = zks_select_ranks_async(e, values_dev, count, ranks_host, nranks, e->sel_out);
+  if (rc) return rc;
+  ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, nranks * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_host) {
+  if (!e || !out_host) return fail(ZKS_EINVAL, "NULL argument");
+  if (support_k < 0 || support_k == 1 || support_k > 32766)
+    return fail(ZKS_EINVAL, "finite support bound must be in [2, 32766], got %d", support_k);
+  if (!(gamma == gamma) || gamma - gamma != 0.0) return fail(ZKS_EINVAL, "exponent must be finite, got %g", gamma);
+  if (support_k == 0 && gamma < zks::kMinUnboundedGamma)
+    return fail(ZKS_EINVAL, "unbounded support requires gamma >= 1.05, got %g", gamma);
+  ZKS_CUDA(cudaSetDevice(e->device));
+  if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
+  zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, e->sel_out);
+  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_stream_uniforms(zks_engine* e, uint64_t seed, uint64_t rep, uint64_t idx, int64_t count, double* out_dev) {
+  if (!e || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (count < 0) return fail(ZKS_EINVAL, "count must be >= 0");
+  if (count == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t nb = (count + 3) / 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (nb + 255) / 256));
+  zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, count, out_dev);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+int zks_draw(zks_engine* e, const zks_table* t, const double* u_dev, int64_t count, int64_t* out_dev) {
+  if (!e || !t || !u_dev || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (count < 0) return fail(ZKS_EINVAL, "count must be >= 0");
+  if (count == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (count + 255) / 256));
+  zks::draw_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(t->cdf, t->guide, t->len, u_dev, count, out_dev);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,420 @@
+// The fused replicate kernel: stream -> inverse-CDF draws -> histogram + log-sum ->
+// Newton/bisection MLE -> fitted normaliser -> KS scan, one warp per replicate.
+//
+// Restates, per replicate, pkg/src/zipfks/montecarlo.py:89-116 (_attempt / run_replicate)
+// with its leaves distribution.py:190-201 (sample), estimate.py:59-146 (log_mean, mle_gamma,
+// _bisect) and gof.py:49-105 (ks_statistic, dense and sparse paths).
+//
+// Layout (per block of kWarps warps):
+//   smem  guide[G+2]   uint16  lower_bound(cdf, j/G), j = 0..G, guide[G+1] = L
+//         hist[w][H+1] uint32  per-warp counts of values 1..H (H = min(L, 2048))
+//   global cdf[L]      fp64    host-built sampling CDF (bit-exact with the reference)
+//          logs[65537] fp64    host-built numpy ln k table
+//          slab[w][n]  uint16  per-warp list of values > H (only when L > H)
+// Draws are never materialised in HBM; per replicate only (ks, gamma_hat, status) is written.
+#pragma once
+#include <cstdint>
+
+#include "zks_series.cuh"
+#include "zks_stream.cuh"
+
+namespace zks {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kHistMax = 2048;             // histogram bins held in shared memory per warp
+constexpr int kGuideLog2 = 12;              // guide table resolution G = 4096
+constexpr int kGuide = 1 << kGuideLog2;
+constexpr double kLn2 = 0.69314718055994530942;  // math.log(2.0)
+constexpr double kKsMargin = 1e-11;  // early-exit safety margin (>> fp64 rounding of the sums)
+
+struct ReplicateArgs {
+  const double* cdf;
+  const uint16_t* guide;
+  const double* logs;
+  uint32_t L;      // draw-table length: K or 65535
+  int32_t K;       // finite support bound, 0 = unbounded
+  int32_t H;       // smem histogram bins per warp
+  int32_t hist_words;
+  double gamma;
+  int64_t n;
+  uint64_t seed, rep, first, count;
+  double* ks_out;
+  double* gh_out;
+  uint8_t* st_out;
+  uint16_t* slab;
+  int64_t slab_cap;
+  unsigned long long* work;
+};
+
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// smallest k (1-based) with cdf[k-1] >= u, clamped to L (distribution.py:200-201)
+__device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restrict__ guide,
+                                               const double* __restrict__ cdf, uint32_t L) {
+  const int j = static_cast<int>(u * static_cast<double>(kGuide));  // exact: G is 2^12
+  uint32_t lo = guide[j], hi = guide[j + 1];
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(cdf + mid) >= u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const uint32_t v = lo + 1;
+  return v > L ? L : v;
+}
+
+struct SampleStats {
+  double log_sum;
+  uint32_t vmin, vmax, over;
+};
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Draw n values of stream (seed, rep, sidx) into the warp's histogram / overflow slab.
+__device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint64_t sidx,
+                                                   const uint16_t* __restrict__ guide, uint32_t* hist,
+                                                   uint16_t* slab, int lane) {
+  uint64_t k0, k1;
+  stream_key(a.seed, a.rep, sidx, k0, k1);
+  const int64_t n = a.n;
+  const int64_t nb = (n + 3) >> 2;
+  const uint32_t H = static_cast<uint32_t>(a.H);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t c1 = 0, c2 = 0, c3 = 0, c4 = 0, vmin = 0xffffffffu, vmax = 0, over = 0;
+  double ls = 0.0;
+  for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+    const int64_t b = b0 + lane;
+    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const bool valid = (4 * b + w) < n;
+      uint32_t v = 0;
+      if (valid) {
+        v = draw_value(uniform_open_closed(r.w[w]), guide, a.cdf, a.L);
+        vmin = min(vmin, v);
+        vmax = max(vmax, v);
+        c1 += (v == 1u);
+        c2 += (v == 2u);
+        c3 += (v == 3u);
+        c4 += (v == 4u);
+        if (v > 4u) {
+          ls += __ldg(a.logs + v);
+          if (v <= H) atomicAdd(hist + v, 1u);
+        }
+      }
+      const bool ov = valid && v > H;
+      const unsigned mask = __ballot_sync(0xffffffffu, ov);
+      if (ov) slab[over + __popc(mask & lt_mask)] = static_cast<uint16_t>(v);
+      over += __popc(mask);
+    }
+  }
+  c1 = warp_sum_u32(c1);
+  c2 = warp_sum_u32(c2);
+  c3 = warp_sum_u32(c3);
+  c4 = warp_sum_u32(c4);
+  if (lane == 0) {
+    hist[1] = c1;
+    hist[2] = c2;
+    hist[3] = c3;
+    hist[4] = c4;
+  }
+  __syncwarp();
+  SampleStats s;
+  const double small = static_cast<double>(c2) * __ldg(a.logs + 2) + static_cast<double>(c3) * __ldg(a.logs + 3) +
+                       static_cast<double>(c4) * __ldg(a.logs + 4);
+  s.log_sum = warp_sum(ls) + small;
+  s.vmin = warp_min_u32(vmin);
+  s.vmax = warp_max_u32(vmax);
+  s.over = over;
+  return s;
+}
+
+__device__ __forceinline__ double model_mean(double x, int K, const double* logs, int lane, bool& ok) {
+  Moments m;
+  ok = log_moments(x, K, logs, lane, m);
+  return m.s1 / m.s0;
+}
+
+// estimate.py:94-112
+__device__ bool bisect_root(double target, int K, const double* logs, int lane, double lo, double hi,
+                            double& root) {
+  bool ok1, ok2;
+  const double f_lo = target - model_mean(lo, K, logs, lane, ok1);
+  const double f_hi = target - model_mean(hi, K, logs, lane, ok2);
+  if (!ok1 || !ok2) return false;
+  if (f_lo == 0.0) {
+    root = lo;
+    return true;
+  }
+  if (f_hi == 0.0) {
+    root = hi;
+    return true;
+  }
+  if (f_lo * f_hi > 0.0) return false;  // NoRootError
+  while (hi - lo > 1e-8) {
+    const double mid = 0.5 * (lo + hi);
+    bool ok;
+    const double f = target - model_mean(mid, K, logs, lane, ok);
+    if (f * f_lo <= 0.0)
+      hi = mid;
+    else
+      lo = mid;
+  }
+  root = 0.5 * (lo + hi);
+  return true;
+}
+
+// estimate.py:115-146 with DEFAULT_SETTINGS (x0 = 0.5, tol 1e-5, 200 iterations, [-20, 20])
+__device__ bool fit_exponent(double target, int K, const double* logs, int lane, double& g) {
+  double lo = -20.0, hi = 20.0;
+  if (K == 0) {
+    lo = kMinUnboundedGamma;
+    hi = kMaxUnboundedGamma;
+  }
+  double x = 0.5;
+  if (!(lo < x && x < hi)) x = lo + 0.01;
+  for (int it = 0; it < 200; ++it) {
+    Moments m;
+    if (!log_moments(x, K, logs, lane, m)) return false;
+    const double mean = m.s1 / m.s0;
+    const double slope = m.s2 / m.s0 - mean * mean;
+    const double x_new = x + (mean - target) / slope;
+    if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(target, K, logs, lane, lo, hi, g);
+    if (fabs(x_new - x) <= 1e-5) {
+      g = x_new;
+      return true;
+    }
+    x = x_new;
+  }
+  return bisect_root(target, K, logs, lane, lo, hi, g);
+}
+
+// Upper bound of sum_{k>=s} k^-g (s >= 2, g > 1): s^-g + s^(1-g)/(g-1).
+__device__ __forceinline__ double tail_upper(double g, double Ls) {
+  const double p = exp(-g * Ls);
+  return p + p * exp(Ls) / (g - 1.0);
+}
+
+struct KsState {
+  double Fb;       // fitted cdf through the last dense k
+  double F_seam;   // fitted cdf at min(kmax, 4096) (sparse endpoint 4097 - 1)
+  uint32_t Cb;     // observations <= last processed k
+  double D;        // lane-local running max gap
+  bool done;
+};
+
+// KS over tiles of 32 consecutive k in [k_first, k_last]; counts[k - base].
+// Dense semantics (gof.py:60-68) for k <= dense_end, sparse endpoint semantics
+// (gof.py:71-105) above it.  Exits early once no later k can beat the current max.
+__device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t k_last, const uint32_t* counts,
+                                         uint32_t base, uint32_t dense_end, double g, double norm, double inv,
+                                         double dn, const double* __restrict__ logs, int lane) {
+  for (uint32_t k0 = k_first; k0 <= k_last && !s.done; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    const bool in = k <= k_last;
+    const uint32_t c = in ? counts[k - base] : 0u;
+    const uint32_t C = s.Cb + warp_scan_u32(c, lane);
+    const double E = static_cast<double>(C) / dn;
+    const uint32_t k_hi = min(k0 + 31u, k_last);
+    double bound_f;
+    if (k0 <= dense_end) {
+      // tiles never straddle dense_end (tiles start at 1 mod 32 and the seam is 4096)
+      const double term = in ? exp(-g * __ldg(logs + k)) * inv : 0.0;
+      const double F = s.Fb + warp_scan(term, lane);
+      if (in) s.D = fmax(s.D, fabs(F - E));
+      s.Fb = __shfl_sync(0xffffffffu, F, 31);
+      if (k_hi == dense_end) s.F_seam = s.Fb;
+      bound_f = 1.0 - s.Fb;
+    } else {
+      if (in && c) {
+        const double Fv = (norm - tail_sum(g, __ldg(logs + k + 1))) / norm;
+        const double Fp = (k - 1 <= static_cast<uint32_t>(kSeam)) ? s.F_seam
+                                                                    : (norm - tail_sum(g, __ldg(logs + k))) / norm;
+        const double Eb = static_cast<double>(C - c) / dn;
+        s.D = fmax(s.D, fmax(fabs(Fv - E), fabs(Fp - Eb)));
+      }
+      bound_f = tail_upper(g, __ldg(logs + k_hi + 1)) * inv;
+    }
+    s.Cb = __shfl_sync(0xffffffffu, C, 31);
+    const double Dw = warp_max(s.D);
+    const double bound = fmax(1.0 - static_cast<double>(s.Cb) / dn, bound_f);
+    if (Dw > bound + kKsMargin) s.done = true;
+  }
+}
+
+__device__ double ks_scan(const ReplicateArgs& a, double g, double norm, const SampleStats& st, uint32_t* hist,
+                          const uint16_t* slab, int lane, bool& used_pages) {
+  const double inv = 1.0 / norm;
+  const double dn = static_cast<double>(a.n);
+  const uint32_t kmax = st.vmax;
+  const uint32_t H = static_cast<uint32_t>(a.H);
+  const uint32_t dense_end = (a.K > 0) ? kmax : min(kmax, static_cast<uint32_t>(kSeam));
+  KsState s{0.0, 0.0, 0u, 0.0, false};
+  ks_tiles(s, 1u, min(kmax, H), hist, 0u, dense_end, g, norm, inv, dn, a.logs, lane);
+  used_pages = false;
+  uint32_t pa = H + 1;
+  while (!s.done && pa <= kmax) {
+    used_pages = true;
+    const uint32_t pb = min(pa + H - 1, kmax);
+    // page histogram of the overflow values in [pa, pb]; next occupied value above pb
+    for (int i = lane; i < a.hist_words; i += 32) hist[i] = 0u;
+    __syncwarp();
+    uint32_t next = 0xffffffffu;
+    for (uint32_t i = lane; i < st.over; i += 32) {
+      const uint32_t v = slab[i];
+      if (v >= pa && v <= pb)
+        atomicAdd(hist + (v - pa), 1u);
+      else if (v > pb)
+        next = min(next, v);
+    }
+    next = warp_min_u32(next);
+    __syncwarp();
+    ks_tiles(s, pa, pb, hist, pa, dense_end, g, norm, inv, dn, a.logs, lane);
+    pa = pb + 1;
+    // sparse region: pages without observations carry no endpoints; jump to the next value
+    if (pa > dense_end && next != 0xffffffffu && next > pa) pa = next;
+  }
+  return warp_max(s.D);
+}
+
+__device__ __forceinline__ void clear_hist(uint32_t* hist, int words, int lane) {
+  uint4* h4 = reinterpret_cast<uint4*>(hist);
+  for (int i = lane; i < words / 4; i += 32) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
+  const int guide_bytes = round_up((kGuide + 2) * 2, 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * a.hist_words;
+  for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
+  clear_hist(hist, a.hist_words, lane);
+  __syncthreads();
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  uint16_t* slab = a.slab ? a.slab + gw * a.slab_cap : nullptr;
+  const int K = a.K;
+  const double dn = static_cast<double>(a.n);
+
+  for (;;) {
+    unsigned long long r = 0;
+    if (lane == 0) r = atomicAdd(a.work, 1ull);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= a.count) break;
+    const uint64_t idx = a.first + r;
+    double ks = __longlong_as_double(0x7ff8000000000000ll), gh = ks;
+    uint8_t status = 2;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const uint64_t sidx = idx + (attempt ? (1ull << 32) : 0ull);  // montecarlo.py:29,110
+      const SampleStats st = sample_pass(a, sidx, guide, hist, slab, lane);
+      double target = st.log_sum;
+      if (target <= 0.0) target += kLn2;  // estimate.py:71-72
+      target /= dn;
+      if (K > 0 && st.vmin == static_cast<uint32_t>(K))  // estimate.py:126-129
+        target -= (log(static_cast<double>(K)) - log(static_cast<double>(K - 1))) / dn;
+      double g = 0.0;
+      const bool ok = fit_exponent(target, K, a.logs, lane, g);
+      bool used_pages = false;
+      if (ok) {
+        const double norm = normaliser(g, K, a.logs, lane);
+        ks = ks_scan(a, g, norm, st, hist, slab, lane, used_pages);
+        gh = g;
+        status = static_cast<uint8_t>(attempt);
+      } else {
+        gh = target;  // diagnostics for the "failed twice" message
+      }
+      const int top = used_pages ? a.hist_words : round_up(static_cast<int>(min(max(st.vmax, 4u), (uint32_t)a.H)) + 1, 4);
+      clear_hist(hist, min(top, a.hist_words), lane);
+      if (ok) break;
+    }
+    if (lane == 0) {
+      a.ks_out[r] = ks;
+      a.gh_out[r] = gh;
+      a.st_out[r] = status;
+    }
+  }
+}
+
+// normalization(gamma, support) of one model (distribution.py:71-85), one warp
+__global__ void normaliser_kernel(double g, int K, const double* __restrict__ logs, double* out) {
+  const double v = normaliser(g, K, logs, threadIdx.x & 31);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// guide[j] = lower_bound(cdf, j / G) for j = 0..G; guide[G + 1] = L
+__global__ void guide_kernel(const double* __restrict__ cdf, uint32_t L, uint16_t* guide) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > kGuide + 1) return;
+  if (j == kGuide + 1) {
+    guide[j] = static_cast<uint16_t>(L);
+    return;
+  }
+  const double u = static_cast<double>(j) / static_cast<double>(kGuide);
+  uint32_t lo = 0, hi = L;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (cdf[mid] >= u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  guide[j] = static_cast<uint16_t>(lo);
+}
+
+// RandomStream.uniforms (distribution.py:186-187) for one stream, block-parallel
+__global__ void uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t idx, int64_t count, double* out) {
+  uint64_t k0, k1;
+  stream_key(seed, rep, idx, k0, k1);
+  const int64_t nb = (count + 3) >> 2;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      if (4 * b + w < count) out[4 * b + w] = uniform_open_closed(r.w[w]);
+  }
+}
+
+// sample() given uniforms (the FixedStream seam, test_distribution.py:24-32)
+__global__ void draw_kernel(const double* __restrict__ cdf, const uint16_t* __restrict__ guide, uint32_t L,
+                            const double* __restrict__ u, int64_t count, int64_t* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = u[i];
+    int64_t v;
+    if (x > 0.0 && x <= 1.0) {
+      v = draw_value(x, guide, cdf, L);
+    } else {
+      // outside (0, 1]: plain lower_bound over the whole table (searchsorted semantics)
+      uint32_t lo = 0, hi = L;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cdf[mid] >= x)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      v = lo + 1 > L ? L : lo + 1;
+    }
+    out[i] = v;
+  }
+}
+
+}  // namespace zks

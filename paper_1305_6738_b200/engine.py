@@ -1,0 +1,179 @@
+"""One CUDA engine per device: owns the C-ABI handle, the ln-k table and the draw tables.
+
+PyTorch is used only for device buffers and the current CUDA stream (plumbing).  Every
+numeric step of the hot path runs in ``libzks_b200.so``.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native
+from .series import natural_logs
+
+_LOG_LEN = 65537  # ln k for k = 0..65536 (tail endpoints reach 65536)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DrawTable:
+    """A sampling CDF resident on the device plus its guide table (zks_table)."""
+
+    __slots__ = ("handle", "length", "engine")
+
+    def __init__(self, engine: "Engine", cdf: np.ndarray):
+        cdf = np.ascontiguousarray(cdf, dtype=np.float64)
+        out = ctypes.c_void_p()
+        engine.bind_stream()
+        _native.check(engine.lib.zks_table_create(engine.handle, cdf.ctypes.data, cdf.size, ctypes.byref(out)))
+        self.handle = out
+        self.length = int(cdf.size)
+        self.engine = engine
+
+    def close(self) -> None:
+        if self.handle:
+            self.engine.lib.zks_table_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Engine:
+    """CUDA engine bound to one device (one per process and device)."""
+
+    def __init__(self, device: int | None = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("zipfks_b200 needs a CUDA device (sm_100a); none is visible")
+        self.lib = _native.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        logs = np.ascontiguousarray(natural_logs(_LOG_LEN - 1), dtype=np.float64)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.zks_engine_create(self.device, logs.ctypes.data, logs.size, ctypes.byref(handle)))
+        self.handle = handle
+        self._tables: OrderedDict[tuple, DrawTable] = OrderedDict()
+        self._lock = threading.Lock()
+
+    # -- streams -------------------------------------------------------------
+    def bind_stream(self):
+        """Enqueue engine work on torch's current stream of this device."""
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device)
+        _native.check(self.lib.zks_engine_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream)))
+        return stream
+
+    def sync(self) -> None:
+        _native.check(self.lib.zks_engine_sync(self.handle))
+
+    # -- tables --------------------------------------------------------------
+    def table(self, gamma: float, support_k: int | None, cdf_builder) -> DrawTable:
+        """Cached device table for the generating model (montecarlo.py:82-86 lru_cache)."""
+        key = (float(gamma), support_k)
+        with self._lock:
+            t = self._tables.get(key)
+            if t is not None:
+                self._tables.move_to_end(key)
+                return t
+            t = DrawTable(self, cdf_builder())
+            self._tables[key] = t
+            while len(self._tables) > 64:
+                _, old = self._tables.popitem(last=False)
+                old.close()
+            return t
+
+    # -- kernels -------------------------------------------------------------
+    def run_replicates(self, table: DrawTable, support_k: int | None, gamma: float, n: int, base_seed: int,
+                       repetition: int, first: int, count: int, ks, gamma_hat, status) -> None:
+        """Enqueue replicates [first, first+count) into device tensors (float64, float64, uint8)."""
+        cell = _native.ZksCell(
+            support_k=0 if support_k is None else int(support_k),
+            reserved=0,
+            gamma=float(gamma),
+            n=int(n),
+            base_seed=int(base_seed),
+            repetition=int(repetition),
+            first=int(first),
+            count=int(count),
+        )
+        self.bind_stream()
+        _native.check(
+            self.lib.zks_run_replicates(
+                self.handle, table.handle, ctypes.byref(cell), ks.data_ptr(), gamma_hat.data_ptr(), status.data_ptr()
+            )
+        )
+
+    def select_ranks(self, values, ranks: list[int], out=None):
+        """Order statistics of a device float64 tensor at zero-based ranks.
+
+        With ``out`` (device float64 tensor) the call is asynchronous; otherwise it returns a
+        list of floats.
+        """
+        r = np.ascontiguousarray(ranks, dtype=np.int64)
+        self.bind_stream()
+        if out is not None:
+            _native.check(
+                self.lib.zks_select_ranks_async(self.handle, values.data_ptr(), values.numel(), r.ctypes.data, r.size,
+                                                out.data_ptr())
+            )
+            return out
+        res = np.empty(r.size, dtype=np.float64)
+        _native.check(
+            self.lib.zks_select_ranks(self.handle, values.data_ptr(), values.numel(), r.ctypes.data, r.size,
+                                      res.ctypes.data)
+        )
+        return [float(x) for x in res]
+
+    def normaliser(self, gamma: float, support_k: int | None) -> float:
+        out = ctypes.c_double()
+        self.bind_stream()
+        _native.check(self.lib.zks_normaliser(self.handle, float(gamma), 0 if support_k is None else int(support_k),
+                                              ctypes.byref(out)))
+        return out.value
+
+    def uniforms(self, seed: int, repetition: int, index: int, count: int, out) -> None:
+        self.bind_stream()
+        _native.check(self.lib.zks_stream_uniforms(self.handle, int(seed), int(repetition), int(index), int(count),
+                                                   out.data_ptr()))
+
+    def draw(self, table: DrawTable, u, out) -> None:
+        self.bind_stream()
+        _native.check(self.lib.zks_draw(self.handle, table.handle, u.data_ptr(), u.numel(), out.data_ptr()))
+
+    def close(self) -> None:
+        for t in self._tables.values():
+            t.close()
+        self._tables.clear()
+        if self.handle:
+            self.lib.zks_engine_destroy(self.handle)
+            self.handle = None
+
+
+_ENGINES: dict[int, Engine] = {}
+_ENGINES_LOCK = threading.Lock()
+
+
+def get_engine(device: int | None = None) -> Engine:
+    """Process-wide engine of ``device`` (default: torch's current device)."""
+    torch = _torch()
+    if device is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("zipfks_b200 needs a CUDA device (sm_100a); none is visible")
+        device = torch.cuda.current_device()
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(device)
+        if eng is None:
+            eng = Engine(device)
+            _ENGINES[device] = eng
+        return eng

@@ -1,0 +1,375 @@
+"""Calibration engine on the GPU: replicates, order-statistic quantiles, cutoff tables.
+
+Drop-in for the reference ``zipfks.montecarlo`` (pkg/src/zipfks/montecarlo.py): same names,
+argument meaning, return types and error behaviour.  The per-replicate pipeline
+(sample -> re-fit -> KS against the re-fit, one retry on stream ``idx + 2**32``) and the
+quantile selection run in ``libzks_b200.so``; this module keeps the host-side contract:
+config validation, the Decimal rank rule, repetition averaging in repetition order, the
+error messages.  Streams are keyed ``(base_seed, repetition, index)``, so results do not
+depend on how replicates are batched or sharded over GPUs.
+"""
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+from decimal import ROUND_FLOOR, Decimal
+from typing import Callable, Iterable, Sequence
+
+import numpy as np
+
+from . import _native
+from .distribution import Support, sampling_cdf, validate_pair
+from .estimate import MAX_UNBOUNDED_GAMMA
+
+DEFAULT_LEVELS = (0.9, 0.95, 0.99, 0.999)  # montecarlo.py:26
+_RETRY_OFFSET = 1 << 32                    # montecarlo.py:29
+
+
+class SimulationError(RuntimeError):
+    """A replicate failed twice, or a table cell could not be computed (montecarlo.py:35)."""
+
+
+def _validate_levels(levels: Sequence[float]) -> tuple[float, ...]:
+    out = tuple(float(q) for q in levels)
+    if not out:
+        raise ValueError("at least one quantile level is required")
+    if any(not 0.0 < q < 1.0 for q in out):
+        raise ValueError(f"quantile levels must lie in (0, 1), got {out}")
+    if any(b <= a for a, b in zip(out, out[1:])):
+        raise ValueError(f"quantile levels must be strictly increasing, got {out}")
+    return out
+
+
+@dataclass(frozen=True)
+class SimulationConfig:
+    """One calibration experiment: R replicates repeated and averaged (montecarlo.py:50-72)."""
+
+    n: int
+    support: Support
+    gamma: float
+    base_seed: int
+    replicates: int = 50000
+    repetitions: int = 10
+    quantiles: tuple[float, ...] = DEFAULT_LEVELS
+
+    def __post_init__(self) -> None:
+        if self.n < 1:
+            raise ValueError(f"sample size must be >= 1, got {self.n}")
+        if self.replicates < 100:
+            raise ValueError(f"need at least 100 replicates, got {self.replicates}")
+        if self.repetitions < 1:
+            raise ValueError(f"need at least one repetition, got {self.repetitions}")
+        if not 0 <= int(self.base_seed) < 1 << 64:
+            raise ValueError("base_seed must fit an unsigned 64-bit integer")
+        object.__setattr__(self, "quantiles", _validate_levels(self.quantiles))
+        validate_pair(self.gamma, self.support)
+
+
+@dataclass(frozen=True)
+class ReplicateOutcome:
+    ks: float
+    gamma_hat: float
+    replicate_index: int
+
+
+def quantile_ranks(count: int, levels: Sequence[float]) -> list[int]:
+    """Zero-based ranks floor(Decimal(str(q)) * count) (montecarlo.py:133-135)."""
+    ranks = []
+    for level in _validate_levels(levels):
+        rank = int((Decimal(str(level)) * count).to_integral_value(rounding=ROUND_FLOOR))
+        if rank >= count:
+            raise ValueError(f"rank {rank} out of range for {count} values")
+        ranks.append(rank)
+    return ranks
+
+
+def resolve_workers(workers: int | None) -> int:
+    """Validated worker count (montecarlo.py:162-167).  Accepted for API compatibility: the
+    device does the parallel work, so results and speed do not depend on it."""
+    if workers is None:
+        return os.cpu_count() or 1
+    if workers < 1:
+        raise ValueError(f"worker count must be >= 1, got {workers}")
+    return workers
+
+
+# ---------------------------------------------------------------------------
+# device plumbing
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _engine():
+    from .engine import get_engine
+
+    return get_engine()
+
+
+def _table(eng, config: SimulationConfig):
+    return eng.table(config.gamma, config.support.k, lambda: sampling_cdf(config.gamma, config.support))
+
+
+class _Slab:
+    """Reusable device outputs (ks, gamma_hat, status) for up to ``cap`` replicates."""
+
+    def __init__(self, eng, cap: int):
+        torch = _torch()
+        dev = f"cuda:{eng.device}"
+        self.cap = cap
+        self.ks = torch.empty(cap, dtype=torch.float64, device=dev)
+        self.gh = torch.empty(cap, dtype=torch.float64, device=dev)
+        self.st = torch.empty(cap, dtype=torch.uint8, device=dev)
+
+
+_SLABS: dict[int, _Slab] = {}
+
+
+def _slab(eng, count: int) -> _Slab:
+    s = _SLABS.get(eng.device)
+    if s is None or s.cap < count:
+        s = _Slab(eng, max(count, 1024))
+        _SLABS[eng.device] = s
+    return s
+
+
+def _failure(config: SimulationConfig, repetition: int, index: int, mean_log: float) -> SimulationError:
+    low, high = (-20.0, 20.0) if config.support.is_finite else (1.05, MAX_UNBOUNDED_GAMMA)
+    reason = f"estimating equation has no root in [{low}, {high}] (mean log of data: {mean_log:.6g})"
+    return SimulationError(
+        f"replicate {index} (repetition {repetition}, gamma={config.gamma}, "
+        f"n={config.n}, support={config.support}) failed twice: {reason}"
+    )
+
+
+def _raise_first_failure(config, repetition, first, status: np.ndarray, gamma_hat: np.ndarray) -> None:
+    bad = np.flatnonzero(status == _native.STATUS_FAILED)
+    if bad.size:
+        i = int(bad[0])
+        raise _failure(config, repetition, first + i, float(gamma_hat[i]))
+
+
+def _enqueue(eng, config: SimulationConfig, repetition: int, first: int, count: int, slab: _Slab, offset: int = 0):
+    """Enqueue replicates [first, first+count) into slab[offset : offset+count]."""
+    table = _table(eng, config)
+    eng.run_replicates(
+        table, config.support.k, config.gamma, config.n, config.base_seed, repetition, first, count,
+        slab.ks[offset:], slab.gh[offset:], slab.st[offset:],
+    )
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+def run_replicate(config: SimulationConfig, index: int, repetition: int = 0) -> ReplicateOutcome:
+    """Sample, re-fit, and score one replicate (montecarlo.py:98-116), on the device."""
+    if not 0 <= index < config.replicates:
+        raise ValueError(f"replicate index {index} outside [0, {config.replicates})")
+    eng = _engine()
+    slab = _slab(eng, 1)
+    _enqueue(eng, config, repetition, index, 1, slab)
+    ks, gh, st = slab.ks[:1].cpu().numpy(), slab.gh[:1].cpu().numpy(), slab.st[:1].cpu().numpy()
+    _raise_first_failure(config, repetition, index, st, gh)
+    return ReplicateOutcome(ks=float(ks[0]), gamma_hat=float(gh[0]), replicate_index=index)
+
+
+def run_repetition(config: SimulationConfig, repetition: int, pool=None) -> tuple[np.ndarray, np.ndarray]:
+    """All replicate outcomes of one repetition in replicate-index order (montecarlo.py:174-191).
+
+    ``pool`` is accepted for signature compatibility and ignored: the device is the pool.
+    """
+    eng = _engine()
+    total = config.replicates
+    slab = _slab(eng, total)
+    _enqueue(eng, config, repetition, 0, total, slab)
+    ks = slab.ks[:total].cpu().numpy().copy()
+    gh = slab.gh[:total].cpu().numpy().copy()
+    st = slab.st[:total].cpu().numpy()
+    _raise_first_failure(config, repetition, 0, st, gh)
+    return ks, gh
+
+
+def order_quantiles(stats, levels: Sequence[float]) -> list[float]:
+    """Order statistics at zero-based ranks floor(R * level) (montecarlo.py:119-136).
+
+    ``stats`` may be a sequence, a numpy array or a CUDA float64 tensor; the selection runs
+    on the device (radix select over the order-preserving bit patterns of the values, so
+    the values must be non-negative, as KS statistics are).
+    """
+    torch = _torch()
+    eng = _engine()
+    if isinstance(stats, torch.Tensor) and stats.is_cuda:
+        values = stats.to(torch.float64).contiguous()
+    else:
+        arr = np.ascontiguousarray(np.asarray(stats, dtype=np.float64))
+        values = torch.from_numpy(arr).to(f"cuda:{eng.device}")
+    count = values.numel()
+    if count == 0:
+        raise ValueError("cannot take quantiles of an empty array")
+    ranks = quantile_ranks(count, levels)
+    if bool((values < 0).any()) or bool(torch.isnan(values).any()):
+        raise ValueError("order_quantiles on the device needs non-negative, non-NaN values")
+    values = values + 0.0  # canonicalise -0.0 to +0.0 (order-preserving bit patterns)
+    out = []
+    for i in range(0, len(ranks), 16):
+        out.extend(eng.select_ranks(values, ranks[i : i + 16]))
+    return out
+
+
+@dataclass
+class _CellPlan:
+    config: SimulationConfig
+    quantiles: object = None   # device [reps, levels]
+    worst: object = None       # device [reps] max status
+    started: object = None
+    finished: object = None
+
+
+def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, gather=None) -> None:
+    """Queue every repetition of one cell: replicates -> (gather) -> selection, all async."""
+    torch = _torch()
+    cfg = plan.config
+    total = cfg.replicates
+    first, stop = shard if shard is not None else (0, total)
+    dev = f"cuda:{eng.device}"
+    ranks = quantile_ranks(total, cfg.quantiles)
+    plan.quantiles = torch.empty((cfg.repetitions, len(ranks)), dtype=torch.float64, device=dev)
+    plan.worst = torch.empty(cfg.repetitions, dtype=torch.uint8, device=dev)
+    plan.started = torch.cuda.Event(enable_timing=True)
+    plan.finished = torch.cuda.Event(enable_timing=True)
+    slab = _slab(eng, total)
+    stream = eng.bind_stream()
+    plan.started.record(stream)
+    for rep in range(cfg.repetitions):
+        _enqueue(eng, cfg, rep, first, stop - first, slab, offset=first)
+        plan.worst[rep] = slab.st[first:stop].max() if stop > first else 0
+        ks = slab.ks[:total]
+        if gather is not None:
+            gather(ks, first, stop)
+        for i in range(0, len(ranks), 16):
+            eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+    plan.finished.record(stream)
+
+
+def _finish_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None) -> list[tuple[float, float]]:
+    cfg = plan.config
+    worst = plan.worst.cpu().numpy()
+    if worst.max(initial=0) >= _native.STATUS_FAILED:
+        # re-run the first failing repetition to name the first failing replicate
+        rep = int(np.flatnonzero(worst >= _native.STATUS_FAILED)[0])
+        first, stop = shard if shard is not None else (0, cfg.replicates)
+        slab = _slab(eng, cfg.replicates)
+        _enqueue(eng, cfg, rep, first, stop - first, slab, offset=first)
+        _raise_first_failure(cfg, rep, first, slab.st[first:stop].cpu().numpy(), slab.gh[first:stop].cpu().numpy())
+    per_rep = plan.quantiles.cpu().numpy()
+    per_level = np.zeros(per_rep.shape[1])
+    for rep in range(cfg.repetitions):  # montecarlo.py:203-211: add in repetition order
+        per_level += per_rep[rep]
+    per_level /= cfg.repetitions
+    return list(zip(cfg.quantiles, (float(c) for c in per_level)))
+
+
+def run_simulation(config: SimulationConfig, workers: int | None = None) -> list[tuple[float, float]]:
+    """(level, cutoff) pairs: per-repetition order quantiles averaged over repetitions
+    (montecarlo.py:194-212)."""
+    resolve_workers(workers)
+    eng = _engine()
+    plan = _CellPlan(config)
+    _enqueue_cell(eng, plan)
+    return _finish_cell(eng, plan)
+
+
+# ---------------------------------------------------------------------------
+# cutoff tables (montecarlo.py:218-314)
+
+class CutoffLookupError(LookupError):
+    """No tabulated cell matches the requested (gamma, n, level)."""
+
+
+GAMMA_LOOKUP_WINDOW = 0.005
+
+
+@dataclass(frozen=True, eq=True)
+class CutoffTable:
+    """Grid of cutoffs over (gamma, n) for one support, plus its provenance."""
+
+    support: Support
+    levels: tuple[float, ...]
+    gammas: tuple[float, ...]
+    ns: tuple[int, ...]
+    cells: dict[tuple[float, int], tuple[float, ...]] = field(compare=True)
+    replicates: int = 50000
+    repetitions: int = 10
+    base_seed: int = 0
+
+    def cutoffs_for(self, gamma: float, n: int) -> tuple[float, ...]:
+        if n not in self.ns:
+            raise CutoffLookupError(f"no tabulated sample size n={n}; compute a bespoke cutoff instead")
+        delta, nearest = min((abs(g - gamma), g) for g in self.gammas)
+        if delta > GAMMA_LOOKUP_WINDOW + 1e-12:
+            raise CutoffLookupError(
+                f"estimated exponent {gamma:.4f} is not within ±{GAMMA_LOOKUP_WINDOW} of "
+                f"any tabulated value; compute a bespoke cutoff instead"
+            )
+        return self.cells[(nearest, n)]
+
+    def cutoff(self, gamma: float, n: int, level: float) -> float:
+        row = self.cutoffs_for(gamma, n)
+        try:
+            return row[self.levels.index(float(level))]
+        except ValueError:
+            raise CutoffLookupError(f"level {level} not tabulated (have {self.levels})") from None
+
+
+def build_table(
+    ns: Iterable[int],
+    gammas: Iterable[float],
+    support: Support,
+    base_seed: int,
+    replicates: int = 50000,
+    repetitions: int = 10,
+    quantiles: Sequence[float] = DEFAULT_LEVELS,
+    workers: int | None = None,
+    progress: Callable[[float, int, float, tuple[float, ...]], None] | None = None,
+) -> CutoffTable:
+    """Fill the (gamma, n) grid (montecarlo.py:263-314).
+
+    Every cell reuses ``base_seed`` exactly as the reference does.  All cells are queued on
+    the device back to back (host table builds overlap device work); ``progress`` receives
+    each cell's device time in seconds.
+    """
+    ns = tuple(int(n) for n in ns)
+    gammas = tuple(float(g) for g in gammas)
+    if not ns or not gammas:
+        raise ValueError("both grids must be nonempty")
+    levels = _validate_levels(quantiles)
+    resolve_workers(workers)
+    plans: list[_CellPlan] = []
+    for gamma in gammas:
+        for n in ns:
+            try:
+                cfg = SimulationConfig(n=n, support=support, gamma=gamma, base_seed=base_seed,
+                                       replicates=replicates, repetitions=repetitions, quantiles=levels)
+            except Exception as err:
+                raise SimulationError(f"table cell (gamma={gamma}, n={n}) failed: {err}") from err
+            plans.append(_CellPlan(cfg))
+    eng = _engine()
+    for plan in plans:
+        _enqueue_cell(eng, plan)
+    cells: dict[tuple[float, int], tuple[float, ...]] = {}
+    for plan in plans:
+        cfg = plan.config
+        try:
+            pairs = _finish_cell(eng, plan)
+        except Exception as err:
+            raise SimulationError(f"table cell (gamma={cfg.gamma}, n={cfg.n}) failed: {err}") from err
+        row = tuple(c for _, c in pairs)
+        cells[(cfg.gamma, cfg.n)] = row
+        if progress is not None:
+            plan.finished.synchronize()
+            progress(cfg.gamma, cfg.n, plan.started.elapsed_time(plan.finished) / 1e3, row)
+    return CutoffTable(support=support, levels=levels, gammas=gammas, ns=ns, cells=cells,
+                       replicates=replicates, repetitions=repetitions, base_seed=base_seed)
