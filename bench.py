@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: KS replicates/s of the untruncated cutoff-table sweep (BASELINE.json configs[1]).
+
+Workload ("config2"): K = inf, gamma = 1.5..3.5 step 0.1 (21 values) x n in {10, 20, 50, 100,
+500, 1000} = 126 cells, base_seed = 1, one repetition, R = 10^6 replicates per cell and GPU
+(weak scaling: at N GPUs each cell has N*10^6 replicates, sharded by index, KS all-gathered
+over NCCL, exact quantiles selected on every rank).  One step = the whole 126-cell sweep:
+per replicate sample -> MLE refit -> KS, then the 4 order-statistic cutoffs per cell.
+
+  value        device time of the sweep with draw tables resident, L2 flushed between steps
+  e2e          the public API paper_1305_6738_b200.build_table (parallel.build_table at N>1):
+               host-built draw tables uploaded every step, cutoffs copied back to the host
+  roofline     replicate kernel work counted in-kernel (FP64 power terms, Philox draws) over
+               its measured launch time, against on-device micro-benchmarked pipe peaks
+  cpu_baseline the CPU oracle (numpy restatement of the reference, bit-identical to it) on
+               all host cores over a bounded sample of the same sweep
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port: the reference is a
+Python package and cannot travel to the GPU box) on this box's cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KS replicates/sec per (gamma,n) at 1/2/4/8 B200 vs host-CPU ref; roofline fraction"
+GAMMAS = tuple(round(1.5 + 0.1 * i, 1) for i in range(21))
+NS = (10, 20, 50, 100, 500, 1000)
+CPU_SAMPLE_GAMMAS = (1.5, 1.9, 2.3, 2.7, 3.1, 3.5)
+LAUNCHES_PER_CELL_REP = 10  # replicate kernel + select init + 8 radix passes
+CLOCK_QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def parse_args():
+    p = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    p.add_argument("--replicates", type=int, default=1_000_000, help="replicates per cell per GPU")
+    p.add_argument("--cpu-replicates", type=int, default=4096, help="replicates per sampled cell on the CPU")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={CLOCK_QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+def cpu_sample_run(replicates: int, workers: int) -> tuple[float, int, float]:
+    """The oracle (numpy restatement of the reference, bit-identical to it) over the sampled
+    cells of the sweep with ``workers`` processes; returns (replicates/s, replicates, seconds)."""
+    from oracle import port
+
+    total = 0
+    t0 = time.perf_counter()
+    for g in CPU_SAMPLE_GAMMAS:
+        for n in NS:
+            port.simulate(g, None, n, 1, replicates, 1, workers=workers)
+            total += replicates
+    dt = time.perf_counter() - t0
+    return total / dt, total, dt
+
+
+def cpu_sample_desc(replicates: int) -> str:
+    return (f"{len(CPU_SAMPLE_GAMMAS)} of 21 gammas {CPU_SAMPLE_GAMMAS} x n {NS} = "
+            f"{len(CPU_SAMPLE_GAMMAS) * len(NS)} cells x {replicates} replicates, K=inf, base_seed=1, "
+            f"1 repetition, multiprocessing pool over all cores (the reference's own parallel driver)")
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample_run(args.cpu_replicates, workers)
+    total = 0
+    secs = 0.0
+    for _ in range(args.steps):
+        _, reps, dt = cpu_sample_run(args.cpu_replicates, workers)
+        total += reps
+        secs += dt
+    value = total / secs
+    line = {
+        "metric": METRIC, "value": value, "unit": "replicates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2 untruncated sweep (bounded CPU sample)", "support": "inf",
+                   "gammas": list(CPU_SAMPLE_GAMMAS), "ns": list(NS), "replicates_per_cell": args.cpu_replicates,
+                   "repetitions": 1, "base_seed": 1},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "replicates/s", "cores": workers, "kind": "port",
+                         "sample": cpu_sample_desc(args.cpu_replicates)},
+        "e2e": {"value": value, "unit": "replicates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+def run_b200(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1305_6738_b200 as zk
+    from paper_1305_6738_b200 import montecarlo as mc
+    from paper_1305_6738_b200 import parallel
+    from paper_1305_6738_b200.engine import get_engine
+
+    torch.cuda.set_device(local)
+    eng = get_engine(local)
+    R = args.replicates * world  # weak scaling: replicates per GPU fixed
+    support = zk.Support.unbounded()
+    configs = [zk.SimulationConfig(n=n, support=support, gamma=g, base_seed=1, replicates=R, repetitions=1)
+               for g in GAMMAS for n in NS]
+    ncells = len(configs)
+    shard = parallel.shard_bounds(R, world, rank) if world > 1 else None
+    gather = parallel.ShardGather(R, world, rank) if world > 1 else None
+    mc._slab(eng, parallel.padded_size(R, world))
+    dev = torch.device("cuda", local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    kernel_events = []
+
+    def sweep(record_kernels=False):
+        plans = []
+        for cfg in configs:
+            plan = mc._CellPlan(cfg)
+            mc._enqueue_cell(eng, plan, shard=shard, gather=gather,
+                             kernel_events=kernel_events if record_kernels else None)
+            plans.append(plan)
+        return plans
+
+    # warm-up (also builds and uploads the 21 draw tables)
+    for _ in range(args.warmup):
+        sweep()
+    torch.cuda.synchronize()
+
+    # work counters for the roofline: one instrumented sweep outside the timed region
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    eng.set_counters(counters)
+    sweep()
+    torch.cuda.synchronize()
+    eng.set_counters(None)
+    work = [int(x) for x in counters.cpu().tolist()]
+    peaks = eng.probe_peaks()
+
+    # timed region
+    stream = torch.cuda.current_stream()
+    total_ms = 0.0
+    plans = None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plans = sweep(record_kernels=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            total_ms += e0.elapsed_time(e1)
+    clock = clocks.summary()
+    kernel_ms = sum(a.elapsed_time(b) for a, b in kernel_events)
+    t = torch.tensor([total_ms, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kernel_ms = t.tolist()
+    value = args.steps * ncells * R / (total_ms / 1e3)
+    rows = {(p.config.gamma, p.config.n): tuple(c for _, c in mc._finish_cell(eng, p, shard=shard)) for p in plans}
+    for row in rows.values():
+        assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
+
+    # roofline of the replicate kernel (dominant kernel)
+    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles = work
+    exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
+    terms = eval_terms + norm_terms + ks_terms
+    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * 8 * exp_flops  # tails: 2 tail sums x 4 exps
+    mul64 = 5.0 * draws  # 20 mulhilo per Philox block of 4 draws
+    launches = ncells  # one replicate kernel per cell per step (1 repetition)
+    kernel_s = kernel_ms / 1e3 / args.steps  # per sweep
+    t_fp64 = fp64_flops / peaks["dfma_flops"]
+    t_int = mul64 / peaks["mul64_per_s"]
+    if t_fp64 >= t_int:
+        roof = {"bound": "fp64", "achieved": fp64_flops / kernel_s / 1e12, "peak": peaks["dfma_flops"] / 1e12,
+                "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "int64-mul", "achieved": mul64 / kernel_s / 1e12, "peak": peaks["mul64_per_s"] / 1e12,
+                "unit": "Tmul64/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["peak_source"] = "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)"
+    roof["work_per_sweep"] = {"replicates": ncells * (R if world == 1 else shard[1] - shard[0]),
+                              "attempts": attempts, "draws": draws, "moment_evals": evals,
+                              "power_terms": terms, "ks_tail_endpoints": ks_tails,
+                              "fp64_exp_dfma_equiv": exp_flops}
+    roof["kernel_ms_per_launch"] = kernel_ms / args.steps / launches
+    roof["kernel_share_of_step"] = kernel_ms / total_ms
+    roof["t_ideal_fp64_ms"] = t_fp64 * 1e3 / launches
+    roof["t_ideal_int_ms"] = t_int * 1e3 / launches
+
+    # end to end through the public API (host tables built + uploaded each step)
+    e2e = None
+    if not args.no_e2e:
+        def api_call():
+            eng.clear_tables()
+            if world > 1:
+                return parallel.build_table(NS, GAMMAS, support, base_seed=1, replicates=R, repetitions=1)
+            return zk.build_table(NS, GAMMAS, support, base_seed=1, replicates=R, repetitions=1)
+
+        api_call()
+        torch.cuda.synchronize()
+        secs = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            table = api_call()
+            secs += time.perf_counter() - t0
+        tt = torch.tensor([secs], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt.item())
+        assert table.cells == rows, "public API and device sweep disagree"
+        e2e = {"value": args.steps * ncells * R / secs, "unit": "replicates/s",
+               "h2d_bytes_per_step": len(GAMMAS) * 65535 * 8,
+               "d2h_bytes_per_step": ncells * (4 * 8 + 1) + (4 * ncells if world > 1 else 0),
+               "api": "paper_1305_6738_b200.build_table" if world == 1 else "paper_1305_6738_b200.parallel.build_table"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        v, reps, dt = cpu_sample_run(args.cpu_replicates, workers)
+        cpu = {"value": v, "unit": "replicates/s", "cores": workers, "kind": "port",
+               "sample": cpu_sample_desc(args.cpu_replicates) + f"; {reps} replicates in {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "replicates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: untruncated Zipf, gamma 1.5..3.5 step 0.1 x n {10,20,50,100,500,1000}",
+                       "cells": ncells, "replicates_per_cell": R, "replicates_per_gpu_per_cell": args.replicates,
+                       "repetitions": 1, "base_seed": 1, "parallelism": f"dp{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * ncells * LAUNCHES_PER_CELL_REP,
+            "clocks": clock,
+            "cutoffs_sample": {f"{g},{n}": rows[(g, n)] for g, n in ((1.5, 10), (2.5, 100), (3.5, 1000))},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_env()
+    if world > 1 and args.impl == "b200":
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_b200(args, world, rank, local)
+    finally:
+        if world > 1 and args.impl == "b200":
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -104,6 +104,18 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * table length (sample, distribution.py:190-201).  Asynchronous. */
 int zks_draw(zks_engine* engine, const zks_table* table, const double* u_dev, int64_t count, int64_t* out_dev);
 
+/* ---- diagnostics (bench.py roofline; not part of the reference interface) ---------------- */
+
+/* Accumulate the replicate kernel's work counters into counters_dev[0..8) (u64, caller
+ * zeroes): attempts, draws, moment evaluations, moment terms, normaliser terms, KS dense
+ * terms, KS sparse endpoints, KS tiles.  NULL switches counting off. */
+int zks_engine_set_counters(zks_engine* engine, unsigned long long* counters_dev);
+
+/* On-device pipe peaks measured by micro-kernels: out_host[0] = FP64 DFMA FLOP/s,
+ * out_host[1] = FP64 exp() evaluations/s, out_host[2] = 64x64->128-bit multiplies/s
+ * (the Philox4x64 core).  Synchronous. */
+int zks_probe_peaks(zks_engine* engine, double* out_host);
+
 #ifdef __cplusplus
 }
 #endif

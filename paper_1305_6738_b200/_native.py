@@ -30,6 +30,8 @@ EXPORTS = (
     "zks_normaliser",
     "zks_stream_uniforms",
     "zks_draw",
+    "zks_engine_set_counters",
+    "zks_probe_peaks",
 )
 
 
@@ -77,6 +79,8 @@ def load() -> ctypes.CDLL:
     lib.zks_normaliser.argtypes = [vp, ctypes.c_double, i32, dp]
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]
+    lib.zks_engine_set_counters.argtypes = [vp, dp]
+    lib.zks_probe_peaks.argtypes = [vp, dp]
     for name in EXPORTS:
         if name not in ("zks_version", "zks_last_error", "zks_engine_destroy", "zks_table_destroy"):
             getattr(lib, name).restype = ctypes.c_int

@@ -10,6 +10,7 @@
 #include "../../include/zipfks_b200.h"
 #include "zks_replicate.cuh"
 #include "zks_select.cuh"
+#include "zks_probe.cuh"
 
 namespace {
 
@@ -55,6 +56,7 @@ struct zks_engine {
   double* staging = nullptr;
   cudaEvent_t staging_done[kStagingSlots] = {};
   int staging_next = 0;
+  unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
 };
 
 struct zks_table {
@@ -205,12 +207,15 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
   a.gh_out = gh_dev;
   a.st_out = st_dev;
   a.work = e->work;
+  a.counters = e->counters;
 
   const size_t smem = zks::round_up((zks::kGuide + 2) * 2, 16) + size_t(zks::kWarps) * a.hist_words * 4;
+  auto kernel = e->counters ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
   if (smem != e->smem_bytes_cached) {
-    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zks::replicate_kernel, zks::kThreads, smem));
+    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zks::replicate_kernel<false>, zks::kThreads, smem));
     if (per_sm < 1) return fail(ZKS_ECUDA, "replicate kernel does not fit (smem %zu)", smem);
     e->blocks_per_sm = per_sm;
     e->smem_bytes_cached = smem;
@@ -238,7 +243,7 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
     a.slab_cap = c->n;
   }
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
-  zks::replicate_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
+  kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
   ZKS_CUDA(cudaGetLastError());
   return ZKS_OK;
 }
@@ -293,6 +298,18 @@ int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_h
   ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
   return ZKS_OK;
+}
+
+int zks_engine_set_counters(zks_engine* e, unsigned long long* counters_dev) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  e->counters = counters_dev;
+  return ZKS_OK;
+}
+
+int zks_probe_peaks(zks_engine* e, double* out_host) {
+  if (!e || !out_host) return fail(ZKS_EINVAL, "NULL argument");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  return zks::probe_peaks(e->stream, e->sms, out_host) ? ZKS_OK : fail(ZKS_ECUDA, "peak probe failed");
 }
 
 int zks_stream_uniforms(zks_engine* e, uint64_t seed, uint64_t rep, uint64_t idx, int64_t count, double* out_dev) {

@@ -45,6 +45,7 @@ struct ReplicateArgs {
   uint16_t* slab;
   int64_t slab_cap;
   unsigned long long* work;
+  unsigned long long* counters;  // optional Work totals (kWorkFields), NULL = off
 };
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -145,18 +146,18 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
   return s;
 }
 
-__device__ __forceinline__ double model_mean(double x, int K, const double* logs, int lane, bool& ok) {
+__device__ __forceinline__ double model_mean(double x, int K, const double* logs, int lane, bool& ok, Work& wk) {
   Moments m;
-  ok = log_moments(x, K, logs, lane, m);
+  ok = log_moments(x, K, logs, lane, m, wk);
   return m.s1 / m.s0;
 }
 
 // estimate.py:94-112
 __device__ bool bisect_root(double target, int K, const double* logs, int lane, double lo, double hi,
-                            double& root) {
+                            double& root, Work& wk) {
   bool ok1, ok2;
-  const double f_lo = target - model_mean(lo, K, logs, lane, ok1);
-  const double f_hi = target - model_mean(hi, K, logs, lane, ok2);
+  const double f_lo = target - model_mean(lo, K, logs, lane, ok1, wk);
+  const double f_hi = target - model_mean(hi, K, logs, lane, ok2, wk);
   if (!ok1 || !ok2) return false;
   if (f_lo == 0.0) {
     root = lo;
@@ -170,7 +171,7 @@ __device__ bool bisect_root(double target, int K, const double* logs, int lane, 
   while (hi - lo > 1e-8) {
     const double mid = 0.5 * (lo + hi);
     bool ok;
-    const double f = target - model_mean(mid, K, logs, lane, ok);
+    const double f = target - model_mean(mid, K, logs, lane, ok, wk);
     if (f * f_lo <= 0.0)
       hi = mid;
     else
@@ -181,7 +182,7 @@ __device__ bool bisect_root(double target, int K, const double* logs, int lane, 
 }
 
 // estimate.py:115-146 with DEFAULT_SETTINGS (x0 = 0.5, tol 1e-5, 200 iterations, [-20, 20])
-__device__ bool fit_exponent(double target, int K, const double* logs, int lane, double& g) {
+__device__ bool fit_exponent(double target, int K, const double* logs, int lane, double& g, Work& wk) {
   double lo = -20.0, hi = 20.0;
   if (K == 0) {
     lo = kMinUnboundedGamma;
@@ -191,18 +192,18 @@ __device__ bool fit_exponent(double target, int K, const double* logs, int lane,
   if (!(lo < x && x < hi)) x = lo + 0.01;
   for (int it = 0; it < 200; ++it) {
     Moments m;
-    if (!log_moments(x, K, logs, lane, m)) return false;
+    if (!log_moments(x, K, logs, lane, m, wk)) return false;
     const double mean = m.s1 / m.s0;
     const double slope = m.s2 / m.s0 - mean * mean;
     const double x_new = x + (mean - target) / slope;
-    if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(target, K, logs, lane, lo, hi, g);
+    if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(target, K, logs, lane, lo, hi, g, wk);
     if (fabs(x_new - x) <= 1e-5) {
       g = x_new;
       return true;
     }
     x = x_new;
   }
-  return bisect_root(target, K, logs, lane, lo, hi, g);
+  return bisect_root(target, K, logs, lane, lo, hi, g, wk);
 }
 
 // Upper bound of sum_{k>=s} k^-g (s >= 2, g > 1): s^-g + s^(1-g)/(g-1).
@@ -224,8 +225,9 @@ struct KsState {
 // (gof.py:71-105) above it.  Exits early once no later k can beat the current max.
 __device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t k_last, const uint32_t* counts,
                                          uint32_t base, uint32_t dense_end, double g, double norm, double inv,
-                                         double dn, const double* __restrict__ logs, int lane) {
+                                         double dn, const double* __restrict__ logs, int lane, Work& wk) {
   for (uint32_t k0 = k_first; k0 <= k_last && !s.done; k0 += 32) {
+    ++wk.ks_tiles;
     const uint32_t k = k0 + lane;
     const bool in = k <= k_last;
     const uint32_t c = in ? counts[k - base] : 0u;
@@ -236,6 +238,7 @@ __device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t 
     if (k0 <= dense_end) {
       // tiles never straddle dense_end (tiles start at 1 mod 32 and the seam is 4096)
       const double term = in ? exp(-g * __ldg(logs + k)) * inv : 0.0;
+      wk.ks_terms += min(32u, k_last - k0 + 1);
       const double F = s.Fb + warp_scan(term, lane);
       if (in) s.D = fmax(s.D, fabs(F - E));
       s.Fb = __shfl_sync(0xffffffffu, F, 31);
@@ -249,6 +252,7 @@ __device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t 
         const double Eb = static_cast<double>(C - c) / dn;
         s.D = fmax(s.D, fmax(fabs(Fv - E), fabs(Fp - Eb)));
       }
+      wk.ks_tails += __popc(__ballot_sync(0xffffffffu, in && c));
       bound_f = tail_upper(g, __ldg(logs + k_hi + 1)) * inv;
     }
     s.Cb = __shfl_sync(0xffffffffu, C, 31);
@@ -259,14 +263,14 @@ __device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t 
 }
 
 __device__ double ks_scan(const ReplicateArgs& a, double g, double norm, const SampleStats& st, uint32_t* hist,
-                          const uint16_t* slab, int lane, bool& used_pages) {
+                          const uint16_t* slab, int lane, bool& used_pages, Work& wk) {
   const double inv = 1.0 / norm;
   const double dn = static_cast<double>(a.n);
   const uint32_t kmax = st.vmax;
   const uint32_t H = static_cast<uint32_t>(a.H);
   const uint32_t dense_end = (a.K > 0) ? kmax : min(kmax, static_cast<uint32_t>(kSeam));
   KsState s{0.0, 0.0, 0u, 0.0, false};
-  ks_tiles(s, 1u, min(kmax, H), hist, 0u, dense_end, g, norm, inv, dn, a.logs, lane);
+  ks_tiles(s, 1u, min(kmax, H), hist, 0u, dense_end, g, norm, inv, dn, a.logs, lane, wk);
   used_pages = false;
   uint32_t pa = H + 1;
   while (!s.done && pa <= kmax) {
@@ -285,7 +289,7 @@ __device__ double ks_scan(const ReplicateArgs& a, double g, double norm, const S
     }
     next = warp_min_u32(next);
     __syncwarp();
-    ks_tiles(s, pa, pb, hist, pa, dense_end, g, norm, inv, dn, a.logs, lane);
+    ks_tiles(s, pa, pb, hist, pa, dense_end, g, norm, inv, dn, a.logs, lane, wk);
     pa = pb + 1;
     // sparse region: pages without observations carry no endpoints; jump to the next value
     if (pa > dense_end && next != 0xffffffffu && next > pa) pa = next;
@@ -299,6 +303,7 @@ __device__ __forceinline__ void clear_hist(uint32_t* hist, int words, int lane) 
   __syncwarp();
 }
 
+template <bool kCount>
 __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
@@ -312,6 +317,7 @@ __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
   uint16_t* slab = a.slab ? a.slab + gw * a.slab_cap : nullptr;
   const int K = a.K;
   const double dn = static_cast<double>(a.n);
+  Work wk{0, 0, 0, 0, 0, 0, 0, 0};
 
   for (;;) {
     unsigned long long r = 0;
@@ -324,17 +330,19 @@ __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
     for (int attempt = 0; attempt < 2; ++attempt) {
       const uint64_t sidx = idx + (attempt ? (1ull << 32) : 0ull);  // montecarlo.py:29,110
       const SampleStats st = sample_pass(a, sidx, guide, hist, slab, lane);
+      ++wk.attempts;
+      wk.draws += a.n;
       double target = st.log_sum;
       if (target <= 0.0) target += kLn2;  // estimate.py:71-72
       target /= dn;
       if (K > 0 && st.vmin == static_cast<uint32_t>(K))  // estimate.py:126-129
         target -= (log(static_cast<double>(K)) - log(static_cast<double>(K - 1))) / dn;
       double g = 0.0;
-      const bool ok = fit_exponent(target, K, a.logs, lane, g);
+      const bool ok = fit_exponent(target, K, a.logs, lane, g, wk);
       bool used_pages = false;
       if (ok) {
-        const double norm = normaliser(g, K, a.logs, lane);
-        ks = ks_scan(a, g, norm, st, hist, slab, lane, used_pages);
+        const double norm = normaliser(g, K, a.logs, lane, wk);
+        ks = ks_scan(a, g, norm, st, hist, slab, lane, used_pages, wk);
         gh = g;
         status = static_cast<uint8_t>(attempt);
       } else {
@@ -350,11 +358,17 @@ __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
       a.st_out[r] = status;
     }
   }
+  if (kCount && lane == 0) {
+    const unsigned long long* f = &wk.attempts;
+    for (int i = 0; i < kWorkFields; ++i)
+      if (f[i]) atomicAdd(a.counters + i, f[i]);
+  }
 }
 
 // normalization(gamma, support) of one model (distribution.py:71-85), one warp
 __global__ void normaliser_kernel(double g, int K, const double* __restrict__ logs, double* out) {
-  const double v = normaliser(g, K, logs, threadIdx.x & 31);
+  Work wk{};
+  const double v = normaliser(g, K, logs, threadIdx.x & 31, wk);
   if (threadIdx.x == 0) *out = v;
 }
 

@@ -151,6 +151,25 @@ class Engine:
         self.bind_stream()
         _native.check(self.lib.zks_draw(self.handle, table.handle, u.data_ptr(), u.numel(), out.data_ptr()))
 
+    # -- diagnostics ---------------------------------------------------------
+    def set_counters(self, counters) -> None:
+        """Count replicate-kernel work into a device uint64/int64 tensor of 8 (None = off)."""
+        ptr = None if counters is None else ctypes.c_void_p(counters.data_ptr())
+        _native.check(self.lib.zks_engine_set_counters(self.handle, ptr))
+
+    def probe_peaks(self) -> dict:
+        """Measured pipe peaks of this device: DFMA FLOP/s, FP64 exp/s, 64-bit mulhilo/s."""
+        out = (ctypes.c_double * 3)()
+        self.bind_stream()
+        _native.check(self.lib.zks_probe_peaks(self.handle, out))
+        return {"dfma_flops": out[0], "exp_per_s": out[1], "mul64_per_s": out[2]}
+
+    def clear_tables(self) -> None:
+        with self._lock:
+            for t in self._tables.values():
+                t.close()
+            self._tables.clear()
+
     def close(self) -> None:
         for t in self._tables.values():
             t.close()

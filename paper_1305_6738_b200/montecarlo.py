@@ -228,8 +228,14 @@ class _CellPlan:
     finished: object = None
 
 
-def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, gather=None) -> None:
-    """Queue every repetition of one cell: replicates -> (gather) -> selection, all async."""
+def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, gather=None,
+                  kernel_events: list | None = None) -> None:
+    """Queue every repetition of one cell: replicates -> (gather) -> selection, all async.
+
+    ``shard`` = (first, stop) restricts this process to replicate indices [first, stop);
+    ``gather(slab_ks)`` must then return a device tensor whose first ``replicates`` entries are
+    the KS values of every index in order (the multi-GPU all-gather, parallel.py).
+    """
     torch = _torch()
     cfg = plan.config
     total = cfg.replicates
@@ -237,18 +243,23 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
     dev = f"cuda:{eng.device}"
     ranks = quantile_ranks(total, cfg.quantiles)
     plan.quantiles = torch.empty((cfg.repetitions, len(ranks)), dtype=torch.float64, device=dev)
-    plan.worst = torch.empty(cfg.repetitions, dtype=torch.uint8, device=dev)
+    plan.worst = torch.zeros(cfg.repetitions, dtype=torch.uint8, device=dev)
     plan.started = torch.cuda.Event(enable_timing=True)
     plan.finished = torch.cuda.Event(enable_timing=True)
     slab = _slab(eng, total)
     stream = eng.bind_stream()
     plan.started.record(stream)
     for rep in range(cfg.repetitions):
-        _enqueue(eng, cfg, rep, first, stop - first, slab, offset=first)
-        plan.worst[rep] = slab.st[first:stop].max() if stop > first else 0
-        ks = slab.ks[:total]
-        if gather is not None:
-            gather(ks, first, stop)
+        if stop > first:
+            if kernel_events is not None:  # bench.py: time the replicate kernel itself
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record(stream)
+            _enqueue(eng, cfg, rep, first, stop - first, slab, offset=first)
+            if kernel_events is not None:
+                k1.record(stream)
+                kernel_events.append((k0, k1))
+            plan.worst[rep] = slab.st[first:stop].max()
+        ks = slab.ks[:total] if gather is None else gather(slab.ks)[:total]
         for i in range(0, len(ranks), 16):
             eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
     plan.finished.record(stream)

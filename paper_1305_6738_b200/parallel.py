@@ -1,0 +1,126 @@
+"""Multi-GPU cutoff tables: one process per GPU, replicate ranges sharded, KS all-gathered.
+
+The reference parallelises one repetition over a process pool of 512-replicate spans
+(montecarlo.py:151-191) and is worker-count invariant because streams are keyed
+``(base_seed, repetition, index)``.  Here each rank of a ``torch.distributed`` group (NCCL
+over NVLink on a B200 box) computes a contiguous shard of replicate indices of every
+(cell, repetition) into its slice of a device buffer, an all-gather assembles the full
+index-ordered KS array on every rank, and every rank runs the same exact selection, so the
+table is bit-identical for any number of GPUs.  The only data-path collective is that
+all-gather (8 B per replicate); a cell's worst status is all-reduced so every rank raises
+the same SimulationError.
+"""
+from __future__ import annotations
+
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _native
+from .distribution import Support
+from .montecarlo import (
+    DEFAULT_LEVELS,
+    CutoffTable,
+    SimulationConfig,
+    SimulationError,
+    _CellPlan,
+    _engine,
+    _enqueue_cell,
+    _finish_cell,
+    _slab,
+    _validate_levels,
+)
+
+
+def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous equal-size shards: rank r owns [r*c, min((r+1)*c, total)), c = ceil(total/world)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    chunk = -(-total // world)
+    start = min(rank * chunk, total)
+    return start, min(start + chunk, total)
+
+
+def padded_size(total: int, world: int) -> int:
+    return -(-total // world) * world
+
+
+class ShardGather:
+    """All-gather of equal-size shards of a 1-D tensor into index order."""
+
+    def __init__(self, total: int, world: int, rank: int, group=None):
+        self.total, self.world, self.rank, self.group = total, world, rank, group
+        self.chunk = -(-total // world)
+        self.out = None
+
+    def __call__(self, local_full):
+        import torch
+        import torch.distributed as dist
+
+        need = self.chunk * self.world
+        if self.out is None or self.out.numel() < need or self.out.device != local_full.device:
+            self.out = torch.empty(need, dtype=local_full.dtype, device=local_full.device)
+        start = self.rank * self.chunk
+        mine = local_full[start : start + self.chunk]
+        if mine.numel() < self.chunk:  # last shard shorter than the padded chunk
+            pad = torch.zeros(self.chunk, dtype=local_full.dtype, device=local_full.device)
+            pad[: mine.numel()] = mine
+            mine = pad
+        dist.all_gather_into_tensor(self.out[:need], mine.contiguous(), group=self.group)
+        return self.out[: self.total]
+
+
+def build_table(
+    ns: Iterable[int],
+    gammas: Iterable[float],
+    support: Support,
+    base_seed: int,
+    replicates: int = 50000,
+    repetitions: int = 10,
+    quantiles: Sequence[float] = DEFAULT_LEVELS,
+    group=None,
+) -> CutoffTable:
+    """montecarlo.build_table over every GPU of ``group`` (default: the world group).
+
+    Call collectively from every rank; every rank returns the same table, equal bit for bit
+    to the single-GPU result.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ns = tuple(int(n) for n in ns)
+    gammas = tuple(float(g) for g in gammas)
+    if not ns or not gammas:
+        raise ValueError("both grids must be nonempty")
+    levels = _validate_levels(quantiles)
+    eng = _engine()
+    plans = []
+    for gamma in gammas:
+        for n in ns:
+            cfg = SimulationConfig(n=n, support=support, gamma=gamma, base_seed=base_seed, replicates=replicates,
+                                   repetitions=repetitions, quantiles=levels)
+            plans.append(_CellPlan(cfg))
+    shard = shard_bounds(replicates, world, rank)
+    gather = ShardGather(replicates, world, rank, group)
+    _slab(eng, padded_size(replicates, world))
+    for plan in plans:
+        _enqueue_cell(eng, plan, shard=shard, gather=gather)
+    worst = torch.stack([p.worst.max() for p in plans]).to(torch.int32)
+    dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
+    for plan, w in zip(plans, worst.tolist()):
+        plan.worst.fill_(w if w < _native.STATUS_FAILED else 0)
+    cells = {}
+    for plan, w in zip(plans, worst.tolist()):
+        cfg = plan.config
+        if w >= _native.STATUS_FAILED:
+            raise SimulationError(f"table cell (gamma={cfg.gamma}, n={cfg.n}) failed: a replicate failed twice")
+        cells[(cfg.gamma, cfg.n)] = tuple(c for _, c in _finish_cell(eng, plan, shard=shard))
+    return CutoffTable(support=support, levels=levels, gammas=gammas, ns=ns, cells=cells, replicates=replicates,
+                       repetitions=repetitions, base_seed=base_seed)
+
+
+def gathered_order(values_by_rank: list[np.ndarray], total: int) -> np.ndarray:
+    """Host-side model of the gather (tests): concatenate equal-size padded shards, keep prefix."""
+    return np.concatenate(values_by_rank)[:total]
