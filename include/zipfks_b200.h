@@ -31,6 +31,9 @@ extern "C" {
 #define ZKS_STATUS_RETRIED 1    /* NoRootError on the first stream, retry at idx + 2^32 ok */
 #define ZKS_STATUS_FAILED 2     /* both streams failed (SimulationError in the shim)      */
 
+#define ZKS_MLE_TABLE 0   /* model moments from the device fit tables (default)           */
+#define ZKS_MLE_DIRECT 1  /* model moments by direct summation, as the reference forms them */
+
 typedef struct zks_engine zks_engine;
 typedef struct zks_table zks_table;
 
@@ -104,7 +107,16 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * table length (sample, distribution.py:190-201).  Asynchronous. */
 int zks_draw(zks_engine* engine, const zks_table* table, const double* u_dev, int64_t count, int64_t* out_dev);
 
-/* ---- diagnostics (bench.py roofline; not part of the reference interface) ---------------- */
+/* ---- diagnostics (bench.py roofline, parity tests; not part of the reference interface) --- */
+
+/* How the replicate kernel evaluates the model functions of the exponent fit
+ * (estimate.py:76-83): ZKS_MLE_TABLE (default) or ZKS_MLE_DIRECT. */
+int zks_engine_set_mle_mode(zks_engine* engine, int mode);
+
+/* Evaluate the fit table of support_k (0 = unbounded) at x_dev[0..count): model mean of ln X,
+ * E[(ln X)^2] and the normaliser (zeta_value for the unbounded support).  Asynchronous. */
+int zks_fit_eval(zks_engine* engine, int32_t support_k, const double* x_dev, int64_t count, double* mu_dev,
+                 double* m2_dev, double* norm_dev);
 
 /* Accumulate the replicate kernel's work counters into counters_dev[0..8) (u64, caller
  * zeroes): attempts, draws, moment evaluations, moment terms, normaliser terms, KS dense

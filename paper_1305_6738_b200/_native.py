@@ -12,6 +12,7 @@ from ._build import LIB
 
 ZKS_OK, ZKS_EINVAL, ZKS_ECUDA = 0, 1, 2
 STATUS_OK, STATUS_RETRIED, STATUS_FAILED = 0, 1, 2
+MLE_TABLE, MLE_DIRECT = 0, 1
 ABI_VERSION = 1
 
 # every symbol include/zipfks_b200.h declares
@@ -30,6 +31,8 @@ EXPORTS = (
     "zks_normaliser",
     "zks_stream_uniforms",
     "zks_draw",
+    "zks_engine_set_mle_mode",
+    "zks_fit_eval",
     "zks_engine_set_counters",
     "zks_probe_peaks",
 )
@@ -80,6 +83,8 @@ def load() -> ctypes.CDLL:
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]
     lib.zks_engine_set_counters.argtypes = [vp, dp]
+    lib.zks_engine_set_mle_mode.argtypes = [vp, ctypes.c_int]
+    lib.zks_fit_eval.argtypes = [vp, i32, dp, i64, dp, dp, dp]
     lib.zks_probe_peaks.argtypes = [vp, dp]
     for name in EXPORTS:
         if name not in ("zks_version", "zks_last_error", "zks_engine_destroy", "zks_table_destroy"):

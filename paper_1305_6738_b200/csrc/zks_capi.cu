@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 
 #include "../../include/zipfks_b200.h"
@@ -57,7 +58,31 @@ struct zks_engine {
   cudaEvent_t staging_done[kStagingSlots] = {};
   int staging_next = 0;
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
+  int mle_mode = ZKS_MLE_TABLE;
+  std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
 };
+
+namespace {
+
+// exponent-fit table of support K, built on the engine stream on first use
+int fit_table_for(zks_engine* e, int K, zks::FitTable** out) {
+  auto it = e->fit_tables.find(K);
+  if (it == e->fit_tables.end()) {
+    zks::FitTable T = zks::fit_layout(K);
+    double* coef = nullptr;
+    ZKS_CUDA(cudaMalloc(&coef, size_t(T.intervals) * zks::kFitStride * sizeof(double)));
+    T.coef = coef;
+    const int threads = 128;
+    const int blocks = (T.intervals * 32 + threads - 1) / threads;
+    zks::fit_table_kernel<<<blocks, threads, 0, e->stream>>>(T, coef, e->logs);
+    ZKS_CUDA(cudaGetLastError());
+    it = e->fit_tables.emplace(K, T).first;
+  }
+  *out = &it->second;
+  return ZKS_OK;
+}
+
+}  // namespace
 
 struct zks_table {
   zks_engine* engine = nullptr;
@@ -112,6 +137,7 @@ void zks_engine_destroy(zks_engine* e) {
   cudaFree(e->slab);
   cudaFree(e->sel);
   cudaFree(e->sel_out);
+  for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
   for (int i = 0; i < kStagingSlots; ++i)
     if (e->staging_done[i]) cudaEventDestroy(e->staging_done[i]);
@@ -208,6 +234,15 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
   a.st_out = st_dev;
   a.work = e->work;
   a.counters = e->counters;
+  a.use_table = e->mle_mode == ZKS_MLE_TABLE;
+  if (a.use_table) {
+    zks::FitTable* T = nullptr;
+    const int rc = fit_table_for(e, c->support_k, &T);
+    if (rc) return rc;
+    a.fit = *T;
+  } else {
+    a.fit = zks::FitTable{};
+  }
 
   const size_t smem = zks::round_up((zks::kGuide + 2) * 2, 16) + size_t(zks::kWarps) * a.hist_words * 4;
   auto kernel = e->counters ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
@@ -297,6 +332,29 @@ int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_h
   ZKS_CUDA(cudaGetLastError());
   ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_engine_set_mle_mode(zks_engine* e, int mode) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  if (mode != ZKS_MLE_TABLE && mode != ZKS_MLE_DIRECT) return fail(ZKS_EINVAL, "unknown MLE mode %d", mode);
+  e->mle_mode = mode;
+  return ZKS_OK;
+}
+
+int zks_fit_eval(zks_engine* e, int32_t support_k, const double* x_dev, int64_t count, double* mu_dev,
+                 double* m2_dev, double* norm_dev) {
+  if (!e || !x_dev || !mu_dev || !m2_dev || !norm_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (support_k < 0 || support_k == 1 || support_k > 32766)
+    return fail(ZKS_EINVAL, "finite support bound must be in [2, 32766], got %d", support_k);
+  if (count <= 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  zks::FitTable* T = nullptr;
+  const int rc = fit_table_for(e, support_k, &T);
+  if (rc) return rc;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
+  zks::fit_eval_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(*T, x_dev, count, mu_dev, m2_dev, norm_dev);
+  ZKS_CUDA(cudaGetLastError());
   return ZKS_OK;
 }
 

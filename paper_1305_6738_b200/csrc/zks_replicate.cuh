@@ -15,6 +15,7 @@
 #pragma once
 #include <cstdint>
 
+#include "zks_fit.cuh"
 #include "zks_series.cuh"
 #include "zks_stream.cuh"
 
@@ -46,6 +47,8 @@ struct ReplicateArgs {
   int64_t slab_cap;
   unsigned long long* work;
   unsigned long long* counters;  // optional Work totals (kWorkFields), NULL = off
+  FitTable fit;                  // exponent-fit table of this support
+  int use_table;                 // 1: table-driven model functions, 0: direct sums
 };
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -146,18 +149,50 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
   return s;
 }
 
-__device__ __forceinline__ double model_mean(double x, int K, const double* logs, int lane, bool& ok, Work& wk) {
+// The model functions the estimator needs, from the fit table (default) or by direct
+// summation exactly as the reference forms them (validation mode).
+struct ModelFns {
+  int K;
+  const double* logs;
+  const FitTable* table;  // NULL = direct sums
+};
+
+__device__ __forceinline__ bool model_mean_slope(const ModelFns& M, double x, int lane, double& mean, double& slope,
+                                                 Work& wk) {
+  if (M.table) {
+    ++wk.evals;
+    fit_mean_slope(*M.table, x, mean, slope);
+    return true;
+  }
   Moments m;
-  ok = log_moments(x, K, logs, lane, m, wk);
+  if (!log_moments(x, M.K, M.logs, lane, m, wk)) return false;
+  mean = m.s1 / m.s0;
+  slope = m.s2 / m.s0 - mean * mean;
+  return true;
+}
+
+__device__ __forceinline__ double model_mean(const ModelFns& M, double x, int lane, bool& ok, Work& wk) {
+  if (M.table) {
+    ++wk.evals;
+    ok = true;
+    return fit_mean(*M.table, x);
+  }
+  Moments m;
+  ok = log_moments(x, M.K, M.logs, lane, m, wk);
   return m.s1 / m.s0;
 }
 
+__device__ __forceinline__ double model_norm(const ModelFns& M, double x, int lane, Work& wk) {
+  if (M.table) return fit_norm(*M.table, x);
+  return normaliser(x, M.K, M.logs, lane, wk);
+}
+
 // estimate.py:94-112
-__device__ bool bisect_root(double target, int K, const double* logs, int lane, double lo, double hi,
-                            double& root, Work& wk) {
+__device__ bool bisect_root(const ModelFns& M, double target, int lane, double lo, double hi, double& root,
+                            Work& wk) {
   bool ok1, ok2;
-  const double f_lo = target - model_mean(lo, K, logs, lane, ok1, wk);
-  const double f_hi = target - model_mean(hi, K, logs, lane, ok2, wk);
+  const double f_lo = target - model_mean(M, lo, lane, ok1, wk);
+  const double f_hi = target - model_mean(M, hi, lane, ok2, wk);
   if (!ok1 || !ok2) return false;
   if (f_lo == 0.0) {
     root = lo;
@@ -171,7 +206,7 @@ __device__ bool bisect_root(double target, int K, const double* logs, int lane, 
   while (hi - lo > 1e-8) {
     const double mid = 0.5 * (lo + hi);
     bool ok;
-    const double f = target - model_mean(mid, K, logs, lane, ok, wk);
+    const double f = target - model_mean(M, mid, lane, ok, wk);
     if (f * f_lo <= 0.0)
       hi = mid;
     else
@@ -182,28 +217,26 @@ __device__ bool bisect_root(double target, int K, const double* logs, int lane, 
 }
 
 // estimate.py:115-146 with DEFAULT_SETTINGS (x0 = 0.5, tol 1e-5, 200 iterations, [-20, 20])
-__device__ bool fit_exponent(double target, int K, const double* logs, int lane, double& g, Work& wk) {
+__device__ bool fit_exponent(const ModelFns& M, double target, int lane, double& g, Work& wk) {
   double lo = -20.0, hi = 20.0;
-  if (K == 0) {
+  if (M.K == 0) {
     lo = kMinUnboundedGamma;
     hi = kMaxUnboundedGamma;
   }
   double x = 0.5;
   if (!(lo < x && x < hi)) x = lo + 0.01;
   for (int it = 0; it < 200; ++it) {
-    Moments m;
-    if (!log_moments(x, K, logs, lane, m, wk)) return false;
-    const double mean = m.s1 / m.s0;
-    const double slope = m.s2 / m.s0 - mean * mean;
+    double mean, slope;
+    if (!model_mean_slope(M, x, lane, mean, slope, wk)) return false;
     const double x_new = x + (mean - target) / slope;
-    if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(target, K, logs, lane, lo, hi, g, wk);
+    if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(M, target, lane, lo, hi, g, wk);
     if (fabs(x_new - x) <= 1e-5) {
       g = x_new;
       return true;
     }
     x = x_new;
   }
-  return bisect_root(target, K, logs, lane, lo, hi, g, wk);
+  return bisect_root(M, target, lane, lo, hi, g, wk);
 }
 
 // Upper bound of sum_{k>=s} k^-g (s >= 2, g > 1): s^-g + s^(1-g)/(g-1).
@@ -304,7 +337,7 @@ __device__ __forceinline__ void clear_hist(uint32_t* hist, int words, int lane) 
 }
 
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up((kGuide + 2) * 2, 16);
@@ -318,6 +351,7 @@ __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
   const int K = a.K;
   const double dn = static_cast<double>(a.n);
   Work wk{0, 0, 0, 0, 0, 0, 0, 0};
+  const ModelFns M{K, a.logs, a.use_table ? &a.fit : nullptr};
 
   for (;;) {
     unsigned long long r = 0;
@@ -338,10 +372,10 @@ __global__ void __launch_bounds__(kThreads) replicate_kernel(ReplicateArgs a) {
       if (K > 0 && st.vmin == static_cast<uint32_t>(K))  // estimate.py:126-129
         target -= (log(static_cast<double>(K)) - log(static_cast<double>(K - 1))) / dn;
       double g = 0.0;
-      const bool ok = fit_exponent(target, K, a.logs, lane, g, wk);
+      const bool ok = fit_exponent(M, target, lane, g, wk);
       bool used_pages = false;
       if (ok) {
-        const double norm = normaliser(g, K, a.logs, lane, wk);
+        const double norm = model_norm(M, g, lane, wk);
         ks = ks_scan(a, g, norm, st, hist, slab, lane, used_pages, wk);
         gh = g;
         status = static_cast<uint8_t>(attempt);

@@ -157,6 +157,19 @@ class Engine:
         ptr = None if counters is None else ctypes.c_void_p(counters.data_ptr())
         _native.check(self.lib.zks_engine_set_counters(self.handle, ptr))
 
+    def set_mle_mode(self, direct: bool) -> None:
+        """Model moments by direct summation (validation) instead of the fit tables."""
+        _native.check(self.lib.zks_engine_set_mle_mode(self.handle, _native.MLE_DIRECT if direct else _native.MLE_TABLE))
+
+    def fit_eval(self, support_k: int | None, x):
+        """Fit-table values (mu, m2, norm) at device float64 points ``x``."""
+        torch = _torch()
+        mu, m2, nrm = (torch.empty_like(x) for _ in range(3))
+        self.bind_stream()
+        _native.check(self.lib.zks_fit_eval(self.handle, 0 if support_k is None else int(support_k), x.data_ptr(),
+                                            x.numel(), mu.data_ptr(), m2.data_ptr(), nrm.data_ptr()))
+        return mu, m2, nrm
+
     def probe_peaks(self) -> dict:
         """Measured pipe peaks of this device: DFMA FLOP/s, FP64 exp/s, 64-bit mulhilo/s."""
         out = (ctypes.c_double * 3)()

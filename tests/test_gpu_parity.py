@@ -100,7 +100,18 @@ def test_fixed_stream_known_answers(zk):
     assert zk.sample(zk.ZipfModel(1.7, zk.Support.finite(30)), 1, FixedStream([0.3])).observations.tolist() == [1]
 
 
-def test_replicates_match_reference_golden(zk, golden):
+@pytest.fixture(params=["table", "direct"])
+def mle_mode(request, zk):
+    """Run a test with the fit tables (default) and with direct model sums."""
+    from paper_1305_6738_b200.engine import get_engine
+
+    eng = get_engine()
+    eng.set_mle_mode(direct=request.param == "direct")
+    yield request.param
+    eng.set_mle_mode(direct=False)
+
+
+def test_replicates_match_reference_golden(zk, golden, mle_mode):
     for ci, K, gamma, n, seed, rep, count in golden_cells(golden):
         ks, gh, st = run_cell(K, gamma, n, seed, rep, 0, count)
         want_st = golden[f"cell{ci}_status"]
@@ -129,7 +140,7 @@ def test_replicates_match_reference_golden(zk, golden):
         (50, 4.0, 40, 12, 0, 600),
     ],
 )
-def test_replicates_match_oracle(zk, K, gamma, n, seed, rep, count):
+def test_replicates_match_oracle(zk, mle_mode, K, gamma, n, seed, rep, count):
     from oracle import port
 
     first = 1000
