@@ -1,0 +1,204 @@
+// Batched replicate kernel for small and moderate n (n <= kBatchVals / 4).
+//
+// Same per-replicate pipeline as replicate_kernel (montecarlo.py:89-116), re-phased so that no
+// phase is serial on a warp: a warp takes a batch of B consecutive replicate indices and
+//   1. derives the B stream keys lane-parallel (SeedSequence -> Philox key, one per lane);
+//   2. draws each replicate's sample warp-cooperatively into shared memory (u16 values),
+//      forming its log-sum / min / max on the way;
+//   3. runs the B Newton/bisection fits lane-parallel (one replicate per lane) on the fit
+//      tables, and the fitted normalisers;
+//   4. scores each replicate's KS statistic warp-cooperatively from its stored sample;
+//   5. retries the (rare) NoRootError replicates on stream idx + 2^32, warp-cooperatively.
+// B = min(32, kBatchVals / n): the sample store is 8 KB per warp.
+#pragma once
+#include "zks_replicate.cuh"
+
+namespace zks {
+
+constexpr int kBatchVals = 4096;  // u16 sample slots per warp
+
+struct DrawStats {
+  double log_sum;
+  uint32_t vmin, vmax;
+};
+
+// Draw the n values of stream key (k0, k1) into v[0..n) (warp-cooperative); warp-reduced stats.
+__device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
+                                                 const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
+  const int64_t n = a.n;
+  const int64_t nb = (n + 3) >> 2;
+  double ls = 0.0;
+  uint32_t mn = 0xffffffffu, mx = 0;
+  for (int64_t b = lane; b < nb; b += 32) {
+    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    uint32_t x[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      x[w] = 0;
+      if (4 * b + w < n) {
+        const uint32_t val = draw_value(uniform_open_closed(r.w[w]), guide, a.cdf, a.L);
+        ls += __ldg(a.logs + val);
+        mn = min(mn, val);
+        mx = max(mx, val);
+        x[w] = val;
+      }
+    }
+    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
+  }
+  DrawStats s;
+  s.log_sum = warp_sum(ls);
+  s.vmin = warp_min_u32(mn);
+  s.vmax = warp_max_u32(mx);
+  return s;
+}
+
+__device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int K, double dn) {
+  double t = log_sum;
+  if (t <= 0.0) t += kLn2;  // estimate.py:71-72
+  t /= dn;
+  if (K > 0 && vmin == static_cast<uint32_t>(K))  // estimate.py:126-129
+    t -= (log(static_cast<double>(K)) - log(static_cast<double>(K - 1))) / dn;
+  return t;
+}
+
+// KS of the stored sample v[0..n): histogram of 1..H, pages above H from v itself.
+__device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
+                                                 uint32_t* hist, const uint16_t* v, int lane, Work& wk) {
+  const int64_t n = a.n;
+  const uint32_t H = static_cast<uint32_t>(a.H);
+  for (int64_t i = 4 * lane; i < n; i += 128) {
+    const uint2 q = *reinterpret_cast<const uint2*>(v + i);
+    const uint32_t x[4] = {q.x & 0xffffu, q.x >> 16, q.y & 0xffffu, q.y >> 16};
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      if (i + w < n && x[w] <= H) atomicAdd(hist + x[w], 1u);
+  }
+  __syncwarp();
+  bool used_pages = false;
+  const double ks = ks_scan(a, g, norm, kmax, hist, v, static_cast<uint32_t>(n), lane, used_pages, wk);
+  const int top = used_pages ? a.hist_words : round_up(static_cast<int>(min(kmax, H)) + 1, 4);
+  clear_hist(hist, min(top, a.hist_words), lane);
+  return ks;
+}
+
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
+  const int guide_bytes = round_up((kGuide + 2) * 2, 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp_bytes = a.hist_words * 4 + kBatchVals * 2;
+  unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
+  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4);
+  for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
+  clear_hist(hist, a.hist_words, lane);
+  __syncthreads();
+
+  const int K = a.K;
+  const double dn = static_cast<double>(a.n);
+  const int B = a.batch;
+  const uint64_t nbatches = (a.count + B - 1) / B;
+  Work wk{0, 0, 0, 0, 0, 0, 0, 0};
+  const ModelFns M{K, a.logs, a.fit, true};
+
+  for (;;) {
+    unsigned long long bid = 0;
+    if (lane == 0) bid = atomicAdd(a.work, 1ull);
+    bid = __shfl_sync(0xffffffffu, bid, 0);
+    if (bid >= nbatches) break;
+    const uint64_t r0 = bid * B;
+    const uint64_t left = a.count - r0;
+    const int nrep = left < static_cast<uint64_t>(B) ? static_cast<int>(left) : B;
+    const bool active = lane < nrep;
+
+    // 1. stream keys, one replicate per lane
+    uint64_t k0 = 0, k1 = 0;
+    if (active) stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
+
+    // 2. samples into shared memory
+    double my_ls = 0.0;
+    uint32_t my_min = 0, my_max = 0;
+    for (int r = 0; r < nrep; ++r) {
+      const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
+      const DrawStats st = draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
+      if (lane == r) {
+        my_ls = st.log_sum;
+        my_min = st.vmin;
+        my_max = st.vmax;
+      }
+    }
+    __syncwarp();
+    if (kCount) {
+      wk.attempts += nrep;
+      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
+    }
+
+    // 3. exponent fits, one replicate per lane
+    double g = 0.0, norm = 1.0, target = 0.0;
+    bool ok = false;
+    Work lw{0, 0, 0, 0, 0, 0, 0, 0};
+    if (active) {
+      target = fit_target(my_ls, my_min, K, dn);
+      ok = fit_exponent(M, target, lane, g, lw);
+      if (ok) norm = fit_norm(a.fit, g);
+    }
+    if (kCount) {
+      unsigned long long e = lw.evals;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+      wk.evals += e;
+    }
+
+    // 4. KS statistics
+    double my_ks = __longlong_as_double(0x7ff8000000000000ll);
+    for (int r = 0; r < nrep; ++r) {
+      if (!__shfl_sync(0xffffffffu, ok, r)) continue;
+      const double gr = __shfl_sync(0xffffffffu, g, r);
+      const double nr = __shfl_sync(0xffffffffu, norm, r);
+      const uint32_t kmax = __shfl_sync(0xffffffffu, my_max, r);
+      const double ks = ks_from_sample(a, gr, nr, kmax, hist, vals + r * a.vals_stride, lane, wk);
+      if (lane == r) my_ks = ks;
+    }
+
+    // 5. retries on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative
+    uint8_t status = ok ? 0 : 2;
+    unsigned fails = __ballot_sync(0xffffffffu, active && !ok);
+    while (fails) {
+      const int r = __ffs(fails) - 1;
+      fails &= fails - 1;
+      uint64_t q0, q1;
+      stream_key(a.seed, a.rep, a.first + r0 + r + (1ull << 32), q0, q1);
+      uint16_t* v = vals + r * a.vals_stride;
+      const DrawStats st = draw_sample(a, q0, q1, guide, v, lane);
+      __syncwarp();
+      const double t2 = fit_target(st.log_sum, st.vmin, K, dn);
+      double g2 = 0.0;
+      const bool ok2 = fit_exponent(M, t2, lane, g2, wk);  // uniform: same inputs on every lane
+      double ks2 = __longlong_as_double(0x7ff8000000000000ll);
+      if (ok2) ks2 = ks_from_sample(a, g2, fit_norm(a.fit, g2), st.vmax, hist, v, lane, wk);
+      if (kCount) {
+        ++wk.attempts;
+        wk.draws += a.n;
+      }
+      if (lane == r) {
+        status = ok2 ? 1 : 2;
+        my_ks = ks2;
+        g = ok2 ? g2 : t2;  // failed twice: report the retry sample's mean log (diagnostics)
+      }
+    }
+
+    if (active) {
+      a.ks_out[r0 + lane] = my_ks;
+      a.gh_out[r0 + lane] = g;
+      a.st_out[r0 + lane] = status;
+    }
+  }
+  if (kCount && lane == 0) {
+    const unsigned long long* f = &wk.attempts;
+    for (int i = 0; i < kWorkFields; ++i)
+      if (f[i]) atomicAdd(a.counters + i, f[i]);
+  }
+}
+
+}  // namespace zks

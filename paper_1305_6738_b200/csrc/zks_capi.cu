@@ -10,6 +10,7 @@
 
 #include "../../include/zipfks_b200.h"
 #include "zks_replicate.cuh"
+#include "zks_batch.cuh"
 #include "zks_select.cuh"
 #include "zks_probe.cuh"
 
@@ -30,13 +31,16 @@ int fail(int code, const char* fmt, ...) {
 #define ZKS_CUDA(call)                                                                            \
   do {                                                                                            \
     cudaError_t e_ = (call);                                                                      \
-    if (e_ != cudaSuccess) return fail(ZKS_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(ZKS_ECUDA, "%s failed at zks_capi.cu:%d: %s", #call, __LINE__, cudaGetErrorString(e_)); \
   } while (0)
 
 constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
 constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
+constexpr int64_t kBatchMaxN = 1024;                  // n up to which replicate_batch_kernel runs
+constexpr uint32_t kBatchHist = 1024;                 // its per-warp histogram bins
 
 }  // namespace
 
@@ -51,8 +55,6 @@ struct zks_engine {
   size_t slab_bytes = 0;
   zks::SelectState* sel = nullptr;
   double* sel_out = nullptr;
-  int blocks_per_sm = 0;
-  size_t smem_bytes_cached = 0;
   // pinned staging ring: table uploads stay asynchronous w.r.t. queued kernels
   double* staging = nullptr;
   cudaEvent_t staging_done[kStagingSlots] = {};
@@ -60,6 +62,7 @@ struct zks_engine {
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
   int mle_mode = ZKS_MLE_TABLE;
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
+  std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
 };
 
 namespace {
@@ -166,8 +169,13 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   zks_table* t = new zks_table();
   t->engine = e;
   t->len = static_cast<uint32_t>(len);
-  cudaError_t err = cudaMalloc(&t->cdf, len * sizeof(double));
-  if (err == cudaSuccess) err = cudaMalloc(&t->guide, (zks::kGuide + 2) * sizeof(uint16_t));
+  // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
+  void* mem = nullptr;
+  cudaError_t err = cudaMallocAsync(&mem, len * sizeof(double) + (zks::kGuide + 2) * sizeof(uint16_t), e->stream);
+  if (err == cudaSuccess) {
+    t->cdf = static_cast<double*>(mem);
+    t->guide = reinterpret_cast<uint16_t*>(t->cdf + len);
+  }
   if (err == cudaSuccess) {
     // stage through a pinned slot so the copy never waits for kernels already queued
     const int slot = e->staging_next;
@@ -194,12 +202,10 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
 
 void zks_table_destroy(zks_table* t) {
   if (!t) return;
-  if (t->engine) {
+  if (t->engine && t->cdf) {
     cudaSetDevice(t->engine->device);
-    cudaStreamSynchronize(t->engine->stream);
+    cudaFreeAsync(t->cdf, t->engine->stream);  // ordered after every queued use of the table
   }
-  cudaFree(t->cdf);
-  cudaFree(t->guide);
   delete t;
 }
 
@@ -244,22 +250,48 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
     a.fit = zks::FitTable{};
   }
 
-  const size_t smem = zks::round_up((zks::kGuide + 2) * 2, 16) + size_t(zks::kWarps) * a.hist_words * 4;
-  auto kernel = e->counters ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
-  if (smem != e->smem_bytes_cached) {
-    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ZKS_CUDA(cudaFuncSetAttribute(zks::replicate_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zks::replicate_kernel<false>, zks::kThreads, smem));
-    if (per_sm < 1) return fail(ZKS_ECUDA, "replicate kernel does not fit (smem %zu)", smem);
-    e->blocks_per_sm = per_sm;
-    e->smem_bytes_cached = smem;
+  const bool counting = e->counters != nullptr;
+  const bool batched = a.use_table && c->n <= kBatchMaxN;
+  const size_t guide_bytes = zks::round_up((zks::kGuide + 2) * 2, 16);
+  void (*kernel)(zks::ReplicateArgs);
+  size_t smem;
+  int64_t per_block;  // replicates one block takes per work item round
+  if (batched) {
+    a.H = static_cast<int32_t>(std::min<uint32_t>(L, kBatchHist));
+    a.hist_words = zks::round_up(std::max(a.H, 4) + 1, 4);
+    a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
+    a.batch = std::min(32, zks::kBatchVals / a.vals_stride);
+    kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
+    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + zks::kBatchVals * 2);
+    per_block = int64_t(zks::kWarps) * a.batch;
+  } else {
+    a.batch = 1;
+    a.vals_stride = 0;
+    kernel = counting ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
+    smem = guide_bytes + size_t(zks::kWarps) * a.hist_words * 4;
+    per_block = zks::kWarps;
   }
-  int64_t blocks = int64_t(e->sms) * e->blocks_per_sm;
-  blocks = std::min<int64_t>(blocks, (int64_t)((c->count + zks::kWarps - 1) / zks::kWarps));
+  int per_sm = 0;
+  {
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), smem);
+    auto it = e->occupancy.find(key);
+    if (it == e->occupancy.end()) {
+      // one per-function ceiling for every launch size (the attribute is not per launch)
+      int optin = 0;
+      ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+      if (smem > size_t(optin)) return fail(ZKS_EINVAL, "replicate kernel needs %zu B of shared memory", smem);
+      ZKS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, zks::kThreads, smem));
+      if (per_sm < 1) return fail(ZKS_ECUDA, "replicate kernel does not fit (smem %zu)", smem);
+      it = e->occupancy.emplace(key, per_sm).first;
+    }
+    per_sm = it->second;
+  }
+  int64_t blocks = int64_t(e->sms) * per_sm;
+  blocks = std::min<int64_t>(blocks, (int64_t)((c->count + per_block - 1) / per_block));
   a.slab = nullptr;
   a.slab_cap = 0;
-  if (L > static_cast<uint32_t>(a.H)) {
+  if (!batched && L > static_cast<uint32_t>(a.H)) {
     // worst case every draw of a replicate lands above the histogram: capacity n per warp
     const size_t per_warp = size_t(c->n) * sizeof(uint16_t);
     int64_t max_blocks = int64_t(kSlabBudget / (per_warp * zks::kWarps));

@@ -49,6 +49,8 @@ struct ReplicateArgs {
   unsigned long long* counters;  // optional Work totals (kWorkFields), NULL = off
   FitTable fit;                  // exponent-fit table of this support
   int use_table;                 // 1: table-driven model functions, 0: direct sums
+  int batch;                     // replicates per warp batch (replicate_batch_kernel)
+  int vals_stride;               // u16 sample slots per replicate in the batch store
 };
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -154,14 +156,15 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
 struct ModelFns {
   int K;
   const double* logs;
-  const FitTable* table;  // NULL = direct sums
+  const FitTable& T;  // the kernel parameter's table (read through the constant bank)
+  bool table;         // false = direct sums
 };
 
 __device__ __forceinline__ bool model_mean_slope(const ModelFns& M, double x, int lane, double& mean, double& slope,
                                                  Work& wk) {
   if (M.table) {
     ++wk.evals;
-    fit_mean_slope(*M.table, x, mean, slope);
+    fit_mean_slope(M.T, x, mean, slope);
     return true;
   }
   Moments m;
@@ -175,7 +178,7 @@ __device__ __forceinline__ double model_mean(const ModelFns& M, double x, int la
   if (M.table) {
     ++wk.evals;
     ok = true;
-    return fit_mean(*M.table, x);
+    return fit_mean(M.T, x);
   }
   Moments m;
   ok = log_moments(x, M.K, M.logs, lane, m, wk);
@@ -183,7 +186,7 @@ __device__ __forceinline__ double model_mean(const ModelFns& M, double x, int la
 }
 
 __device__ __forceinline__ double model_norm(const ModelFns& M, double x, int lane, Work& wk) {
-  if (M.table) return fit_norm(*M.table, x);
+  if (M.table) return fit_norm(M.T, x);
   return normaliser(x, M.K, M.logs, lane, wk);
 }
 
@@ -295,11 +298,12 @@ __device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t 
   }
 }
 
-__device__ double ks_scan(const ReplicateArgs& a, double g, double norm, const SampleStats& st, uint32_t* hist,
-                          const uint16_t* slab, int lane, bool& used_pages, Work& wk) {
+// KS of one sample: counts of 1..H in `hist`; values above H are found in over_vals[0..over_n)
+// (which may also hold values <= H: they are ignored).
+__device__ double ks_scan(const ReplicateArgs& a, double g, double norm, uint32_t kmax, uint32_t* hist,
+                          const uint16_t* over_vals, uint32_t over_n, int lane, bool& used_pages, Work& wk) {
   const double inv = 1.0 / norm;
   const double dn = static_cast<double>(a.n);
-  const uint32_t kmax = st.vmax;
   const uint32_t H = static_cast<uint32_t>(a.H);
   const uint32_t dense_end = (a.K > 0) ? kmax : min(kmax, static_cast<uint32_t>(kSeam));
   KsState s{0.0, 0.0, 0u, 0.0, false};
@@ -313,8 +317,8 @@ __device__ double ks_scan(const ReplicateArgs& a, double g, double norm, const S
     for (int i = lane; i < a.hist_words; i += 32) hist[i] = 0u;
     __syncwarp();
     uint32_t next = 0xffffffffu;
-    for (uint32_t i = lane; i < st.over; i += 32) {
-      const uint32_t v = slab[i];
+    for (uint32_t i = lane; i < over_n; i += 32) {
+      const uint32_t v = over_vals[i];
       if (v >= pa && v <= pb)
         atomicAdd(hist + (v - pa), 1u);
       else if (v > pb)
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
   const int K = a.K;
   const double dn = static_cast<double>(a.n);
   Work wk{0, 0, 0, 0, 0, 0, 0, 0};
-  const ModelFns M{K, a.logs, a.use_table ? &a.fit : nullptr};
+  const ModelFns M{K, a.logs, a.fit, a.use_table != 0};
 
   for (;;) {
     unsigned long long r = 0;
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
       bool used_pages = false;
       if (ok) {
         const double norm = model_norm(M, g, lane, wk);
-        ks = ks_scan(a, g, norm, st, hist, slab, lane, used_pages, wk);
+        ks = ks_scan(a, g, norm, st.vmax, hist, slab, st.over, lane, used_pages, wk);
         gh = g;
         status = static_cast<uint8_t>(attempt);
       } else {
