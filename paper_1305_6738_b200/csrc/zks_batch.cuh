@@ -31,16 +31,17 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   uint32_t mn = 0xffffffffu, mx = 0;
   for (int64_t b = lane; b < nb; b += 32) {
     const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    bool vb[4];
     uint32_t x[4];
 #pragma unroll
+    for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
+    draw_block(r, vb, guide, a.cdf, a.L, x);
+#pragma unroll
     for (int w = 0; w < 4; ++w) {
-      x[w] = 0;
-      if (4 * b + w < n) {
-        const uint32_t val = draw_value(uniform_open_closed(r.w[w]), guide, a.cdf, a.L);
-        ls += __ldg(a.logs + val);
-        mn = min(mn, val);
-        mx = max(mx, val);
-        x[w] = val;
+      if (vb[w]) {
+        ls += __ldg(a.logs + x[w]);
+        mn = min(mn, x[w]);
+        mx = max(mx, x[w]);
       }
     }
     *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
@@ -63,7 +64,7 @@ __device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int 
 
 // KS of the stored sample v[0..n): histogram of 1..H, pages above H from v itself.
 __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
-                                                 uint32_t* hist, const uint16_t* v, int lane, Work& wk) {
+                                                 uint32_t* hist, uint32_t* queue, const uint16_t* v, int lane, Work& wk) {
   const int64_t n = a.n;
   const uint32_t H = static_cast<uint32_t>(a.H);
   for (int64_t i = 4 * lane; i < n; i += 128) {
@@ -75,7 +76,7 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
   }
   __syncwarp();
   bool used_pages = false;
-  const double ks = ks_scan(a, g, norm, kmax, hist, v, static_cast<uint32_t>(n), lane, used_pages, wk);
+  const double ks = ks_scan(a, g, norm, kmax, hist, v, static_cast<uint32_t>(n), queue, lane, used_pages, wk);
   const int top = used_pages ? a.hist_words : round_up(static_cast<int>(min(kmax, H)) + 1, 4);
   clear_hist(hist, min(top, a.hist_words), lane);
   return ks;
@@ -87,10 +88,11 @@ __global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateA
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up((kGuide + 2) * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int warp_bytes = a.hist_words * 4 + kBatchVals * 2;
+  const int warp_bytes = a.hist_words * 4 + 3 * kKsQueue * 4 + kBatchVals * 2;
   unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
-  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4);
+  uint32_t* queue = hist + a.hist_words;
+  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
   for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateA
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, my_max, r);
-      const double ks = ks_from_sample(a, gr, nr, kmax, hist, vals + r * a.vals_stride, lane, wk);
+      const double ks = ks_from_sample(a, gr, nr, kmax, hist, queue, vals + r * a.vals_stride, lane, wk);
       if (lane == r) my_ks = ks;
     }
 
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateA
       double g2 = 0.0;
       const bool ok2 = fit_exponent(M, t2, lane, g2, wk);  // uniform: same inputs on every lane
       double ks2 = __longlong_as_double(0x7ff8000000000000ll);
-      if (ok2) ks2 = ks_from_sample(a, g2, fit_norm(a.fit, g2), st.vmax, hist, v, lane, wk);
+      if (ok2) ks2 = ks_from_sample(a, g2, fit_norm(a.fit, g2), st.vmax, hist, queue, v, lane, wk);
       if (kCount) {
         ++wk.attempts;
         wk.draws += a.n;

@@ -262,13 +262,13 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
     a.batch = std::min(32, zks::kBatchVals / a.vals_stride);
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + zks::kBatchVals * 2);
+    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + 3 * zks::kKsQueue * 4 + zks::kBatchVals * 2);
     per_block = int64_t(zks::kWarps) * a.batch;
   } else {
     a.batch = 1;
     a.vals_stride = 0;
     kernel = counting ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * a.hist_words * 4;
+    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words + 3 * zks::kKsQueue) * 4;
     per_block = zks::kWarps;
   }
   int per_sm = 0;

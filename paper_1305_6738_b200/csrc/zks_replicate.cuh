@@ -71,6 +71,46 @@ __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restr
   return v > L ? L : v;
 }
 
+// The four draws of one Philox block, their lower_bound searches interleaved so that up to four
+// independent cdf loads are in flight per lane.  Lanes with valid[w] false yield 0.
+__device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
+                                           const double* __restrict__ cdf, uint32_t L, uint32_t out[4]) {
+  double u[4];
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    u[w] = uniform_open_closed(r.w[w]);
+    const int j = static_cast<int>(u[w] * static_cast<double>(kGuide));
+    lo[w] = valid[w] ? guide[j] : 0u;
+    hi[w] = valid[w] ? guide[j + 1] : 0u;
+  }
+  for (;;) {
+    bool act[4];
+    uint32_t mid[4];
+    double cv[4];
+    bool any = false;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      act[w] = lo[w] < hi[w];
+      any |= act[w];
+      mid[w] = (lo[w] + hi[w]) >> 1;
+      cv[w] = act[w] ? __ldg(cdf + mid[w]) : 0.0;
+    }
+    if (!any) break;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (act[w]) {
+        if (cv[w] >= u[w])
+          hi[w] = mid[w];
+        else
+          lo[w] = mid[w] + 1;
+      }
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) out[w] = valid[w] ? min(lo[w] + 1, L) : 0u;
+}
+
 struct SampleStats {
   double log_sum;
   uint32_t vmin, vmax, over;
@@ -107,12 +147,16 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
   for (int64_t b0 = 0; b0 < nb; b0 += 32) {
     const int64_t b = b0 + lane;
     const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    bool vb[4];
+    uint32_t vv[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) vb[w] = (4 * b + w) < n;
+    draw_block(r, vb, guide, a.cdf, a.L, vv);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const bool valid = (4 * b + w) < n;
-      uint32_t v = 0;
+      const bool valid = vb[w];
+      const uint32_t v = vv[w];
       if (valid) {
-        v = draw_value(uniform_open_closed(r.w[w]), guide, a.cdf, a.L);
         vmin = min(vmin, v);
         vmax = max(vmax, v);
         c1 += (v == 1u);
@@ -242,78 +286,193 @@ __device__ bool fit_exponent(const ModelFns& M, double target, int lane, double&
   return bisect_root(M, target, lane, lo, hi, g, wk);
 }
 
-// Upper bound of sum_{k>=s} k^-g (s >= 2, g > 1): s^-g + s^(1-g)/(g-1).
-__device__ __forceinline__ double tail_upper(double g, double Ls) {
-  const double p = exp(-g * Ls);
-  return p + p * exp(Ls) / (g - 1.0);
-}
+// ---------------------------------------------------------------------------- KS statistic
+//
+// The reference scans F(k) - E(k) over every k = 1..kmax (gof.py:60-68), or, for an unbounded
+// fit with kmax > 4096, only the stretch endpoints v and v-1 of the observed values v, with
+// F from the cumulative table below the seam and an Euler-Maclaurin tail above it
+// (gof.py:71-105).  Both give the same supremum (E is constant between observations while F
+// rises, so each stretch attains its extremes at its ends).  Here:
+//   * head, k <= kKsHead: dense, F(k) = S(k) / norm with S the running sum of k^-g, exactly
+//     the reference's cumulative form;
+//   * k > kKsHead: endpoints only, S(v) = S(kKsHead) + EM(kKsHead+1 .. v) by Euler-Maclaurin
+//     through the third-derivative term (the order of series.tail_mass, series.py:141-160),
+//     S(v-1) = S(v) - v^-g.  Observed values are gathered tile by tile from the histogram
+//     into a per-warp queue and scored 32 at a time, so the exp work scales with the number of
+//     distinct values, not with kmax.
+// The scan stops once no later k can beat the current maximum:
+//   sup_{k' > k} |F(k') - E(k')| <= max(1 - E(k), 1 - F(k)).
+constexpr uint32_t kKsHead = 64;
+constexpr int kKsQueue = 64;  // per-warp endpoint queue entries
 
 struct KsState {
-  double Fb;       // fitted cdf through the last dense k
-  double F_seam;   // fitted cdf at min(kmax, 4096) (sparse endpoint 4097 - 1)
-  uint32_t Cb;     // observations <= last processed k
-  double D;        // lane-local running max gap
+  double S;       // running sum of k^-g through the last dense k
+  double S_head;  // S(min(kmax, kKsHead))
+  double Dw;      // warp max of D as of the last flush (warp-uniform)
+  uint32_t Cb;    // observations <= last processed k
+  double D;       // lane-local running max gap
   bool done;
+  uint32_t next_fcheck;  // no F-based exit test before this k
 };
 
-// KS over tiles of 32 consecutive k in [k_first, k_last]; counts[k - base].
-// Dense semantics (gof.py:60-68) for k <= dense_end, sparse endpoint semantics
-// (gof.py:71-105) above it.  Exits early once no later k can beat the current max.
-__device__ __forceinline__ void ks_tiles(KsState& s, uint32_t k_first, uint32_t k_last, const uint32_t* counts,
-                                         uint32_t base, uint32_t dense_end, double g, double norm, double inv,
-                                         double dn, const double* __restrict__ logs, int lane, Work& wk) {
+struct KsCtx {
+  double g, inv, inv_n;
+  double fa, a_pow, La;  // f(a) = a^-g, a^(1-g), ln a for a = kKsHead + 1
+  const double* logs;
+  uint32_t* qk;  // queue: value v
+  uint32_t* qc;  // queue: observations < v
+  uint32_t* qn;  // queue: observations == v
+};
+
+// S(v) - S(kKsHead) = sum_{k=a}^{v} k^-g, a = kKsHead + 1, by Euler-Maclaurin; also returns v^-g
+__device__ __forceinline__ double em_block(const KsCtx& c, uint32_t v, double& fv) {
+  const double Lv = __ldg(c.logs + v);
+  const double b = static_cast<double>(v);
+  const double a = static_cast<double>(kKsHead + 1);
+  fv = exp(-c.g * Lv);
+  const double om = 1.0 - c.g;
+  // integral_a^v x^-g dx = a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
+  const double integral = (om == 0.0) ? (Lv - c.La) : c.a_pow * expm1(om * (Lv - c.La)) / om;
+  const double d1 = -c.g * (fv / b - c.fa / a);  // f'(v) - f'(a)
+  const double g3 = c.g * (c.g + 1.0) * (c.g + 2.0);
+  const double d3 = -g3 * (fv / (b * b * b) - c.fa / (a * a * a));  // f'''(v) - f'''(a)
+  return integral + 0.5 * (c.fa + fv) + d1 / 12.0 - d3 / 720.0;
+}
+
+// score queue entries [0, cnt) lane-parallel (cnt <= 32)
+__device__ __forceinline__ void ks_flush(KsState& s, const KsCtx& c, int cnt, int lane, Work& wk) {
+  if (cnt <= 0) return;
+  double Fv = 0.0;
+  if (lane < cnt) {
+    const uint32_t v = c.qk[lane];
+    const uint32_t before = c.qc[lane];
+    const uint32_t here = c.qn[lane];
+    double fv;
+    const double Sv = s.S_head + em_block(c, v, fv);
+    Fv = Sv * c.inv;
+    const double Fp = (Sv - fv) * c.inv;
+    const double E = static_cast<double>(before + here) * c.inv_n;
+    const double Eb = static_cast<double>(before) * c.inv_n;
+    s.D = fmax(s.D, fmax(fabs(Fv - E), fabs(Fp - Eb)));
+  }
+  wk.ks_tails += cnt;
+}
+
+// exit test: every later gap is bounded by max(1 - E, 1 - F) at the scan position
+__device__ __forceinline__ void ks_check(KsState& s, double F_pos, double inv_n) {
+  const double Dw = warp_max(s.D);
+  const double bound = fmax(1.0 - static_cast<double>(s.Cb) * inv_n, 1.0 - F_pos);
+  if (Dw > bound + kKsMargin) s.done = true;
+}
+
+// Tiles of 32 consecutive k in [k_first, k_last] with counts[k - base], above the head.
+__device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int& q, uint32_t k_first,
+                                                uint32_t k_last, const uint32_t* counts, uint32_t base, int lane,
+                                                Work& wk) {
+  const unsigned lt = (1u << lane) - 1u;
   for (uint32_t k0 = k_first; k0 <= k_last && !s.done; k0 += 32) {
     ++wk.ks_tiles;
     const uint32_t k = k0 + lane;
     const bool in = k <= k_last;
-    const uint32_t c = in ? counts[k - base] : 0u;
-    const uint32_t C = s.Cb + warp_scan_u32(c, lane);
-    const double E = static_cast<double>(C) / dn;
-    const uint32_t k_hi = min(k0 + 31u, k_last);
-    double bound_f;
-    if (k0 <= dense_end) {
-      // tiles never straddle dense_end (tiles start at 1 mod 32 and the seam is 4096)
-      const double term = in ? exp(-g * __ldg(logs + k)) * inv : 0.0;
-      wk.ks_terms += min(32u, k_last - k0 + 1);
-      const double F = s.Fb + warp_scan(term, lane);
-      if (in) s.D = fmax(s.D, fabs(F - E));
-      s.Fb = __shfl_sync(0xffffffffu, F, 31);
-      if (k_hi == dense_end) s.F_seam = s.Fb;
-      bound_f = 1.0 - s.Fb;
-    } else {
-      if (in && c) {
-        const double Fv = (norm - tail_sum(g, __ldg(logs + k + 1))) / norm;
-        const double Fp = (k - 1 <= static_cast<uint32_t>(kSeam)) ? s.F_seam
-                                                                    : (norm - tail_sum(g, __ldg(logs + k))) / norm;
-        const double Eb = static_cast<double>(C - c) / dn;
-        s.D = fmax(s.D, fmax(fabs(Fv - E), fabs(Fp - Eb)));
-      }
-      wk.ks_tails += __popc(__ballot_sync(0xffffffffu, in && c));
-      bound_f = tail_upper(g, __ldg(logs + k_hi + 1)) * inv;
+    const uint32_t cnt = in ? counts[k - base] : 0u;
+    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
+    const unsigned nz = __ballot_sync(0xffffffffu, cnt != 0u);
+    if (cnt) {
+      const int slot = q + __popc(nz & lt);
+      c.qk[slot] = k;
+      c.qc[slot] = C - cnt;
+      c.qn[slot] = cnt;
     }
+    q += __popc(nz);
     s.Cb = __shfl_sync(0xffffffffu, C, 31);
-    const double Dw = warp_max(s.D);
-    const double bound = fmax(1.0 - static_cast<double>(s.Cb) / dn, bound_f);
-    if (Dw > bound + kKsMargin) s.done = true;
+    __syncwarp();
+    if (q >= 32) {
+      ks_flush(s, c, 32, lane, wk);
+      __syncwarp();
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+      if (lane < q - 32) {
+        a0 = c.qk[32 + lane];
+        a1 = c.qc[32 + lane];
+        a2 = c.qn[32 + lane];
+      }
+      __syncwarp();
+      if (lane < q - 32) {
+        c.qk[lane] = a0;
+        c.qc[lane] = a1;
+        c.qn[lane] = a2;
+      }
+      q -= 32;
+      __syncwarp();
+      s.Dw = warp_max(s.D);
+    }
+    // exit test, only once the empirical part of the bound allows it (D changes only at flushes)
+    const uint32_t k_hi = min(k0 + 31u, k_last);
+    // (F checks back off geometrically in k: heavy tails make F approach 1 slowly)
+    if (k_hi >= s.next_fcheck && s.Dw > 1.0 - static_cast<double>(s.Cb) * c.inv_n + kKsMargin) {
+      ks_flush(s, c, q, lane, wk);
+      q = 0;
+      __syncwarp();
+      s.Dw = warp_max(s.D);
+      double fk;
+      const double F_pos = (s.S_head + em_block(c, k_hi, fk)) * c.inv;
+      ++wk.ks_tails;
+      if (s.Dw > fmax(1.0 - static_cast<double>(s.Cb) * c.inv_n, 1.0 - F_pos) + kKsMargin)
+        s.done = true;
+      else
+        s.next_fcheck = 2 * k_hi - kKsHead;
+    }
   }
 }
 
 // KS of one sample: counts of 1..H in `hist`; values above H are found in over_vals[0..over_n)
-// (which may also hold values <= H: they are ignored).
+// (which may also hold values <= H: they are ignored).  `queue` is 3 * kKsQueue u32 of
+// per-warp shared memory.
 __device__ double ks_scan(const ReplicateArgs& a, double g, double norm, uint32_t kmax, uint32_t* hist,
-                          const uint16_t* over_vals, uint32_t over_n, int lane, bool& used_pages, Work& wk) {
-  const double inv = 1.0 / norm;
-  const double dn = static_cast<double>(a.n);
+                          const uint16_t* over_vals, uint32_t over_n, uint32_t* queue, int lane, bool& used_pages,
+                          Work& wk) {
+  KsCtx c;
+  c.g = g;
+  c.inv = 1.0 / norm;
+  c.inv_n = 1.0 / static_cast<double>(a.n);
+  c.logs = a.logs;
+  c.qk = queue;
+  c.qc = queue + kKsQueue;
+  c.qn = queue + 2 * kKsQueue;
   const uint32_t H = static_cast<uint32_t>(a.H);
-  const uint32_t dense_end = (a.K > 0) ? kmax : min(kmax, static_cast<uint32_t>(kSeam));
-  KsState s{0.0, 0.0, 0u, 0.0, false};
-  ks_tiles(s, 1u, min(kmax, H), hist, 0u, dense_end, g, norm, inv, dn, a.logs, lane, wk);
+  KsState s{0.0, 0.0, 0.0, 0u, 0.0, false, 0u};  // S, S_head, Dw, Cb, D, done, next_fcheck
   used_pages = false;
+
+  // head: dense, exactly the reference's cumulative form
+  const uint32_t head_end = min(kmax, kKsHead);
+  for (uint32_t k0 = 1; k0 <= head_end && !s.done; k0 += 32) {
+    ++wk.ks_tiles;
+    const uint32_t k = k0 + lane;
+    const bool in = k <= head_end;
+    const uint32_t cnt = in ? hist[k] : 0u;
+    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
+    const double term = in ? exp(-g * __ldg(a.logs + k)) : 0.0;
+    const double S = s.S + warp_scan(term, lane);
+    if (in) s.D = fmax(s.D, fabs(S * c.inv - static_cast<double>(C) * c.inv_n));
+    s.S = __shfl_sync(0xffffffffu, S, 31);
+    s.Cb = __shfl_sync(0xffffffffu, C, 31);
+    wk.ks_terms += min(32u, head_end - k0 + 1);
+    ks_check(s, s.S * c.inv, c.inv_n);
+  }
+  if (s.done || kmax <= kKsHead) return warp_max(s.D);
+  s.S_head = s.S;
+  s.Dw = warp_max(s.D);
+  c.La = __ldg(a.logs + kKsHead + 1);
+  c.fa = exp(-g * c.La);
+  c.a_pow = static_cast<double>(kKsHead + 1) * c.fa;
+
+  // above the head: endpoints of the observed values
+  int q = 0;
+  ks_sparse_tiles(s, c, q, kKsHead + 1, min(kmax, H), hist, 0u, lane, wk);
   uint32_t pa = H + 1;
   while (!s.done && pa <= kmax) {
     used_pages = true;
     const uint32_t pb = min(pa + H - 1, kmax);
-    // page histogram of the overflow values in [pa, pb]; next occupied value above pb
+    // page histogram of the values in [pa, pb]; next occupied value above pb
     for (int i = lane; i < a.hist_words; i += 32) hist[i] = 0u;
     __syncwarp();
     uint32_t next = 0xffffffffu;
@@ -326,11 +485,11 @@ __device__ double ks_scan(const ReplicateArgs& a, double g, double norm, uint32_
     }
     next = warp_min_u32(next);
     __syncwarp();
-    ks_tiles(s, pa, pb, hist, pa, dense_end, g, norm, inv, dn, a.logs, lane, wk);
+    ks_sparse_tiles(s, c, q, pa, pb, hist, pa, lane, wk);
     pa = pb + 1;
-    // sparse region: pages without observations carry no endpoints; jump to the next value
-    if (pa > dense_end && next != 0xffffffffu && next > pa) pa = next;
+    if (next != 0xffffffffu && next > pa) pa = next;  // no observations in between: no endpoints
   }
+  ks_flush(s, c, q, lane, wk);
   return warp_max(s.D);
 }
 
@@ -346,7 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up((kGuide + 2) * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * a.hist_words;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * (a.hist_words + 3 * kKsQueue);
+  uint32_t* queue = hist + a.hist_words;
   for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
@@ -380,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
       bool used_pages = false;
       if (ok) {
         const double norm = model_norm(M, g, lane, wk);
-        ks = ks_scan(a, g, norm, st.vmax, hist, slab, st.over, lane, used_pages, wk);
+        ks = ks_scan(a, g, norm, st.vmax, hist, slab, st.over, queue, lane, used_pages, wk);
         gh = g;
         status = static_cast<uint8_t>(attempt);
       } else {
