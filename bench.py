@@ -266,6 +266,13 @@ def run_b200(args, world, rank, local):
                 "unit": "Tmul64/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+        roof["traffic"] = tr["dram_bytes_read_per_launch"] + tr["dram_bytes_write_per_launch"]
+        roof["traffic_source"] = tr["source"]
+    except (OSError, KeyError, ValueError):
+        pass
     roof["peak_source"] = "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)"
     roof["work_per_sweep"] = {"replicates": ncells * (R if world == 1 else shard[1] - shard[0]),
                               "attempts": attempts, "draws": draws, "moment_evals": evals,
