@@ -25,11 +25,11 @@ struct DrawStats {
 // Draw the n values of stream key (k0, k1) into v[0..n) (warp-cooperative); warp-reduced stats.
 __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
                                                  const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
-  const int64_t n = a.n;
-  const int64_t nb = (n + 3) >> 2;
+  const int n = static_cast<int>(a.n);  // batch kernel: n <= kBatchVals
+  const int nb = (n + 3) >> 2;
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0;
-  for (int64_t b = lane; b < nb; b += 32) {
+  for (int b = lane; b < nb; b += 32) {
     const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
     bool vb[4];
     uint32_t x[4];
@@ -65,14 +65,28 @@ __device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int 
 // KS of the stored sample v[0..n): histogram of 1..H, pages above H from v itself.
 __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
                                                  uint32_t* hist, uint32_t* queue, const uint16_t* v, int lane, Work& wk) {
-  const int64_t n = a.n;
+  const int n = static_cast<int>(a.n);
   const uint32_t H = static_cast<uint32_t>(a.H);
-  for (int64_t i = 4 * lane; i < n; i += 128) {
+  // values 1 and 2 (most of the mass for gamma >~ 1.5) are counted in registers: a shared
+  // atomic on one bin from 32 lanes would serialise
+  uint32_t c1 = 0, c2 = 0;
+  for (int i = 4 * lane; i < n; i += 128) {
     const uint2 q = *reinterpret_cast<const uint2*>(v + i);
     const uint32_t x[4] = {q.x & 0xffffu, q.x >> 16, q.y & 0xffffu, q.y >> 16};
 #pragma unroll
-    for (int w = 0; w < 4; ++w)
-      if (i + w < n && x[w] <= H) atomicAdd(hist + x[w], 1u);
+    for (int w = 0; w < 4; ++w) {
+      if (i + w < n) {
+        c1 += x[w] == 1u;
+        c2 += x[w] == 2u;
+        if (x[w] > 2u && x[w] <= H) atomicAdd(hist + x[w], 1u);
+      }
+    }
+  }
+  c1 = warp_sum_u32(c1);
+  c2 = warp_sum_u32(c2);
+  if (lane == 0) {
+    hist[1] = c1;
+    if (H >= 2) hist[2] = c2;
   }
   __syncwarp();
   bool used_pages = false;
