@@ -107,6 +107,48 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * table length (sample, distribution.py:190-201).  Asynchronous. */
 int zks_draw(zks_engine* engine, const zks_table* table, const double* u_dev, int64_t count, int64_t* out_dev);
 
+/* ---- user samples (fit --bespoke, batched dataset fitting) --------------------- */
+
+#define ZKS_FIT_EXPONENT 1  /* estimate the exponent (mle_gamma)                            */
+#define ZKS_FIT_KS 2        /* score the KS statistic (against the fit, or gamma_in)         */
+
+#define ZKS_SAMPLE_OK 0
+#define ZKS_SAMPLE_NOROOT 2   /* NoRootError (estimate.py:101-105)                         */
+#define ZKS_SAMPLE_OUTSIDE 3  /* an observation outside the support (or >= 2^32)           */
+#define ZKS_SAMPLE_EMPTY 4
+
+/* MleSettings (estimate.py:24-47). */
+typedef struct {
+  double initial_guess;
+  double absolute_tolerance;
+  int32_t max_iterations;
+  int32_t reserved;
+  double bracket_lo, bracket_hi;
+} zks_mle_settings;
+
+/* For each sample i = values_dev[offsets_dev[i] .. offsets_dev[i+1]) (positive int64): its
+ * log_mean (estimate.py:59-73), with ZKS_FIT_EXPONENT its mle_gamma (estimate.py:115-146;
+ * settings NULL = DEFAULT_SETTINGS), with ZKS_FIT_KS its ks_statistic and argmax_k
+ * (gof.py:49-105) against the fitted exponent or, without ZKS_FIT_EXPONENT, against
+ * gamma_in_dev[i] with normaliser norm_in_dev[i] (NULL: summed on the device).  Replaces the
+ * per-sample calls of cli._cmd_fit (cli.py:197-262).  Asynchronous. */
+int zks_fit_samples(zks_engine* engine, int32_t support_k, const int64_t* values_dev, const int64_t* offsets_dev,
+                    int64_t nsamples, int32_t mode, const zks_mle_settings* settings, const double* gamma_in_dev,
+                    const double* norm_in_dev, double* log_mean_dev, double* gamma_dev, double* ks_dev,
+                    int64_t* argmax_dev, uint8_t* status_dev);
+
+/* Reference series at gamma_dev[i]: out_dev[4i..4i+4) = (s0, s1, s2, normaliser) with
+ * s_p = sum k^-g (ln k)^p over 1..K (finite_log_moments, series.py:68-73) or the zeta series
+ * with its Euler-Maclaurin tail and m-doubling rule (zeta_log_moments, series.py:102-123),
+ * normaliser = normalization (distribution.py:71-85).  NaN where the series diverges. */
+int zks_series_eval(zks_engine* engine, int32_t support_k, const double* gamma_dev, int64_t count, double* out_dev);
+
+/* The exponent for given mean-log targets: Newton/bisection as mle_gamma, or with bisect_only
+ * the bisection of _bisect (estimate.py:94-112) on [bracket_lo, bracket_hi].  status 2 =
+ * NoRootError.  Asynchronous. */
+int zks_solve_exponents(zks_engine* engine, int32_t support_k, const double* target_dev, int64_t count,
+                        const zks_mle_settings* settings, int32_t bisect_only, double* gamma_dev, uint8_t* status_dev);
+
 /* ---- diagnostics (bench.py roofline, parity tests; not part of the reference interface) --- */
 
 /* How the replicate kernel evaluates the model functions of the exponent fit

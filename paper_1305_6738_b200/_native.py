@@ -31,11 +31,29 @@ EXPORTS = (
     "zks_normaliser",
     "zks_stream_uniforms",
     "zks_draw",
+    "zks_fit_samples",
+    "zks_series_eval",
+    "zks_solve_exponents",
     "zks_engine_set_mle_mode",
     "zks_fit_eval",
     "zks_engine_set_counters",
     "zks_probe_peaks",
 )
+
+
+FIT_EXPONENT, FIT_KS = 1, 2
+SAMPLE_OK, SAMPLE_NOROOT, SAMPLE_OUTSIDE, SAMPLE_EMPTY = 0, 2, 3, 4
+
+
+class ZksMleSettings(ctypes.Structure):
+    _fields_ = [
+        ("initial_guess", ctypes.c_double),
+        ("absolute_tolerance", ctypes.c_double),
+        ("max_iterations", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("bracket_lo", ctypes.c_double),
+        ("bracket_hi", ctypes.c_double),
+    ]
 
 
 class ZksCell(ctypes.Structure):
@@ -83,6 +101,10 @@ def load() -> ctypes.CDLL:
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]
     lib.zks_engine_set_counters.argtypes = [vp, dp]
+    lib.zks_fit_samples.argtypes = [vp, i32, dp, dp, i64, i32, ctypes.POINTER(ZksMleSettings), dp, dp, dp, dp, dp, dp,
+                                    dp]
+    lib.zks_series_eval.argtypes = [vp, i32, dp, i64, dp]
+    lib.zks_solve_exponents.argtypes = [vp, i32, dp, i64, ctypes.POINTER(ZksMleSettings), i32, dp, dp]
     lib.zks_engine_set_mle_mode.argtypes = [vp, ctypes.c_int]
     lib.zks_fit_eval.argtypes = [vp, i32, dp, i64, dp, dp, dp]
     lib.zks_probe_peaks.argtypes = [vp, dp]

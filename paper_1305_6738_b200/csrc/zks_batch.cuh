@@ -89,11 +89,10 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
     if (H >= 2) hist[2] = c2;
   }
   __syncwarp();
-  bool used_pages = false;
-  const double ks = ks_scan(a, g, norm, kmax, hist, v, static_cast<uint32_t>(n), queue, lane, used_pages, wk);
-  const int top = used_pages ? a.hist_words : round_up(static_cast<int>(min(kmax, H)) + 1, 4);
+  const KsOut ko = ks_scan<uint16_t, false>(ks_params(a), g, norm, kmax, hist, v, static_cast<uint32_t>(n), queue, lane, wk);
+  const int top = ko.used_pages ? a.hist_words : round_up(static_cast<int>(min(kmax, H)) + 1, 4);
   clear_hist(hist, min(top, a.hist_words), lane);
-  return ks;
+  return ko.D;
 }
 
 template <bool kCount>

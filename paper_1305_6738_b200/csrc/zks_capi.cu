@@ -11,6 +11,7 @@
 #include "../../include/zipfks_b200.h"
 #include "zks_replicate.cuh"
 #include "zks_batch.cuh"
+#include "zks_samples.cuh"
 #include "zks_select.cuh"
 #include "zks_probe.cuh"
 
@@ -421,6 +422,103 @@ int zks_draw(zks_engine* e, const zks_table* t, const double* u_dev, int64_t cou
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (count + 255) / 256));
   zks::draw_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(t->cdf, t->guide, t->len, u_dev, count, out_dev);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+zks::MleParams mle_params(const zks_mle_settings* s) {
+  zks::MleParams P;
+  if (s) {
+    P.x0 = s->initial_guess;
+    P.tol = s->absolute_tolerance;
+    P.max_iter = s->max_iterations;
+    P.lo = s->bracket_lo;
+    P.hi = s->bracket_hi;
+  }
+  return P;
+}
+
+int check_support(int32_t k) {
+  if (k < 0 || k == 1 || k > 32766) return fail(ZKS_EINVAL, "finite support bound must be in [2, 32766], got %d", k);
+  return ZKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int zks_fit_samples(zks_engine* e, int32_t support_k, const int64_t* values_dev, const int64_t* offsets_dev,
+                    int64_t nsamples, int32_t mode, const zks_mle_settings* settings, const double* gamma_in_dev,
+                    const double* norm_in_dev, double* log_mean_dev, double* gamma_dev, double* ks_dev,
+                    int64_t* argmax_dev, uint8_t* status_dev) {
+  if (!e || !offsets_dev || !log_mean_dev || !gamma_dev || !ks_dev || !argmax_dev || !status_dev)
+    return fail(ZKS_EINVAL, "NULL argument");
+  if (int rc = check_support(support_k)) return rc;
+  if (nsamples < 0) return fail(ZKS_EINVAL, "nsamples must be >= 0");
+  if (!(mode & ZKS_FIT_EXPONENT) && (mode & ZKS_FIT_KS) && !gamma_in_dev)
+    return fail(ZKS_EINVAL, "scoring without a fit needs the model exponents");
+  const zks::MleParams P = mle_params(settings);
+  if (settings && (P.tol <= 0.0 || P.max_iter < 1 || !(P.lo < P.x0 && P.x0 < P.hi)))
+    return fail(ZKS_EINVAL, "invalid MLE settings");
+  if (nsamples == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  zks::SamplesArgs a{};
+  a.values = values_dev;
+  a.offsets = offsets_dev;
+  a.nsamples = nsamples;
+  a.K = support_k;
+  a.logs = e->logs;
+  a.mle = P;
+  a.mode = mode;
+  a.gamma_in = gamma_in_dev;
+  a.norm_in = norm_in_dev;
+  a.log_mean_out = log_mean_dev;
+  a.gamma_out = gamma_dev;
+  a.ks_out = ks_dev;
+  a.argmax_out = argmax_dev;
+  a.status_out = status_dev;
+  a.hist_words = zks::round_up(zks::kSamplesHist + 1, 4);
+  a.work = e->work;
+  // the fit tables cover [-20, 20] (finite) and [1.05, 20] (unbounded): wider brackets sum directly
+  a.use_table = e->mle_mode == ZKS_MLE_TABLE && (support_k == 0 || (P.lo >= -20.0 && P.hi <= 20.0));
+  if (a.use_table) {
+    zks::FitTable* T = nullptr;
+    if (int rc = fit_table_for(e, support_k, &T)) return rc;
+    a.fit = *T;
+  }
+  const size_t smem = size_t(zks::kWarps) * (a.hist_words + zks::kKsQueueWords) * 4;
+  ZKS_CUDA(cudaFuncSetAttribute(zks::samples_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (nsamples + zks::kWarps - 1) / zks::kWarps));
+  ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+  zks::samples_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+int zks_series_eval(zks_engine* e, int32_t support_k, const double* gamma_dev, int64_t count, double* out_dev) {
+  if (!e || !gamma_dev || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (int rc = check_support(support_k)) return rc;
+  if (count <= 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t blocks = (count * 32 + 255) / 256;
+  zks::series_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(gamma_dev, count, support_k, e->logs, out_dev);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+int zks_solve_exponents(zks_engine* e, int32_t support_k, const double* target_dev, int64_t count,
+                        const zks_mle_settings* settings, int32_t bisect_only, double* gamma_dev, uint8_t* status_dev) {
+  if (!e || !target_dev || !gamma_dev || !status_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (int rc = check_support(support_k)) return rc;
+  if (count <= 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t blocks = (count * 32 + 255) / 256;
+  zks::solve_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(target_dev, count, support_k, e->logs, mle_params(settings),
+                                                             bisect_only, gamma_dev, status_dev);
   ZKS_CUDA(cudaGetLastError());
   return ZKS_OK;
 }

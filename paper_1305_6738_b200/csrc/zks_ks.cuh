@@ -1,0 +1,301 @@
+// KS statistic of one sample, warp-cooperative (gof.py:49-105).
+//
+// The reference scans F(k) - E(k) over every k = 1..kmax (gof.py:60-68), or, for an unbounded
+// fit with kmax > 4096, only the stretch endpoints v and v-1 of the observed values v, with
+// F from the cumulative table below the seam and an Euler-Maclaurin tail above it
+// (gof.py:71-105).  Both give the same supremum (E is constant between observations while F
+// rises, so each stretch attains its extremes at its ends).  Here:
+//   * head, k <= kKsHead: dense, F(k) = S(k) / norm with S the running sum of k^-g, the
+//     reference's cumulative form;
+//   * k > kKsHead: endpoints only, S(v) = S(kKsHead) + EM(kKsHead+1 .. v) by Euler-Maclaurin
+//     through the third-derivative term (the order of series.tail_mass, series.py:141-160),
+//     S(v-1) = S(v) - v^-g.  Observed values are gathered tile by tile from the histogram
+//     into a per-warp queue and scored 32 at a time, so the exp work scales with the number of
+//     distinct values, not with kmax.
+// The scan stops once no later k can beat the current maximum:
+//   sup_{k' > k} |F(k') - E(k')| <= max(1 - E(k), 1 - F(k)).
+// kArg also tracks the smallest k attaining the maximum (KsResult.argmax_k); exact mode forms
+// E(k) = C(k) / n and the head F(k) as the running sum of (k^-g * (1/norm)), as the reference
+// writes them, so trivial samples reproduce the reference's exact values (0, 2/3, ...).
+#pragma once
+#include <cstdint>
+
+#include "zks_series.cuh"
+
+namespace zks {
+
+constexpr uint32_t kKsHead = 64;
+constexpr int kKsQueue = 64;         // per-warp endpoint queue entries
+constexpr int kKsQueueWords = 3 * kKsQueue;
+constexpr double kKsMargin = 1e-11;  // early-exit safety margin (>> fp64 rounding of the sums)
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+struct KsParams {
+  int64_t n;
+  uint32_t H;          // histogram bins held in `hist` (values 1..H)
+  int hist_words;      // words of `hist` (>= H + 1, multiple of 4)
+  const double* logs;  // ln k, k = 0..65536
+  bool exact;          // reference-exact forms (user-sample API)
+};
+
+struct KsOut {
+  double D;
+  uint32_t argk;
+  bool used_pages;
+};
+
+struct KsState {
+  double S;       // running sum of k^-g through the last dense k
+  double F;       // exact mode: running sum of k^-g / norm
+  double S_head;  // S(min(kmax, kKsHead))
+  double Dw;      // warp max of D as of the last flush (warp-uniform)
+  uint32_t Cb;    // observations <= last processed k
+  double D;       // lane-local running max gap
+  uint32_t kb;    // lane-local smallest k attaining D (kArg)
+  bool done;
+  uint64_t next_fcheck;  // no F-based exit test before this k
+};
+
+struct KsCtx {
+  double g, inv, inv_n, dn;
+  double fa, a_pow, La;  // f(a) = a^-g, a^(1-g), ln a for a = kKsHead + 1
+  bool exact;
+  const double* logs;
+  uint32_t* qk;  // queue: value v
+  uint32_t* qc;  // queue: observations < v
+  uint32_t* qn;  // queue: observations == v
+};
+
+__device__ __forceinline__ double ln_of(const double* logs, uint64_t v) {
+  return v <= 65536u ? __ldg(logs + v) : log(static_cast<double>(v));
+}
+
+__device__ __forceinline__ double emp(const KsCtx& c, uint32_t C) {
+  return c.exact ? static_cast<double>(C) / c.dn : static_cast<double>(C) * c.inv_n;
+}
+
+template <bool kArg>
+__device__ __forceinline__ void take(KsState& s, double gap, uint32_t k) {
+  if (kArg) {
+    if (gap > s.D) {
+      s.D = gap;
+      s.kb = k;
+    }
+  } else {
+    s.D = fmax(s.D, gap);
+  }
+}
+
+// S(v) - S(kKsHead) = sum_{k=a}^{v} k^-g, a = kKsHead + 1, by Euler-Maclaurin; also returns v^-g
+__device__ __forceinline__ double em_block(const KsCtx& c, uint64_t v, double& fv) {
+  const double Lv = ln_of(c.logs, v);
+  const double b = static_cast<double>(v);
+  const double a = static_cast<double>(kKsHead + 1);
+  fv = exp(-c.g * Lv);
+  const double om = 1.0 - c.g;
+  // integral_a^v x^-g dx = a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
+  const double integral = (om == 0.0) ? (Lv - c.La) : c.a_pow * expm1(om * (Lv - c.La)) / om;
+  const double d1 = -c.g * (fv / b - c.fa / a);  // f'(v) - f'(a)
+  const double g3 = c.g * (c.g + 1.0) * (c.g + 2.0);
+  const double d3 = -g3 * (fv / (b * b * b) - c.fa / (a * a * a));  // f'''(v) - f'''(a)
+  return integral + 0.5 * (c.fa + fv) + d1 / 12.0 - d3 / 720.0;
+}
+
+// score queue entries [0, cnt) lane-parallel (cnt <= 32)
+template <bool kArg>
+__device__ __forceinline__ void ks_flush(KsState& s, const KsCtx& c, int cnt, int lane, Work& wk) {
+  if (cnt <= 0) return;
+  if (lane < cnt) {
+    const uint32_t v = c.qk[lane];
+    const uint32_t before = c.qc[lane];
+    const uint32_t here = c.qn[lane];
+    double fv;
+    const double Sv = s.S_head + em_block(c, v, fv);
+    const double Fv = Sv * c.inv;
+    const double Fp = (Sv - fv) * c.inv;
+    take<kArg>(s, fabs(Fp - emp(c, before)), v - 1);  // k = v - 1 first (smaller k wins ties)
+    take<kArg>(s, fabs(Fv - emp(c, before + here)), v);
+  }
+  wk.ks_tails += cnt;
+}
+
+// Tiles of 32 consecutive k in [k_first, k_last] with counts[k - base], above the head.
+template <bool kArg>
+__device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int& q, uint64_t k_first, uint64_t k_last,
+                                                const uint32_t* counts, uint64_t base, int lane, Work& wk) {
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t k0 = k_first; k0 <= k_last && !s.done; k0 += 32) {
+    ++wk.ks_tiles;
+    const uint64_t k = k0 + lane;
+    const bool in = k <= k_last;
+    const uint32_t cnt = in ? counts[k - base] : 0u;
+    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
+    const unsigned nz = __ballot_sync(0xffffffffu, cnt != 0u);
+    if (cnt) {
+      const int slot = q + __popc(nz & lt);
+      c.qk[slot] = static_cast<uint32_t>(k);
+      c.qc[slot] = C - cnt;
+      c.qn[slot] = cnt;
+    }
+    q += __popc(nz);
+    s.Cb = __shfl_sync(0xffffffffu, C, 31);
+    __syncwarp();
+    if (q >= 32) {
+      ks_flush<kArg>(s, c, 32, lane, wk);
+      __syncwarp();
+      uint32_t a0 = 0, a1 = 0, a2 = 0;
+      if (lane < q - 32) {
+        a0 = c.qk[32 + lane];
+        a1 = c.qc[32 + lane];
+        a2 = c.qn[32 + lane];
+      }
+      __syncwarp();
+      if (lane < q - 32) {
+        c.qk[lane] = a0;
+        c.qc[lane] = a1;
+        c.qn[lane] = a2;
+      }
+      q -= 32;
+      __syncwarp();
+      s.Dw = warp_max(s.D);
+    }
+    // exit test, only once the empirical part of the bound allows it (D changes only at
+    // flushes); F-based tests back off geometrically in k (heavy tails approach 1 slowly)
+    const uint64_t k_hi = k0 + 31u < k_last ? k0 + 31u : k_last;
+    if (k_hi >= s.next_fcheck && s.Dw > 1.0 - emp(c, s.Cb) + kKsMargin) {
+      ks_flush<kArg>(s, c, q, lane, wk);
+      q = 0;
+      __syncwarp();
+      s.Dw = warp_max(s.D);
+      double fk;
+      const double F_pos = (s.S_head + em_block(c, k_hi, fk)) * c.inv;
+      ++wk.ks_tails;
+      if (s.Dw > fmax(1.0 - emp(c, s.Cb), 1.0 - F_pos) + kKsMargin)
+        s.done = true;
+      else
+        s.next_fcheck = 2 * k_hi - kKsHead;
+    }
+  }
+}
+
+// KS of one sample with counts of 1..H in `hist`; values above H are found in
+// over_vals[0..over_n) (which may also hold values <= H: they are ignored).  `queue` is
+// kKsQueueWords u32 of per-warp shared memory.  `hist` is left dirty (see used_pages).
+template <typename VT, bool kArg>
+__device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax, uint32_t* hist,
+                         const VT* over_vals, uint32_t over_n, uint32_t* queue, int lane, Work& wk) {
+  KsCtx c;
+  c.g = g;
+  c.inv = 1.0 / norm;
+  c.dn = static_cast<double>(p.n);
+  c.inv_n = 1.0 / c.dn;
+  c.exact = p.exact;
+  c.logs = p.logs;
+  c.qk = queue;
+  c.qc = queue + kKsQueue;
+  c.qn = queue + 2 * kKsQueue;
+  const uint64_t H = p.H;
+  KsState s{};
+  s.kb = 0xffffffffu;
+  KsOut out{0.0, 0u, false};
+
+  // head: dense, the reference's cumulative form
+  const uint32_t head_end = static_cast<uint32_t>(kmax < kKsHead ? kmax : kKsHead);
+  for (uint32_t k0 = 1; k0 <= head_end && !s.done; k0 += 32) {
+    ++wk.ks_tiles;
+    const uint32_t k = k0 + lane;
+    const bool in = k <= head_end;
+    const uint32_t cnt = in ? hist[k] : 0u;
+    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
+    const double term = in ? exp(-g * __ldg(p.logs + k)) : 0.0;
+    const double S = s.S + warp_scan(term, lane);
+    double F;
+    if (c.exact) {
+      F = s.F + warp_scan(term * c.inv, lane);
+      s.F = __shfl_sync(0xffffffffu, F, 31);
+    } else {
+      F = S * c.inv;
+    }
+    if (in) take<kArg>(s, fabs(F - emp(c, C)), k);
+    s.S = __shfl_sync(0xffffffffu, S, 31);
+    s.Cb = __shfl_sync(0xffffffffu, C, 31);
+    wk.ks_terms += min(32u, head_end - k0 + 1);
+    const double Dw = warp_max(s.D);
+    if (Dw > fmax(1.0 - emp(c, s.Cb), 1.0 - s.S * c.inv) + kKsMargin) s.done = true;
+  }
+  if (!s.done && kmax > kKsHead) {
+    s.S_head = s.S;
+    s.Dw = warp_max(s.D);
+    c.La = __ldg(p.logs + kKsHead + 1);
+    c.fa = exp(-g * c.La);
+    c.a_pow = static_cast<double>(kKsHead + 1) * c.fa;
+
+    // above the head: endpoints of the observed values
+    int q = 0;
+    ks_sparse_tiles<kArg>(s, c, q, kKsHead + 1, kmax < H ? kmax : H, hist, 0u, lane, wk);
+    uint64_t pa = H + 1;
+    while (!s.done && pa <= kmax) {
+      out.used_pages = true;
+      const uint64_t pb = pa + H - 1 < kmax ? pa + H - 1 : kmax;
+      // page histogram of the values in [pa, pb]; next occupied value above pb
+      for (int i = lane; i < p.hist_words; i += 32) hist[i] = 0u;
+      __syncwarp();
+      uint64_t next = ~0ull;
+      for (uint32_t i = lane; i < over_n; i += 32) {
+        const uint64_t v = static_cast<uint64_t>(over_vals[i]);
+        if (v >= pa && v <= pb)
+          atomicAdd(hist + (v - pa), 1u);
+        else if (v > pb)
+          next = v < next ? v : next;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(0xffffffffu, next, o);
+        next = t < next ? t : next;
+      }
+      __syncwarp();
+      ks_sparse_tiles<kArg>(s, c, q, pa, pb, hist, pa, lane, wk);
+      pa = pb + 1;
+      if (next != ~0ull && next > pa) pa = next;  // no observations in between: no endpoints
+    }
+    ks_flush<kArg>(s, c, q, lane, wk);
+  }
+  // warp result: max gap, smallest k among equal maxima
+  double D = s.D;
+  uint32_t kb = s.kb;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double Do = __shfl_xor_sync(0xffffffffu, D, o);
+    const uint32_t ko = __shfl_xor_sync(0xffffffffu, kb, o);
+    if (Do > D || (Do == D && ko < kb)) {
+      D = Do;
+      kb = ko;
+    }
+  }
+  out.D = D;
+  out.argk = kb;
+  return out;
+}
+
+__device__ __forceinline__ void clear_hist(uint32_t* hist, int words, int lane) {
+  uint4* h4 = reinterpret_cast<uint4*>(hist);
+  for (int i = lane; i < words / 4; i += 32) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+}
+
+}  // namespace zks

@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "zks_fit.cuh"
+#include "zks_ks.cuh"
 #include "zks_series.cuh"
 #include "zks_stream.cuh"
 
@@ -27,7 +28,6 @@ constexpr int kHistMax = 2048;             // histogram bins held in shared memo
 constexpr int kGuideLog2 = 12;              // guide table resolution G = 4096
 constexpr int kGuide = 1 << kGuideLog2;
 constexpr double kLn2 = 0.69314718055994530942;  // math.log(2.0)
-constexpr double kKsMargin = 1e-11;  // early-exit safety margin (>> fp64 rounding of the sums)
 
 struct ReplicateArgs {
   const double* cdf;
@@ -116,21 +116,6 @@ struct SampleStats {
   uint32_t vmin, vmax, over;
 };
 
-__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 // Draw n values of stream (seed, rep, sidx) into the warp's histogram / overflow slab.
 __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint64_t sidx,
@@ -263,21 +248,30 @@ __device__ bool bisect_root(const ModelFns& M, double target, int lane, double l
   return true;
 }
 
-// estimate.py:115-146 with DEFAULT_SETTINGS (x0 = 0.5, tol 1e-5, 200 iterations, [-20, 20])
-__device__ bool fit_exponent(const ModelFns& M, double target, int lane, double& g, Work& wk) {
-  double lo = -20.0, hi = 20.0;
+// MleSettings (estimate.py:24-50); the Monte Carlo always uses DEFAULT_SETTINGS (montecarlo.py:93)
+struct MleParams {
+  double x0 = 0.5;
+  double tol = 1e-5;
+  int max_iter = 200;
+  double lo = -20.0, hi = 20.0;  // bracket
+};
+
+// estimate.py:86-91 (_search_range) and 115-146 (mle_gamma)
+__device__ bool fit_exponent(const ModelFns& M, double target, int lane, double& g, Work& wk,
+                             const MleParams& P = MleParams()) {
+  double lo = P.lo, hi = P.hi;
   if (M.K == 0) {
-    lo = kMinUnboundedGamma;
-    hi = kMaxUnboundedGamma;
+    lo = fmax(lo, kMinUnboundedGamma);
+    hi = fmin(hi, kMaxUnboundedGamma);
   }
-  double x = 0.5;
+  double x = P.x0;
   if (!(lo < x && x < hi)) x = lo + 0.01;
-  for (int it = 0; it < 200; ++it) {
+  for (int it = 0; it < P.max_iter; ++it) {
     double mean, slope;
     if (!model_mean_slope(M, x, lane, mean, slope, wk)) return false;
     const double x_new = x + (mean - target) / slope;
     if (!isfinite(x_new) || x_new < lo || x_new > hi) return bisect_root(M, target, lane, lo, hi, g, wk);
-    if (fabs(x_new - x) <= 1e-5) {
+    if (fabs(x_new - x) <= P.tol) {
       g = x_new;
       return true;
     }
@@ -286,217 +280,15 @@ __device__ bool fit_exponent(const ModelFns& M, double target, int lane, double&
   return bisect_root(M, target, lane, lo, hi, g, wk);
 }
 
-// ---------------------------------------------------------------------------- KS statistic
-//
-// The reference scans F(k) - E(k) over every k = 1..kmax (gof.py:60-68), or, for an unbounded
-// fit with kmax > 4096, only the stretch endpoints v and v-1 of the observed values v, with
-// F from the cumulative table below the seam and an Euler-Maclaurin tail above it
-// (gof.py:71-105).  Both give the same supremum (E is constant between observations while F
-// rises, so each stretch attains its extremes at its ends).  Here:
-//   * head, k <= kKsHead: dense, F(k) = S(k) / norm with S the running sum of k^-g, exactly
-//     the reference's cumulative form;
-//   * k > kKsHead: endpoints only, S(v) = S(kKsHead) + EM(kKsHead+1 .. v) by Euler-Maclaurin
-//     through the third-derivative term (the order of series.tail_mass, series.py:141-160),
-//     S(v-1) = S(v) - v^-g.  Observed values are gathered tile by tile from the histogram
-//     into a per-warp queue and scored 32 at a time, so the exp work scales with the number of
-//     distinct values, not with kmax.
-// The scan stops once no later k can beat the current maximum:
-//   sup_{k' > k} |F(k') - E(k')| <= max(1 - E(k), 1 - F(k)).
-constexpr uint32_t kKsHead = 64;
-constexpr int kKsQueue = 64;  // per-warp endpoint queue entries
-
-struct KsState {
-  double S;       // running sum of k^-g through the last dense k
-  double S_head;  // S(min(kmax, kKsHead))
-  double Dw;      // warp max of D as of the last flush (warp-uniform)
-  uint32_t Cb;    // observations <= last processed k
-  double D;       // lane-local running max gap
-  bool done;
-  uint32_t next_fcheck;  // no F-based exit test before this k
-};
-
-struct KsCtx {
-  double g, inv, inv_n;
-  double fa, a_pow, La;  // f(a) = a^-g, a^(1-g), ln a for a = kKsHead + 1
-  const double* logs;
-  uint32_t* qk;  // queue: value v
-  uint32_t* qc;  // queue: observations < v
-  uint32_t* qn;  // queue: observations == v
-};
-
-// S(v) - S(kKsHead) = sum_{k=a}^{v} k^-g, a = kKsHead + 1, by Euler-Maclaurin; also returns v^-g
-__device__ __forceinline__ double em_block(const KsCtx& c, uint32_t v, double& fv) {
-  const double Lv = __ldg(c.logs + v);
-  const double b = static_cast<double>(v);
-  const double a = static_cast<double>(kKsHead + 1);
-  fv = exp(-c.g * Lv);
-  const double om = 1.0 - c.g;
-  // integral_a^v x^-g dx = a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
-  const double integral = (om == 0.0) ? (Lv - c.La) : c.a_pow * expm1(om * (Lv - c.La)) / om;
-  const double d1 = -c.g * (fv / b - c.fa / a);  // f'(v) - f'(a)
-  const double g3 = c.g * (c.g + 1.0) * (c.g + 2.0);
-  const double d3 = -g3 * (fv / (b * b * b) - c.fa / (a * a * a));  // f'''(v) - f'''(a)
-  return integral + 0.5 * (c.fa + fv) + d1 / 12.0 - d3 / 720.0;
-}
-
-// score queue entries [0, cnt) lane-parallel (cnt <= 32)
-__device__ __forceinline__ void ks_flush(KsState& s, const KsCtx& c, int cnt, int lane, Work& wk) {
-  if (cnt <= 0) return;
-  double Fv = 0.0;
-  if (lane < cnt) {
-    const uint32_t v = c.qk[lane];
-    const uint32_t before = c.qc[lane];
-    const uint32_t here = c.qn[lane];
-    double fv;
-    const double Sv = s.S_head + em_block(c, v, fv);
-    Fv = Sv * c.inv;
-    const double Fp = (Sv - fv) * c.inv;
-    const double E = static_cast<double>(before + here) * c.inv_n;
-    const double Eb = static_cast<double>(before) * c.inv_n;
-    s.D = fmax(s.D, fmax(fabs(Fv - E), fabs(Fp - Eb)));
-  }
-  wk.ks_tails += cnt;
-}
-
-// exit test: every later gap is bounded by max(1 - E, 1 - F) at the scan position
-__device__ __forceinline__ void ks_check(KsState& s, double F_pos, double inv_n) {
-  const double Dw = warp_max(s.D);
-  const double bound = fmax(1.0 - static_cast<double>(s.Cb) * inv_n, 1.0 - F_pos);
-  if (Dw > bound + kKsMargin) s.done = true;
-}
-
-// Tiles of 32 consecutive k in [k_first, k_last] with counts[k - base], above the head.
-__device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int& q, uint32_t k_first,
-                                                uint32_t k_last, const uint32_t* counts, uint32_t base, int lane,
-                                                Work& wk) {
-  const unsigned lt = (1u << lane) - 1u;
-  for (uint32_t k0 = k_first; k0 <= k_last && !s.done; k0 += 32) {
-    ++wk.ks_tiles;
-    const uint32_t k = k0 + lane;
-    const bool in = k <= k_last;
-    const uint32_t cnt = in ? counts[k - base] : 0u;
-    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
-    const unsigned nz = __ballot_sync(0xffffffffu, cnt != 0u);
-    if (cnt) {
-      const int slot = q + __popc(nz & lt);
-      c.qk[slot] = k;
-      c.qc[slot] = C - cnt;
-      c.qn[slot] = cnt;
-    }
-    q += __popc(nz);
-    s.Cb = __shfl_sync(0xffffffffu, C, 31);
-    __syncwarp();
-    if (q >= 32) {
-      ks_flush(s, c, 32, lane, wk);
-      __syncwarp();
-      uint32_t a0 = 0, a1 = 0, a2 = 0;
-      if (lane < q - 32) {
-        a0 = c.qk[32 + lane];
-        a1 = c.qc[32 + lane];
-        a2 = c.qn[32 + lane];
-      }
-      __syncwarp();
-      if (lane < q - 32) {
-        c.qk[lane] = a0;
-        c.qc[lane] = a1;
-        c.qn[lane] = a2;
-      }
-      q -= 32;
-      __syncwarp();
-      s.Dw = warp_max(s.D);
-    }
-    // exit test, only once the empirical part of the bound allows it (D changes only at flushes)
-    const uint32_t k_hi = min(k0 + 31u, k_last);
-    // (F checks back off geometrically in k: heavy tails make F approach 1 slowly)
-    if (k_hi >= s.next_fcheck && s.Dw > 1.0 - static_cast<double>(s.Cb) * c.inv_n + kKsMargin) {
-      ks_flush(s, c, q, lane, wk);
-      q = 0;
-      __syncwarp();
-      s.Dw = warp_max(s.D);
-      double fk;
-      const double F_pos = (s.S_head + em_block(c, k_hi, fk)) * c.inv;
-      ++wk.ks_tails;
-      if (s.Dw > fmax(1.0 - static_cast<double>(s.Cb) * c.inv_n, 1.0 - F_pos) + kKsMargin)
-        s.done = true;
-      else
-        s.next_fcheck = 2 * k_hi - kKsHead;
-    }
-  }
-}
-
-// KS of one sample: counts of 1..H in `hist`; values above H are found in over_vals[0..over_n)
-// (which may also hold values <= H: they are ignored).  `queue` is 3 * kKsQueue u32 of
-// per-warp shared memory.
-__device__ double ks_scan(const ReplicateArgs& a, double g, double norm, uint32_t kmax, uint32_t* hist,
-                          const uint16_t* over_vals, uint32_t over_n, uint32_t* queue, int lane, bool& used_pages,
-                          Work& wk) {
-  KsCtx c;
-  c.g = g;
-  c.inv = 1.0 / norm;
-  c.inv_n = 1.0 / static_cast<double>(a.n);
-  c.logs = a.logs;
-  c.qk = queue;
-  c.qc = queue + kKsQueue;
-  c.qn = queue + 2 * kKsQueue;
-  const uint32_t H = static_cast<uint32_t>(a.H);
-  KsState s{0.0, 0.0, 0.0, 0u, 0.0, false, 0u};  // S, S_head, Dw, Cb, D, done, next_fcheck
-  used_pages = false;
-
-  // head: dense, exactly the reference's cumulative form
-  const uint32_t head_end = min(kmax, kKsHead);
-  for (uint32_t k0 = 1; k0 <= head_end && !s.done; k0 += 32) {
-    ++wk.ks_tiles;
-    const uint32_t k = k0 + lane;
-    const bool in = k <= head_end;
-    const uint32_t cnt = in ? hist[k] : 0u;
-    const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
-    const double term = in ? exp(-g * __ldg(a.logs + k)) : 0.0;
-    const double S = s.S + warp_scan(term, lane);
-    if (in) s.D = fmax(s.D, fabs(S * c.inv - static_cast<double>(C) * c.inv_n));
-    s.S = __shfl_sync(0xffffffffu, S, 31);
-    s.Cb = __shfl_sync(0xffffffffu, C, 31);
-    wk.ks_terms += min(32u, head_end - k0 + 1);
-    ks_check(s, s.S * c.inv, c.inv_n);
-  }
-  if (s.done || kmax <= kKsHead) return warp_max(s.D);
-  s.S_head = s.S;
-  s.Dw = warp_max(s.D);
-  c.La = __ldg(a.logs + kKsHead + 1);
-  c.fa = exp(-g * c.La);
-  c.a_pow = static_cast<double>(kKsHead + 1) * c.fa;
-
-  // above the head: endpoints of the observed values
-  int q = 0;
-  ks_sparse_tiles(s, c, q, kKsHead + 1, min(kmax, H), hist, 0u, lane, wk);
-  uint32_t pa = H + 1;
-  while (!s.done && pa <= kmax) {
-    used_pages = true;
-    const uint32_t pb = min(pa + H - 1, kmax);
-    // page histogram of the values in [pa, pb]; next occupied value above pb
-    for (int i = lane; i < a.hist_words; i += 32) hist[i] = 0u;
-    __syncwarp();
-    uint32_t next = 0xffffffffu;
-    for (uint32_t i = lane; i < over_n; i += 32) {
-      const uint32_t v = over_vals[i];
-      if (v >= pa && v <= pb)
-        atomicAdd(hist + (v - pa), 1u);
-      else if (v > pb)
-        next = min(next, v);
-    }
-    next = warp_min_u32(next);
-    __syncwarp();
-    ks_sparse_tiles(s, c, q, pa, pb, hist, pa, lane, wk);
-    pa = pb + 1;
-    if (next != 0xffffffffu && next > pa) pa = next;  // no observations in between: no endpoints
-  }
-  ks_flush(s, c, q, lane, wk);
-  return warp_max(s.D);
-}
-
-__device__ __forceinline__ void clear_hist(uint32_t* hist, int words, int lane) {
-  uint4* h4 = reinterpret_cast<uint4*>(hist);
-  for (int i = lane; i < words / 4; i += 32) h4[i] = make_uint4(0u, 0u, 0u, 0u);
-  __syncwarp();
+// KS parameters of a replicate launch
+__device__ __forceinline__ KsParams ks_params(const ReplicateArgs& a) {
+  KsParams p;
+  p.n = a.n;
+  p.H = static_cast<uint32_t>(a.H);
+  p.hist_words = a.hist_words;
+  p.logs = a.logs;
+  p.exact = false;
+  return p;
 }
 
 template <bool kCount>
@@ -540,7 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
       bool used_pages = false;
       if (ok) {
         const double norm = model_norm(M, g, lane, wk);
-        ks = ks_scan(a, g, norm, st.vmax, hist, slab, st.over, queue, lane, used_pages, wk);
+        const KsOut ko = ks_scan<uint16_t, false>(ks_params(a), g, norm, st.vmax, hist, slab, st.over, queue, lane, wk);
+        ks = ko.D;
+        used_pages = ko.used_pages;
         gh = g;
         status = static_cast<uint8_t>(attempt);
       } else {

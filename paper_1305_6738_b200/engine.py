@@ -151,6 +151,58 @@ class Engine:
         self.bind_stream()
         _native.check(self.lib.zks_draw(self.handle, table.handle, u.data_ptr(), u.numel(), out.data_ptr()))
 
+    # -- user samples / series ------------------------------------------------
+    @staticmethod
+    def _settings(settings):
+        if settings is None:
+            return None
+        lo, hi = settings.bracket
+        return _native.ZksMleSettings(float(settings.initial_guess), float(settings.absolute_tolerance),
+                                      int(settings.max_iterations), 0, float(lo), float(hi))
+
+    def fit_samples(self, support_k, values, offsets, mode, settings=None, gamma_in=None, norm_in=None) -> dict:
+        """zks_fit_samples over device int64 ``values`` split by device int64 ``offsets``."""
+        torch = _torch()
+        ns = offsets.numel() - 1
+        dev = values.device
+        out = {
+            "log_mean": torch.empty(ns, dtype=torch.float64, device=dev),
+            "gamma": torch.empty(ns, dtype=torch.float64, device=dev),
+            "ks": torch.empty(ns, dtype=torch.float64, device=dev),
+            "argmax": torch.empty(ns, dtype=torch.int64, device=dev),
+            "status": torch.empty(ns, dtype=torch.uint8, device=dev),
+        }
+        st = self._settings(settings)
+        self.bind_stream()
+        _native.check(self.lib.zks_fit_samples(
+            self.handle, 0 if support_k is None else int(support_k), values.data_ptr(), offsets.data_ptr(), ns,
+            int(mode), ctypes.byref(st) if st is not None else None,
+            gamma_in.data_ptr() if gamma_in is not None else None, norm_in.data_ptr() if norm_in is not None else None,
+            out["log_mean"].data_ptr(), out["gamma"].data_ptr(), out["ks"].data_ptr(), out["argmax"].data_ptr(),
+            out["status"].data_ptr()))
+        return out
+
+    def series(self, support_k, gammas):
+        """(s0, s1, s2, normaliser) rows at device float64 ``gammas`` (reference formulas)."""
+        torch = _torch()
+        out = torch.empty((gammas.numel(), 4), dtype=torch.float64, device=gammas.device)
+        self.bind_stream()
+        _native.check(self.lib.zks_series_eval(self.handle, 0 if support_k is None else int(support_k),
+                                               gammas.data_ptr(), gammas.numel(), out.data_ptr()))
+        return out
+
+    def solve(self, support_k, targets, settings=None, bisect_only=False):
+        torch = _torch()
+        g = torch.empty_like(targets)
+        st = torch.empty(targets.numel(), dtype=torch.uint8, device=targets.device)
+        s = self._settings(settings)
+        self.bind_stream()
+        _native.check(self.lib.zks_solve_exponents(self.handle, 0 if support_k is None else int(support_k),
+                                                   targets.data_ptr(), targets.numel(),
+                                                   ctypes.byref(s) if s is not None else None, int(bisect_only),
+                                                   g.data_ptr(), st.data_ptr()))
+        return g, st
+
     # -- diagnostics ---------------------------------------------------------
     def set_counters(self, counters) -> None:
         """Count replicate-kernel work into a device uint64/int64 tensor of 8 (None = off)."""

@@ -8,12 +8,65 @@ tail masses) run on the device (csrc/zks_series.cuh).
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 MAX_FINITE_SUPPORT = 32766   # series.py:20
 SERIES_RTOL = 1e-12          # series.py:23
 
 _cache = np.zeros(1)
+
+
+@dataclass(frozen=True)
+class LogTable:
+    """Precomputed natural logarithms of 1..limit, indexable by integer value (series.py:47-52)."""
+
+    logs: np.ndarray
+    limit: int
+
+
+def build_log_table(limit: int) -> LogTable:
+    """Table of ln k for k = 1..limit; entry 0 is padding (series.py:55-65)."""
+    if isinstance(limit, bool) or not isinstance(limit, (int, np.integer)):
+        raise ValueError(f"log table limit must be an integer, got {limit!r}")
+    if limit < 1 or limit > MAX_FINITE_SUPPORT:
+        raise ValueError(f"log table limit must be in [1, {MAX_FINITE_SUPPORT}], got {limit}")
+    return LogTable(logs=natural_logs(int(limit)), limit=int(limit))
+
+
+def _series_rows(gammas, support) -> np.ndarray:
+    """(s0, s1, s2, normaliser) per exponent from the device (zks_series_eval)."""
+    import torch
+
+    from .engine import get_engine
+
+    eng = get_engine()
+    g = torch.as_tensor(np.asarray(gammas, dtype=np.float64).ravel()).to(f"cuda:{eng.device}")
+    return eng.series(None if support is None else support.k, g).cpu().numpy()
+
+
+def finite_log_moments(gamma: float, k: int) -> tuple[float, float, float]:
+    """(s0, s1, s2), s_p = sum_{j=1..k} j^-gamma (ln j)^p (series.py:68-73), on the device."""
+    from .distribution import Support
+
+    s0, s1, s2, _ = _series_rows([gamma], Support.finite(k))[0]
+    return float(s0), float(s1), float(s2)
+
+
+def zeta_log_moments(gamma: float) -> tuple[float, float, float]:
+    """(s0, s1, s2) of the zeta series with its Euler-Maclaurin tail (series.py:102-123)."""
+    if gamma <= 1.0:
+        raise ValueError(f"series diverges for gamma <= 1, got {gamma}")
+    s0, s1, s2, _ = _series_rows([gamma], None)[0]
+    return float(s0), float(s1), float(s2)
+
+
+def zeta_value(gamma: float) -> float:
+    """sum_{k>=1} k^-gamma (series.py:126-138)."""
+    if gamma <= 1.0:
+        raise ValueError(f"series diverges for gamma <= 1, got {gamma}")
+    return float(_series_rows([gamma], None)[0][3])
 
 
 def natural_logs(limit: int) -> np.ndarray:
