@@ -41,7 +41,7 @@ constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory ca
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
 constexpr int64_t kBatchMaxN = 1024;                  // n up to which replicate_batch_kernel runs
-constexpr uint32_t kBatchHist = 1024;                 // its per-warp histogram bins
+constexpr uint32_t kBatchHist = 512;                  // its per-warp histogram bins
 
 }  // namespace
 
@@ -258,7 +258,8 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
   size_t smem;
   int64_t per_block;  // replicates one block takes per work item round
   if (batched) {
-    a.H = static_cast<int32_t>(std::min<uint32_t>(L, kBatchHist));
+    // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
+    a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
     a.hist_words = zks::round_up(std::max(a.H, 4) + 1, 4);
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
     a.batch = std::min(32, zks::kBatchVals / a.vals_stride);

@@ -27,6 +27,7 @@ namespace zks {
 constexpr uint32_t kKsHead = 64;
 constexpr int kKsQueue = 64;         // per-warp endpoint queue entries
 constexpr int kKsQueueWords = 3 * kKsQueue;
+constexpr uint32_t kOverCap = 128;     // values above the histogram ordered in registers (<= kKsQueueWords)
 constexpr double kKsMargin = 1e-11;  // early-exit safety margin (>> fp64 rounding of the sums)
 
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
@@ -248,8 +249,75 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     // above the head: endpoints of the observed values
     int q = 0;
     ks_sparse_tiles<kArg>(s, c, q, kKsHead + 1, kmax < H ? kmax : H, hist, 0u, lane, wk);
+    bool paged = true;
+    if (!s.done && kmax > H) {
+      // Values above H are few unless the tail is very heavy: with at most kOverCap of them,
+      // take them in increasing order by repeated warp minimum over registers (no pages).
+      ks_flush<kArg>(s, c, q, lane, wk);  // the emptied queue stages the values
+      q = 0;
+      __syncwarp();
+      s.Dw = warp_max(s.D);
+      const unsigned lt = (1u << lane) - 1u;
+      uint32_t m = 0;
+      for (uint32_t i0 = 0; i0 < over_n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint64_t v = i < over_n ? static_cast<uint64_t>(over_vals[i]) : 0ull;
+        const bool big = v > H;
+        const unsigned b = __ballot_sync(0xffffffffu, big);
+        const uint32_t slot = m + __popc(b & lt);
+        if (big && slot < kOverCap) queue[slot] = static_cast<uint32_t>(v);
+        m += __popc(b);
+      }
+      __syncwarp();
+      if (m <= kOverCap) {
+        paged = false;
+        uint32_t r[kOverCap / 32];
+#pragma unroll
+        for (int j = 0; j < kOverCap / 32; ++j) {
+          const uint32_t idx = j * 32 + lane;
+          r[j] = idx < m ? queue[idx] : 0xffffffffu;
+        }
+        __syncwarp();
+        int ne = 0;
+        while (!s.done) {
+          uint32_t mn = 0xffffffffu;
+#pragma unroll
+          for (int j = 0; j < kOverCap / 32; ++j) mn = min(mn, r[j]);
+          mn = warp_min_u32(mn);
+          if (mn == 0xffffffffu) break;
+          uint32_t cnt = 0;
+#pragma unroll
+          for (int j = 0; j < kOverCap / 32; ++j)
+            if (r[j] == mn) {
+              ++cnt;
+              r[j] = 0xffffffffu;
+            }
+          cnt = warp_sum_u32(cnt);
+          if (lane == 0) {
+            c.qk[ne] = mn;
+            c.qc[ne] = s.Cb;
+            c.qn[ne] = cnt;
+          }
+          s.Cb += cnt;
+          if (++ne == 32) {
+            __syncwarp();
+            ks_flush<kArg>(s, c, 32, lane, wk);
+            ne = 0;
+            __syncwarp();
+            s.Dw = warp_max(s.D);
+            if (s.Dw > 1.0 - emp(c, s.Cb) + kKsMargin) {
+              double fk;
+              const double F_pos = (s.S_head + em_block(c, mn, fk)) * c.inv;
+              if (s.Dw > fmax(1.0 - emp(c, s.Cb), 1.0 - F_pos) + kKsMargin) s.done = true;
+            }
+          }
+        }
+        __syncwarp();
+        ks_flush<kArg>(s, c, ne, lane, wk);
+      }
+    }
     uint64_t pa = H + 1;
-    while (!s.done && pa <= kmax) {
+    while (paged && !s.done && pa <= kmax) {
       out.used_pages = true;
       const uint64_t pb = pa + H - 1 < kmax ? pa + H - 1 : kmax;
       // page histogram of the values in [pa, pb]; next occupied value above pb
