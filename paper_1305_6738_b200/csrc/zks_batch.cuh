@@ -16,6 +16,7 @@
 namespace zks {
 
 constexpr int kBatchVals = 4096;  // u16 sample slots per warp
+constexpr int kLaneDrawMaxN = 128;  // below this n a lane draws a whole replicate
 
 struct DrawStats {
   double log_sum;
@@ -50,6 +51,37 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   s.log_sum = warp_sum(ls);
   s.vmin = warp_min_u32(mn);
   s.vmax = warp_max_u32(mx);
+  return s;
+}
+
+// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle).
+__device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
+                                                      const uint16_t* __restrict__ guide, uint16_t* v) {
+  const int n = static_cast<int>(a.n);
+  const int nb = (n + 3) >> 2;
+  double ls = 0.0;
+  uint32_t mn = 0xffffffffu, mx = 0;
+  for (int b = 0; b < nb; ++b) {
+    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    bool vb[4];
+    uint32_t x[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
+    draw_block(r, vb, guide, a.cdf, a.L, x);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (vb[w]) {
+        ls += __ldg(a.logs + x[w]);
+        mn = min(mn, x[w]);
+        mx = max(mx, x[w]);
+      }
+    }
+    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
+  }
+  DrawStats s;
+  s.log_sum = ls;
+  s.vmin = mn;
+  s.vmax = mx;
   return s;
 }
 
@@ -134,13 +166,23 @@ __global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateA
     // 2. samples into shared memory
     double my_ls = 0.0;
     uint32_t my_min = 0, my_max = 0;
-    for (int r = 0; r < nrep; ++r) {
-      const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
-      const DrawStats st = draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
-      if (lane == r) {
+    if (a.n < kLaneDrawMaxN) {
+      // few Philox blocks per replicate: each lane draws its own replicate's sample
+      if (active) {
+        const DrawStats st = draw_sample_lane(a, k0, k1, guide, vals + lane * a.vals_stride);
         my_ls = st.log_sum;
         my_min = st.vmin;
         my_max = st.vmax;
+      }
+    } else {
+      for (int r = 0; r < nrep; ++r) {
+        const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
+        const DrawStats st = draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
+        if (lane == r) {
+          my_ls = st.log_sum;
+          my_min = st.vmin;
+          my_max = st.vmax;
+        }
       }
     }
     __syncwarp();
