@@ -15,7 +15,13 @@
 
 namespace zks {
 
-constexpr int kBatchVals = 4096;  // u16 sample slots per warp
+#ifndef ZKS_BATCH_MINB
+#define ZKS_BATCH_MINB 2
+#endif
+#ifndef ZKS_BATCH_VALS
+#define ZKS_BATCH_VALS 4096
+#endif
+constexpr int kBatchVals = ZKS_BATCH_VALS;  // u16 sample slots per warp
 constexpr int kLaneDrawMaxN = 128;  // below this n a lane draws a whole replicate
 
 struct DrawStats {
@@ -36,7 +42,7 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
     uint32_t x[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block(r, vb, guide, a.cdf, a.L, x);
+    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -67,7 +73,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
     uint32_t x[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block(r, vb, guide, a.cdf, a.L, x);
+    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -128,17 +134,17 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
 }
 
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads, 2) replicate_batch_kernel(ReplicateArgs a) {
+__global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
-  const int guide_bytes = round_up((kGuide + 2) * 2, 16);
+  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warp_bytes = a.hist_words * 4 + 3 * kKsQueue * 4 + kBatchVals * 2;
   unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;
   uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
-  for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
+  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
 

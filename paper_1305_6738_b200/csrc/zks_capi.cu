@@ -172,7 +172,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   t->len = static_cast<uint32_t>(len);
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
-  cudaError_t err = cudaMallocAsync(&mem, len * sizeof(double) + (zks::kGuide + 2) * sizeof(uint16_t), e->stream);
+  cudaError_t err = cudaMallocAsync(&mem, len * sizeof(double) + 2 * zks::kGuideLevel * sizeof(uint16_t), e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
     t->guide = reinterpret_cast<uint16_t*>(t->cdf + len);
@@ -190,7 +190,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
     if (err == cudaSuccess) err = cudaEventRecord(e->staging_done[slot], e->stream);
   }
   if (err == cudaSuccess) {
-    zks::guide_kernel<<<(zks::kGuide + 2 + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
+    zks::guide_kernel<<<(2 * zks::kGuideLevel + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
     err = cudaGetLastError();
   }
   if (err != cudaSuccess) {
@@ -253,7 +253,8 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
 
   const bool counting = e->counters != nullptr;
   const bool batched = a.use_table && c->n <= kBatchMaxN;
-  const size_t guide_bytes = zks::round_up((zks::kGuide + 2) * 2, 16);
+  a.guide_levels = L > 4096u ? 2 : 1;
+  const size_t guide_bytes = zks::round_up(a.guide_levels * zks::kGuideLevel * 2, 16);
   void (*kernel)(zks::ReplicateArgs);
   size_t smem;
   int64_t per_block;  // replicates one block takes per work item round

@@ -27,11 +27,15 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kHistMax = 2048;             // histogram bins held in shared memory per warp
 constexpr int kGuideLog2 = 12;              // guide table resolution G = 4096
 constexpr int kGuide = 1 << kGuideLog2;
+constexpr int kGuideLevel = kGuide + 2;     // entries per guide level
+// second level: the top 2^-5 of u in 4096 bins of 2^-17 (heavy tails: k ranges per bin stay short)
+constexpr double kGuide2Start = 0.96875;    // 1 - 2^-5
+constexpr double kGuide2Scale = 131072.0;   // 2^17
 constexpr double kLn2 = 0.69314718055994530942;  // math.log(2.0)
 
 struct ReplicateArgs {
   const double* cdf;
-  const uint16_t* guide;
+  const uint16_t* guide;  // guide_levels x kGuideLevel entries
   const double* logs;
   uint32_t L;      // draw-table length: K or 65535
   int32_t K;       // finite support bound, 0 = unbounded
@@ -51,15 +55,25 @@ struct ReplicateArgs {
   int use_table;                 // 1: table-driven model functions, 0: direct sums
   int batch;                     // replicates per warp batch (replicate_batch_kernel)
   int vals_stride;               // u16 sample slots per replicate in the batch store
+  int guide_levels;              // 1, or 2 for long tables (L > 4096)
 };
+
+// guide lookup: [lo, hi] brackets lower_bound(cdf, u)
+__device__ __forceinline__ void guide_bracket(double u, const uint16_t* guide, bool two, uint32_t& lo, uint32_t& hi) {
+  const bool up = two && u >= kGuide2Start;
+  const int j = up ? static_cast<int>((u - kGuide2Start) * kGuide2Scale) : static_cast<int>(u * static_cast<double>(kGuide));
+  const uint16_t* g = guide + (up ? kGuideLevel : 0) + j;
+  lo = g[0];
+  hi = g[1];
+}
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // smallest k (1-based) with cdf[k-1] >= u, clamped to L (distribution.py:200-201)
 __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restrict__ guide,
-                                               const double* __restrict__ cdf, uint32_t L) {
-  const int j = static_cast<int>(u * static_cast<double>(kGuide));  // exact: G is 2^12
-  uint32_t lo = guide[j], hi = guide[j + 1];
+                                               const double* __restrict__ cdf, uint32_t L, bool two) {
+  uint32_t lo, hi;
+  guide_bracket(u, guide, two, lo, hi);  // exact index arithmetic: u is a multiple of 2^-53
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
     if (__ldg(cdf + mid) >= u)
@@ -74,15 +88,14 @@ __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restr
 // The four draws of one Philox block, their lower_bound searches interleaved so that up to four
 // independent cdf loads are in flight per lane.  Lanes with valid[w] false yield 0.
 __device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
-                                           const double* __restrict__ cdf, uint32_t L, uint32_t out[4]) {
+                                           const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
   double u[4];
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     u[w] = uniform_open_closed(r.w[w]);
-    const int j = static_cast<int>(u[w] * static_cast<double>(kGuide));
-    lo[w] = valid[w] ? guide[j] : 0u;
-    hi[w] = valid[w] ? guide[j + 1] : 0u;
+    guide_bracket(u[w], guide, two, lo[w], hi[w]);
+    if (!valid[w]) hi[w] = lo[w];
   }
   for (;;) {
     bool act[4];
@@ -136,7 +149,7 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
     uint32_t vv[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = (4 * b + w) < n;
-    draw_block(r, vb, guide, a.cdf, a.L, vv);
+    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, vv);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const bool valid = vb[w];
@@ -295,11 +308,11 @@ template <bool kCount>
 __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
-  const int guide_bytes = round_up((kGuide + 2) * 2, 16);
+  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * (a.hist_words + 3 * kKsQueue);
   uint32_t* queue = hist + a.hist_words;
-  for (int i = threadIdx.x; i < kGuide + 2; i += blockDim.x) guide[i] = a.guide[i];
+  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
@@ -364,15 +377,18 @@ __global__ void normaliser_kernel(double g, int K, const double* __restrict__ lo
   if (threadIdx.x == 0) *out = v;
 }
 
-// guide[j] = lower_bound(cdf, j / G) for j = 0..G; guide[G + 1] = L
+// level 0: guide[j] = lower_bound(cdf, j / G), j = 0..G; level 1: lower_bound(cdf, 1 - 2^-5 + j 2^-17);
+// each level ends with L
 __global__ void guide_kernel(const double* __restrict__ cdf, uint32_t L, uint16_t* guide) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j > kGuide + 1) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * kGuideLevel) return;
+  const int level = t / kGuideLevel, j = t % kGuideLevel;
   if (j == kGuide + 1) {
-    guide[j] = static_cast<uint16_t>(L);
+    guide[t] = static_cast<uint16_t>(L);
     return;
   }
-  const double u = static_cast<double>(j) / static_cast<double>(kGuide);
+  const double u = level ? kGuide2Start + static_cast<double>(j) / kGuide2Scale
+                         : static_cast<double>(j) / static_cast<double>(kGuide);
   uint32_t lo = 0, hi = L;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -381,7 +397,7 @@ __global__ void guide_kernel(const double* __restrict__ cdf, uint32_t L, uint16_
     else
       lo = mid + 1;
   }
-  guide[j] = static_cast<uint16_t>(lo);
+  guide[t] = static_cast<uint16_t>(lo);
 }
 
 // RandomStream.uniforms (distribution.py:186-187) for one stream, block-parallel
@@ -406,7 +422,7 @@ __global__ void draw_kernel(const double* __restrict__ cdf, const uint16_t* __re
     const double x = u[i];
     int64_t v;
     if (x > 0.0 && x <= 1.0) {
-      v = draw_value(x, guide, cdf, L);
+      v = draw_value(x, guide, cdf, L, true);
     } else {
       // outside (0, 1]: plain lower_bound over the whole table (searchsorted semantics)
       uint32_t lo = 0, hi = L;
