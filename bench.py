@@ -38,7 +38,6 @@ METRIC = "KS replicates/sec per (gamma,n) at 1/2/4/8 B200 vs host-CPU ref; roofl
 GAMMAS = tuple(round(1.5 + 0.1 * i, 1) for i in range(21))
 NS = (10, 20, 50, 100, 500, 1000)
 CPU_SAMPLE_GAMMAS = (1.5, 1.9, 2.3, 2.7, 3.1, 3.5)
-LAUNCHES_PER_CELL_REP = 10  # replicate kernel + select init + 8 radix passes
 CLOCK_QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -199,12 +198,9 @@ def run_b200(args, world, rank, local):
     kernel_events = []
 
     def sweep(record_kernels=False):
-        plans = []
-        for cfg in configs:
-            plan = mc._CellPlan(cfg)
-            mc._enqueue_cell(eng, plan, shard=shard, gather=gather,
-                             kernel_events=kernel_events if record_kernels else None)
-            plans.append(plan)
+        plans = [mc._CellPlan(cfg) for cfg in configs]
+        mc._enqueue_plans(eng, plans, shard=shard, gather=gather,
+                          kernel_events=kernel_events if record_kernels else None)
         return plans
 
     # warm-up (also builds and uploads the 21 draw tables)
@@ -213,7 +209,7 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
 
     # work counters for the roofline: one instrumented sweep outside the timed region
-    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    counters = torch.zeros(10, dtype=torch.int64, device=dev)
     eng.set_counters(counters)
     sweep()
     torch.cuda.synchronize()
@@ -225,6 +221,7 @@ def run_b200(args, world, rank, local):
     stream = torch.cuda.current_stream()
     total_ms = 0.0
     plans = None
+    launches0 = eng.launches
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -238,6 +235,7 @@ def run_b200(args, world, rank, local):
             barrier()
             total_ms += e0.elapsed_time(e1)
     clock = clocks.summary()
+    timed_launches = eng.launches - launches0
     kernel_ms = sum(a.elapsed_time(b) for a, b in kernel_events)
     t = torch.tensor([total_ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -249,22 +247,31 @@ def run_b200(args, world, rank, local):
         assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
 
     # roofline of the replicate kernel (dominant kernel)
-    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles = work
+    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made = work
     exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
     terms = eval_terms + norm_terms + ks_terms
-    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * 8 * exp_flops  # tails: 2 tail sums x 4 exps
-    mul64 = 5.0 * draws  # 20 mulhilo per Philox block of 4 draws
-    launches = ncells  # one replicate kernel per cell per step (1 repetition)
+    # endpoint scoring: one exp + one expm1 per value (Euler-Maclaurin block)
+    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * (2 * exp_flops + 20.0)
+    mul64 = 5.0 * draws  # Philox draws inside replicate kernels: 20 mulhilo per block of 4
+    hbm_bytes = 8.0 * staged + 17.0 * attempts  # staged uniforms read + (ks, gamma_hat, status) written
+    launches = len(kernel_events) // max(args.steps, 1)  # replicate-kernel launches per sweep
     kernel_s = kernel_ms / 1e3 / args.steps  # per sweep
-    t_fp64 = fp64_flops / peaks["dfma_flops"]
-    t_int = mul64 / peaks["mul64_per_s"]
-    if t_fp64 >= t_int:
-        roof = {"bound": "fp64", "achieved": fp64_flops / kernel_s / 1e12, "peak": peaks["dfma_flops"] / 1e12,
-                "unit": "TFLOP/s"}
-    else:
-        roof = {"bound": "int64-mul", "achieved": mul64 / kernel_s / 1e12, "peak": peaks["mul64_per_s"] / 1e12,
-                "unit": "Tmul64/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
+    hbm_peak = 6532.5e9
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm_peak = float(json.load(fh)["hbm_gbs"]) * 1e9
+    except (OSError, KeyError, ValueError):
+        pass
+    bounds = {
+        "fp64": (fp64_flops / peaks["dfma_flops"], fp64_flops / kernel_s / 1e12, peaks["dfma_flops"] / 1e12, "TFLOP/s"),
+        "int64-mul": (mul64 / peaks["mul64_per_s"], mul64 / kernel_s / 1e12, peaks["mul64_per_s"] / 1e12, "Tmul64/s"),
+        "hbm": (hbm_bytes / hbm_peak, hbm_bytes / kernel_s / 1e9, hbm_peak / 1e9, "GB/s"),
+    }
+    name = max(bounds, key=lambda b: bounds[b][0])
+    t_ideal, achieved, peak, unit = bounds[name]
+    roof = {"bound": name, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak}
+    roof["t_ideal_ms_per_sweep"] = {b: v[0] * 1e3 for b, v in bounds.items()}
+    roof["staging_philox_draws"] = staged_made
     roof["traffic"] = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -275,13 +282,11 @@ def run_b200(args, world, rank, local):
         pass
     roof["peak_source"] = "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)"
     roof["work_per_sweep"] = {"replicates": ncells * (R if world == 1 else shard[1] - shard[0]),
-                              "attempts": attempts, "draws": draws, "moment_evals": evals,
+                              "attempts": attempts, "draws": draws, "staged_draws": staged, "moment_evals": evals,
                               "power_terms": terms, "ks_tail_endpoints": ks_tails,
                               "fp64_exp_dfma_equiv": exp_flops}
-    roof["kernel_ms_per_launch"] = kernel_ms / args.steps / launches
+    roof["kernel_ms_per_launch"] = kernel_ms / args.steps / max(launches, 1)
     roof["kernel_share_of_step"] = kernel_ms / total_ms
-    roof["t_ideal_fp64_ms"] = t_fp64 * 1e3 / launches
-    roof["t_ideal_int_ms"] = t_int * 1e3 / launches
 
     # end to end through the public API (host tables built + uploaded each step)
     e2e = None
@@ -331,7 +336,7 @@ def run_b200(args, world, rank, local):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * ncells * LAUNCHES_PER_CELL_REP,
+            "gpu_launches": timed_launches,
             "clocks": clock,
             "cutoffs_sample": {f"{g},{n}": rows[(g, n)] for g, n in ((1.5, 10), (2.5, 100), (3.5, 1000))},
         }

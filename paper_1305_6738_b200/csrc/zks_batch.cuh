@@ -60,6 +60,49 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   return s;
 }
 
+// The same draws from staged uniforms (row u of this replicate), warp-cooperative.
+__device__ __forceinline__ DrawStats draw_sample_staged(const ReplicateArgs& a, const double* __restrict__ u,
+                                                        const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
+  const int n = static_cast<int>(a.n);
+  const int nb = (n + 3) >> 2;
+  const bool two = a.guide_levels == 2;
+  double ls = 0.0;
+  uint32_t mn = 0xffffffffu, mx = 0;
+  // rows hold whole Philox blocks (the staging kernel writes all 4 words of the last block), so
+  // every block is one 32-byte load; the next block's load is issued before this one is used
+  double2 p0 = make_double2(1.0, 1.0), p1 = p0;
+  if (lane < nb) {
+    p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane));
+    p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane + 2));
+  }
+  for (int b = lane; b < nb; b += 32) {
+    bool vb[4];
+    uint32_t x[4];
+    const double uu[4] = {p0.x, p0.y, p1.x, p1.y};
+    if (b + 32 < nb) {
+      p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32)));
+      p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32) + 2));
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
+    draw_block_u(uu, vb, guide, a.cdf, a.L, two, x);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (vb[w]) {
+        ls += __ldg(a.logs + x[w]);
+        mn = min(mn, x[w]);
+        mx = max(mx, x[w]);
+      }
+    }
+    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
+  }
+  DrawStats s;
+  s.log_sum = warp_sum(ls);
+  s.vmin = warp_min_u32(mn);
+  s.vmax = warp_max_u32(mx);
+  return s;
+}
+
 // The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle).
 __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
                                                       const uint16_t* __restrict__ guide, uint16_t* v) {
@@ -152,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
   const double dn = static_cast<double>(a.n);
   const int B = a.batch;
   const uint64_t nbatches = (a.count + B - 1) / B;
-  Work wk{0, 0, 0, 0, 0, 0, 0, 0};
+  Work wk{};
   const ModelFns M{K, a.logs, a.fit, true};
 
   for (;;) {
@@ -183,7 +226,10 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     } else {
       for (int r = 0; r < nrep; ++r) {
         const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
-        const DrawStats st = draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
+        const DrawStats st =
+            a.ubuf ? draw_sample_staged(a, a.ubuf + (a.first + r0 + r - a.ubuf_first) * a.ubuf_stride, guide,
+                                        vals + r * a.vals_stride, lane)
+                   : draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
         if (lane == r) {
           my_ls = st.log_sum;
           my_min = st.vmin;
@@ -194,13 +240,17 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     __syncwarp();
     if (kCount) {
       wk.attempts += nrep;
-      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
+      const unsigned long long d = static_cast<unsigned long long>(nrep) * a.n;
+      if (a.ubuf && a.n >= kLaneDrawMaxN)
+        wk.staged += d;
+      else
+        wk.draws += d;
     }
 
     // 3. exponent fits, one replicate per lane
     double g = 0.0, norm = 1.0, target = 0.0;
     bool ok = false;
-    Work lw{0, 0, 0, 0, 0, 0, 0, 0};
+    Work lw{};
     if (active) {
       target = fit_target(my_ls, my_min, K, dn);
       ok = fit_exponent(M, target, lane, g, lw);
@@ -262,6 +312,35 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     for (int i = 0; i < kWorkFields; ++i)
       if (f[i]) atomicAdd(a.counters + i, f[i]);
   }
+}
+
+// Uniforms of replicate indices [first, first + count) of stream (seed, rep, .): row i holds the
+// n draws of index first + i (padded to `stride`), one warp per replicate.  Shared by every
+// cell of a sweep with the same (n, base_seed, repetition): build_table reuses base_seed for
+// all cells (montecarlo.py:276-277), so they consume identical streams.
+__global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t first,
+                                                             uint64_t count, int64_t n, int64_t stride, double* out,
+                                                             unsigned long long* counters) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t nb = (n + 3) >> 2;
+  unsigned long long made = 0;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < count; i += warps) {
+    uint64_t k0, k1;
+    stream_key(seed, rep, first + i, k0, k1);
+    double* row = out + i * stride;
+    for (int64_t b = lane; b < nb; b += 32) {
+      const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+      double4 q;
+      q.x = uniform_open_closed(r.w[0]);
+      q.y = uniform_open_closed(r.w[1]);
+      q.z = uniform_open_closed(r.w[2]);
+      q.w = uniform_open_closed(r.w[3]);
+      *reinterpret_cast<double4*>(row + 4 * b) = q;
+    }
+    made += 4 * nb;
+  }
+  if (counters && lane == 0 && made) atomicAdd(counters + kWorkFields, made);
 }
 
 }  // namespace zks

@@ -210,8 +210,51 @@ void zks_table_destroy(zks_table* t) {
   delete t;
 }
 
+namespace {
+struct Staged {
+  const double* u;
+  int64_t stride;
+  uint64_t first, count;
+  int64_t n;
+};
+int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
+                        uint8_t* st_dev, const Staged* staged);
+}  // namespace
+
 int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
                        uint8_t* st_dev) {
+  return run_replicates_impl(e, t, c, ks_dev, gh_dev, st_dev, nullptr);
+}
+
+int64_t zks_staging_stride(int64_t n) { return (n + 3) / 4 * 4; }
+
+int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64_t first, uint64_t count, int64_t n,
+                       double* u_dev) {
+  if (!e || !u_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)n);
+  if (count == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (int64_t)((count + 7) / 8)));
+  zks::stage_uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, repetition, first, count, n,
+                                                                     zks_staging_stride(n), u_dev, e->counters);
+  ZKS_CUDA(cudaGetLastError());
+  return ZKS_OK;
+}
+
+int zks_run_replicates_staged(zks_engine* e, const zks_table* t, const zks_cell* c, const double* u_dev,
+                              uint64_t u_first, uint64_t u_count, double* ks_dev, double* gh_dev, uint8_t* st_dev) {
+  if (!u_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (!c) return fail(ZKS_EINVAL, "cell is NULL");
+  const Staged s{u_dev, zks_staging_stride(c->n), u_first, u_count, c->n};
+  return run_replicates_impl(e, t, c, ks_dev, gh_dev, st_dev, &s);
+}
+
+}  // extern "C"
+
+namespace {
+
+int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
+                        uint8_t* st_dev, const Staged* staged) {
   if (!e || !t || !c) return fail(ZKS_EINVAL, "engine/table/cell is NULL");
   if (c->n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)c->n);
   if (c->support_k < 0 || c->support_k == 1 || c->support_k > 32766)
@@ -241,6 +284,17 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
   a.st_out = st_dev;
   a.work = e->work;
   a.counters = e->counters;
+  a.ubuf = nullptr;
+  a.ubuf_stride = 0;
+  a.ubuf_first = 0;
+  if (staged) {
+    if (c->first < staged->first || c->first + c->count > staged->first + staged->count || staged->n != c->n)
+      return fail(ZKS_EINVAL, "staged uniforms do not cover replicates [%llu, %llu) of n = %lld",
+                  (unsigned long long)c->first, (unsigned long long)(c->first + c->count), (long long)c->n);
+    a.ubuf = staged->u;
+    a.ubuf_stride = staged->stride;
+    a.ubuf_first = staged->first;
+  }
   a.use_table = e->mle_mode == ZKS_MLE_TABLE;
   if (a.use_table) {
     zks::FitTable* T = nullptr;
@@ -317,6 +371,10 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
   ZKS_CUDA(cudaGetLastError());
   return ZKS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
                            int32_t nranks, double* out_dev) {

@@ -117,22 +117,34 @@ __device__ __forceinline__ double em_block(const KsCtx& c, uint64_t v, double& f
   return integral + 0.5 * (c.fa + fv) + d1 / 12.0 - d3 / 720.0;
 }
 
+struct FlushTail {
+  double F_last;    // fitted cdf at the last scored value
+  uint32_t C_last;  // observations <= the last scored value
+};
+
 // score queue entries [0, cnt) lane-parallel (cnt <= 32)
 template <bool kArg>
-__device__ __forceinline__ void ks_flush(KsState& s, const KsCtx& c, int cnt, int lane, Work& wk) {
-  if (cnt <= 0) return;
+__device__ __forceinline__ FlushTail ks_flush(KsState& s, const KsCtx& c, int cnt, int lane, Work& wk) {
+  FlushTail ft{0.0, 0u};
+  if (cnt <= 0) return ft;
+  double Fv = 0.0;
+  uint32_t Ca = 0;
   if (lane < cnt) {
     const uint32_t v = c.qk[lane];
     const uint32_t before = c.qc[lane];
     const uint32_t here = c.qn[lane];
     double fv;
     const double Sv = s.S_head + em_block(c, v, fv);
-    const double Fv = Sv * c.inv;
+    Fv = Sv * c.inv;
+    Ca = before + here;
     const double Fp = (Sv - fv) * c.inv;
     take<kArg>(s, fabs(Fp - emp(c, before)), v - 1);  // k = v - 1 first (smaller k wins ties)
-    take<kArg>(s, fabs(Fv - emp(c, before + here)), v);
+    take<kArg>(s, fabs(Fv - emp(c, Ca)), v);
   }
   wk.ks_tails += cnt;
+  ft.F_last = __shfl_sync(0xffffffffu, Fv, cnt - 1);
+  ft.C_last = __shfl_sync(0xffffffffu, Ca, cnt - 1);
+  return ft;
 }
 
 // Tiles of 32 consecutive k in [k_first, k_last] with counts[k - base], above the head.
@@ -271,49 +283,97 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       __syncwarp();
       if (m <= kOverCap) {
         paged = false;
-        uint32_t r[kOverCap / 32];
+        constexpr int kSlots = kOverCap / 32;
+        uint32_t r[kSlots];  // element i = slot * 32 + lane
 #pragma unroll
-        for (int j = 0; j < kOverCap / 32; ++j) {
+        for (int j = 0; j < kSlots; ++j) {
           const uint32_t idx = j * 32 + lane;
           r[j] = idx < m ? queue[idx] : 0xffffffffu;
         }
         __syncwarp();
-        int ne = 0;
-        while (!s.done) {
-          uint32_t mn = 0xffffffffu;
+        // bitonic sort of the kOverCap values across the warp (padding 0xffffffff sorts last)
 #pragma unroll
-          for (int j = 0; j < kOverCap / 32; ++j) mn = min(mn, r[j]);
-          mn = warp_min_u32(mn);
-          if (mn == 0xffffffffu) break;
-          uint32_t cnt = 0;
+        for (int k = 2; k <= static_cast<int>(kOverCap); k <<= 1) {
 #pragma unroll
-          for (int j = 0; j < kOverCap / 32; ++j)
-            if (r[j] == mn) {
-              ++cnt;
-              r[j] = 0xffffffffu;
+          for (int jj = k >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+            for (int sl = 0; sl < kSlots; ++sl) {
+              const int i = sl * 32 + lane;
+              const bool up = (i & k) == 0;
+              if (jj >= 32) {
+                const int ps = sl ^ (jj >> 5);
+                if (ps > sl) {
+                  const uint32_t a0 = r[sl], a1 = r[ps];
+                  const bool sw = up ? a0 > a1 : a0 < a1;
+                  r[sl] = sw ? a1 : a0;
+                  r[ps] = sw ? a0 : a1;
+                }
+              } else {
+                const uint32_t o = __shfl_xor_sync(0xffffffffu, r[sl], jj);
+                const bool low = (lane & jj) == 0;
+                r[sl] = (low == up) ? min(r[sl], o) : max(r[sl], o);
+              }
             }
-          cnt = warp_sum_u32(cnt);
-          if (lane == 0) {
-            c.qk[ne] = mn;
-            c.qc[ne] = s.Cb;
-            c.qn[ne] = cnt;
           }
-          s.Cb += cnt;
-          if (++ne == 32) {
+        }
+        // runs of equal values: each run's last element becomes an endpoint entry
+        const unsigned lt = (1u << lane) - 1u;
+        int ne = 0;
+        uint32_t run_start = 0;  // prefix max of start indices, carried across slots
+        for (int sl = 0; sl < kSlots && !s.done; ++sl) {
+          const uint32_t v = r[sl];
+          const uint32_t i = sl * 32 + lane;
+          uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+          const uint32_t last_prev = sl ? __shfl_sync(0xffffffffu, r[sl > 0 ? sl - 1 : 0], 31) : 0u;
+          if (lane == 0) prev = sl ? last_prev : 0u;
+          uint32_t next = __shfl_down_sync(0xffffffffu, v, 1);
+          const uint32_t first_next = sl + 1 < kSlots ? __shfl_sync(0xffffffffu, r[sl + 1 < kSlots ? sl + 1 : sl], 0)
+                                                      : 0xffffffffu;
+          if (lane == 31) next = first_next;
+          const bool start = (i == 0) || v != prev;
+          uint32_t st_idx = start ? i : 0u;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, st_idx, o);
+            if (lane >= o) st_idx = max(st_idx, t);
+          }
+          st_idx = max(st_idx, run_start);
+          run_start = __shfl_sync(0xffffffffu, st_idx, 31);
+          const bool end = v != 0xffffffffu && v != next;
+          const unsigned em = __ballot_sync(0xffffffffu, end);
+          if (end) {
+            const int slot = ne + __popc(em & lt);
+            c.qk[slot] = v;
+            c.qc[slot] = s.Cb + st_idx;
+            c.qn[slot] = i - st_idx + 1;
+          }
+          ne += __popc(em);
+          __syncwarp();
+          if (ne >= 32) {
+            const FlushTail fl = ks_flush<kArg>(s, c, 32, lane, wk);
             __syncwarp();
-            ks_flush<kArg>(s, c, 32, lane, wk);
-            ne = 0;
+            uint32_t a0 = 0, a1 = 0, a2 = 0;
+            if (lane < ne - 32) {
+              a0 = c.qk[32 + lane];
+              a1 = c.qc[32 + lane];
+              a2 = c.qn[32 + lane];
+            }
+            __syncwarp();
+            if (lane < ne - 32) {
+              c.qk[lane] = a0;
+              c.qc[lane] = a1;
+              c.qn[lane] = a2;
+            }
+            ne -= 32;
             __syncwarp();
             s.Dw = warp_max(s.D);
-            if (s.Dw > 1.0 - emp(c, s.Cb) + kKsMargin) {
-              double fk;
-              const double F_pos = (s.S_head + em_block(c, mn, fk)) * c.inv;
-              if (s.Dw > fmax(1.0 - emp(c, s.Cb), 1.0 - F_pos) + kKsMargin) s.done = true;
-            }
+            // observations <= the last scored value, and F there, bound every later gap
+            if (s.Dw > fmax(1.0 - emp(c, fl.C_last), 1.0 - fl.F_last) + kKsMargin) s.done = true;
           }
         }
         __syncwarp();
         ks_flush<kArg>(s, c, ne, lane, wk);
+        s.Cb += m;
       }
     }
     uint64_t pa = H + 1;

@@ -56,6 +56,11 @@ struct ReplicateArgs {
   int batch;                     // replicates per warp batch (replicate_batch_kernel)
   int vals_stride;               // u16 sample slots per replicate in the batch store
   int guide_levels;              // 1, or 2 for long tables (L > 4096)
+  // staged uniforms (shared by the cells of a sweep with equal n and seed): u of replicate
+  // index i, draw j at ubuf[(i - ubuf_first) * ubuf_stride + j]; NULL = generate (Philox)
+  const double* ubuf;
+  int64_t ubuf_stride;
+  uint64_t ubuf_first;
 };
 
 // guide lookup: [lo, hi] brackets lower_bound(cdf, u)
@@ -87,13 +92,11 @@ __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restr
 
 // The four draws of one Philox block, their lower_bound searches interleaved so that up to four
 // independent cdf loads are in flight per lane.  Lanes with valid[w] false yield 0.
-__device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
-                                           const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
-  double u[4];
+__device__ __forceinline__ void draw_block_u(const double u[4], const bool valid[4], const uint16_t* __restrict__ guide,
+                                             const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
-    u[w] = uniform_open_closed(r.w[w]);
     guide_bracket(u[w], guide, two, lo[w], hi[w]);
     if (!valid[w]) hi[w] = lo[w];
   }
@@ -122,6 +125,14 @@ __device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4],
   }
 #pragma unroll
   for (int w = 0; w < 4; ++w) out[w] = valid[w] ? min(lo[w] + 1, L) : 0u;
+}
+
+__device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
+                                           const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
+  double u[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) u[w] = uniform_open_closed(r.w[w]);
+  draw_block_u(u, valid, guide, cdf, L, two, out);
 }
 
 struct SampleStats {
@@ -319,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
   uint16_t* slab = a.slab ? a.slab + gw * a.slab_cap : nullptr;
   const int K = a.K;
   const double dn = static_cast<double>(a.n);
-  Work wk{0, 0, 0, 0, 0, 0, 0, 0};
+  Work wk{};
   const ModelFns M{K, a.logs, a.fit, a.use_table != 0};
 
   for (;;) {

@@ -65,6 +65,7 @@ class Engine:
         self.handle = handle
         self._tables: OrderedDict[tuple, DrawTable] = OrderedDict()
         self._lock = threading.Lock()
+        self.launches = 0  # kernels this engine has launched (bench.py reports the timed-region delta)
 
     # -- streams -------------------------------------------------------------
     def bind_stream(self):
@@ -87,6 +88,7 @@ class Engine:
                 self._tables.move_to_end(key)
                 return t
             t = DrawTable(self, cdf_builder())
+            self.launches += 1  # guide table
             self._tables[key] = t
             while len(self._tables) > 64:
                 _, old = self._tables.popitem(last=False)
@@ -108,11 +110,33 @@ class Engine:
             count=int(count),
         )
         self.bind_stream()
+        self.launches += 1
         _native.check(
             self.lib.zks_run_replicates(
                 self.handle, table.handle, ctypes.byref(cell), ks.data_ptr(), gamma_hat.data_ptr(), status.data_ptr()
             )
         )
+
+    def staging_stride(self, n: int) -> int:
+        return int(self.lib.zks_staging_stride(int(n)))
+
+    def stage_uniforms(self, seed: int, repetition: int, first: int, count: int, n: int, out) -> None:
+        """Uniform rows of replicate indices [first, first+count) into device float64 ``out``."""
+        self.bind_stream()
+        self.launches += 1
+        _native.check(self.lib.zks_stage_uniforms(self.handle, int(seed), int(repetition), int(first), int(count),
+                                                  int(n), out.data_ptr()))
+
+    def run_replicates_staged(self, table: DrawTable, support_k, gamma, n, base_seed, repetition, first, count,
+                              u, u_first, u_count, ks, gamma_hat, status) -> None:
+        cell = _native.ZksCell(support_k=0 if support_k is None else int(support_k), reserved=0, gamma=float(gamma),
+                               n=int(n), base_seed=int(base_seed), repetition=int(repetition), first=int(first),
+                               count=int(count))
+        self.bind_stream()
+        self.launches += 1
+        _native.check(self.lib.zks_run_replicates_staged(self.handle, table.handle, ctypes.byref(cell), u.data_ptr(),
+                                                         int(u_first), int(u_count), ks.data_ptr(),
+                                                         gamma_hat.data_ptr(), status.data_ptr()))
 
     def select_ranks(self, values, ranks: list[int], out=None):
         """Order statistics of a device float64 tensor at zero-based ranks.
@@ -122,6 +146,7 @@ class Engine:
         """
         r = np.ascontiguousarray(ranks, dtype=np.int64)
         self.bind_stream()
+        self.launches += 9  # init + 8 radix passes
         if out is not None:
             _native.check(
                 self.lib.zks_select_ranks_async(self.handle, values.data_ptr(), values.numel(), r.ctypes.data, r.size,

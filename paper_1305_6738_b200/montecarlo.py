@@ -265,6 +265,83 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
     plan.finished.record(stream)
 
 
+_STAGE_MIN_N, _STAGE_MAX_N = 128, 1024  # n range where the batch kernel reads staged uniforms
+_STAGE_BYTES = 2 << 30                   # staging buffer budget
+
+
+def _stage_key(cfg: SimulationConfig):
+    return (cfg.support.k, cfg.n, cfg.base_seed, cfg.replicates, cfg.repetitions, cfg.quantiles)
+
+
+def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
+    """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
+
+    build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
+    equal n draw from identical uniforms: they are generated once per chunk of replicate
+    indices (zks_stage_uniforms) and every cell's replicate kernel reads them.  Results are
+    identical to running the cells one by one.
+    """
+    torch = _torch()
+    cfg0 = plans[0].config
+    n = cfg0.n
+    if len(plans) < 2 or not _STAGE_MIN_N <= n <= _STAGE_MAX_N:
+        for plan in plans:
+            _enqueue_cell(eng, plan, shard=shard, gather=gather, kernel_events=kernel_events)
+        return
+    total = cfg0.replicates
+    first, stop = shard if shard is not None else (0, total)
+    dev = f"cuda:{eng.device}"
+    ranks = quantile_ranks(total, cfg0.quantiles)
+    stride = eng.staging_stride(n)
+    chunk = max(1, min(stop - first, _STAGE_BYTES // (8 * stride)))
+    key = ("stage", eng.device)
+    ubuf = _SLABS.get(key)
+    if ubuf is None or ubuf.numel() < chunk * stride:
+        ubuf = torch.empty(chunk * stride, dtype=torch.float64, device=dev)
+        _SLABS[key] = ubuf
+    outs = []
+    stream = eng.bind_stream()
+    for plan in plans:
+        plan.quantiles = torch.empty((cfg0.repetitions, len(ranks)), dtype=torch.float64, device=dev)
+        plan.worst = torch.zeros(cfg0.repetitions, dtype=torch.uint8, device=dev)
+        plan.started = torch.cuda.Event(enable_timing=True)
+        plan.finished = torch.cuda.Event(enable_timing=True)
+        plan.started.record(stream)
+        outs.append(_Slab(eng, max(total, 1)))
+    tables = [_table(eng, p.config) for p in plans]
+    for rep in range(cfg0.repetitions):
+        for c0 in range(first, stop, chunk):
+            cnt = min(chunk, stop - c0)
+            eng.stage_uniforms(cfg0.base_seed, rep, c0, cnt, n, ubuf)
+            for plan, table, out in zip(plans, tables, outs):
+                cfg = plan.config
+                if kernel_events is not None:
+                    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    k0.record(stream)
+                eng.run_replicates_staged(table, cfg.support.k, cfg.gamma, n, cfg.base_seed, rep, c0, cnt, ubuf, c0,
+                                          cnt, out.ks[c0:], out.gh[c0:], out.st[c0:])
+                if kernel_events is not None:
+                    k1.record(stream)
+                    kernel_events.append((k0, k1))
+        for plan, out in zip(plans, outs):
+            if stop > first:
+                plan.worst[rep] = out.st[first:stop].max()
+            ks = out.ks[:total] if gather is None else gather(out.ks)[:total]
+            for i in range(0, len(ranks), 16):
+                eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+    for plan in plans:
+        plan.finished.record(stream)
+
+
+def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
+    """Queue many cells, grouping those that can share uniform streams (_enqueue_group)."""
+    groups: dict = {}
+    for plan in plans:
+        groups.setdefault(_stage_key(plan.config), []).append(plan)
+    for group in groups.values():
+        _enqueue_group(eng, group, shard=shard, gather=gather, kernel_events=kernel_events)
+
+
 def _finish_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None) -> list[tuple[float, float]]:
     cfg = plan.config
     worst = plan.worst.cpu().numpy()
@@ -368,8 +445,7 @@ def build_table(
                 raise SimulationError(f"table cell (gamma={gamma}, n={n}) failed: {err}") from err
             plans.append(_CellPlan(cfg))
     eng = _engine()
-    for plan in plans:
-        _enqueue_cell(eng, plan)
+    _enqueue_plans(eng, plans)
     cells: dict[tuple[float, int], tuple[float, ...]] = {}
     for plan in plans:
         cfg = plan.config

@@ -25,7 +25,7 @@ from .montecarlo import (
     SimulationError,
     _CellPlan,
     _engine,
-    _enqueue_cell,
+    _enqueue_plans,
     _finish_cell,
     _slab,
     _validate_levels,
@@ -105,8 +105,7 @@ def build_table(
     shard = shard_bounds(replicates, world, rank)
     gather = ShardGather(replicates, world, rank, group)
     _slab(eng, padded_size(replicates, world))
-    for plan in plans:
-        _enqueue_cell(eng, plan, shard=shard, gather=gather)
+    _enqueue_plans(eng, plans, shard=shard, gather=gather)
     worst = torch.stack([p.worst.max() for p in plans]).to(torch.int32)
     dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
     for plan, w in zip(plans, worst.tolist()):

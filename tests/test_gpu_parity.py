@@ -201,6 +201,23 @@ def test_build_table_matches_run_simulation(zk):
                        repetitions=1)
 
 
+def test_sweep_with_shared_uniforms_matches_cells(zk):
+    # build_table stages one uniform stream per (n, repetition) for all gammas (n in [128, 1024]);
+    # every cell must equal its own run_simulation bit for bit
+    table = zk.build_table(ns=(200, 700), gammas=(1.6, 2.2, 3.0), support=zk.Support.unbounded(), base_seed=3,
+                           replicates=3000, repetitions=2)
+    for (g, n), row in table.cells.items():
+        cfg = zk.SimulationConfig(n=n, support=zk.Support.unbounded(), gamma=g, base_seed=3, replicates=3000,
+                                  repetitions=2)
+        assert row == tuple(c for _, c in zk.run_simulation(cfg)), (g, n)
+    t2 = zk.build_table(ns=(300,), gammas=(0.5, 1.5), support=zk.Support.finite(1000), base_seed=8,
+                        replicates=2000, repetitions=1)
+    for (g, n), row in t2.cells.items():
+        cfg = zk.SimulationConfig(n=n, support=zk.Support.finite(1000), gamma=g, base_seed=8, replicates=2000,
+                                  repetitions=1)
+        assert row == tuple(c for _, c in zk.run_simulation(cfg)), (g, n)
+
+
 def test_large_n_config4_sample_properties(zk):
     # BASELINE config 4 shape at n = 10^6: size-independent checks (range, determinism)
     ks1, gh1, st1 = run_cell(None, 2.0, 1_000_000, 1, 0, 0, 8)
