@@ -176,6 +176,21 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
   return ko.D;
 }
 
+// KS from pre-drawn head counts (values 1..kKsHead) and the list of values above kKsHead.
+__device__ __forceinline__ double ks_from_head_tail(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
+                                                    uint32_t* hist, uint32_t* queue, const uint32_t* head,
+                                                    const uint16_t* tail, uint32_t m, int lane, Work& wk) {
+  hist[lane + 1] = head[lane];
+  hist[lane + 33] = head[lane + 32];
+  __syncwarp();
+  KsParams p = ks_params(a);
+  p.H = kKsHead;
+  p.P = static_cast<uint32_t>(a.pre_page);
+  const KsOut ko = ks_scan<uint16_t, false>(p, g, norm, kmax, hist, tail, m, queue, lane, wk);
+  clear_hist(hist, ko.used_pages ? a.hist_words : round_up(static_cast<int>(kKsHead) + 1, 4), lane);
+  return ko.D;
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -223,6 +238,14 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
         my_min = st.vmin;
         my_max = st.vmax;
       }
+    } else if (a.pre_head) {
+      // drawn by draw_stats_kernel: only the per-replicate statistics are read here
+      if (active) {
+        const uint64_t row = a.first + r0 + lane - a.pre_first;
+        my_ls = a.pre_ls[row];
+        my_min = a.pre_min[row];
+        my_max = a.pre_max[row];
+      }
     } else {
       for (int r = 0; r < nrep; ++r) {
         const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
@@ -241,7 +264,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     if (kCount) {
       wk.attempts += nrep;
       const unsigned long long d = static_cast<unsigned long long>(nrep) * a.n;
-      if (a.ubuf && a.n >= kLaneDrawMaxN)
+      if (a.pre_head && a.n >= kLaneDrawMaxN)
+        ;  // counted by draw_stats_kernel
+      else if (a.ubuf && a.n >= kLaneDrawMaxN)
         wk.staged += d;
       else
         wk.draws += d;
@@ -270,7 +295,14 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, my_max, r);
-      const double ks = ks_from_sample(a, gr, nr, kmax, hist, queue, vals + r * a.vals_stride, lane, wk);
+      double ks;
+      if (a.pre_head && a.n >= kLaneDrawMaxN) {
+        const uint64_t row = a.first + r0 + r - a.pre_first;
+        ks = ks_from_head_tail(a, gr, nr, kmax, hist, queue, a.pre_head + row * kKsHead,
+                               a.pre_tail + row * a.vals_stride, a.pre_m[row], lane, wk);
+      } else {
+        ks = ks_from_sample(a, gr, nr, kmax, hist, queue, vals + r * a.vals_stride, lane, wk);
+      }
       if (lane == r) my_ks = ks;
     }
 
@@ -341,6 +373,111 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
     made += 4 * nb;
   }
   if (counters && lane == 0 && made) atomicAdd(counters + kWorkFields, made);
+}
+
+// The draw phase on its own, at high occupancy: one warp per replicate of [first, first+count)
+// draws its sample and writes what the fit and the KS scan need -- log-sum, min, max, the counts
+// of the values 1..kKsHead and the list of values above it -- so replicate_batch_kernel (with
+// a.pre_head) never touches the n draws again.  Uniforms from Philox, or from a staged sweep
+// buffer (a.ubuf).
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads, 4) draw_stats_kernel(ReplicateArgs a, uint32_t* head_out,
+                                                                 uint16_t* tail_out, uint32_t* m_out, double* ls_out,
+                                                                 uint32_t* min_out, uint32_t* max_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
+  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* bins = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * (kKsHead + 1);
+  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  for (int i = lane; i <= static_cast<int>(kKsHead); i += 32) bins[i] = 0u;
+  __syncthreads();
+  const bool two = a.guide_levels == 2;
+  const int n = static_cast<int>(a.n);
+  const int nb = (n + 3) >> 2;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  unsigned long long philox = 0, staged = 0;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.count; i += warps) {
+    const uint64_t idx = a.first + i;
+    uint16_t* tail = tail_out + i * a.vals_stride;
+    uint64_t k0 = 0, k1 = 0;
+    const double* u = nullptr;
+    if (a.ubuf) {
+      u = a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride;
+      staged += n;
+    } else {
+      stream_key(a.seed, a.rep, idx, k0, k1);
+      philox += n;
+    }
+    double ls = 0.0;
+    uint32_t mn = 0xffffffffu, mx = 0, m = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      bool vb[4];
+      uint32_t x[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
+      if (u) {
+        double uu[4] = {1.0, 1.0, 1.0, 1.0};
+        if (b < nb) {
+          const double2 q0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * b));
+          const double2 q1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * b + 2));
+          uu[0] = q0.x;
+          uu[1] = q0.y;
+          uu[2] = q1.x;
+          uu[3] = q1.y;
+        }
+        draw_block_u(uu, vb, guide, a.cdf, a.L, two, x);
+      } else {
+        const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+        draw_block(r, vb, guide, a.cdf, a.L, two, x);
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t v = x[w];
+        if (vb[w]) {
+          ls += __ldg(a.logs + v);
+          mn = min(mn, v);
+          mx = max(mx, v);
+          c1 += v == 1u;
+          c2 += v == 2u;
+          c3 += v == 3u;
+          c4 += v == 4u;
+          if (v > 4u && v <= kKsHead) atomicAdd(bins + v, 1u);
+        }
+        const bool big = vb[w] && v > kKsHead;
+        const unsigned bm = __ballot_sync(0xffffffffu, big);
+        if (big) tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+        m += __popc(bm);
+      }
+    }
+    ls = warp_sum(ls);
+    mn = warp_min_u32(mn);
+    mx = warp_max_u32(mx);
+    c1 = warp_sum_u32(c1);
+    c2 = warp_sum_u32(c2);
+    c3 = warp_sum_u32(c3);
+    c4 = warp_sum_u32(c4);
+    __syncwarp();
+    uint32_t* head = head_out + i * kKsHead;  // head[k - 1] = count of value k
+    const uint32_t h0 = bins[lane + 1], h1 = bins[lane + 33];
+    head[lane] = lane == 0 ? c1 : lane == 1 ? c2 : lane == 2 ? c3 : lane == 3 ? c4 : h0;
+    head[lane + 32] = h1;
+    bins[lane + 1] = 0u;
+    bins[lane + 33] = 0u;
+    __syncwarp();
+    if (lane == 0) {
+      ls_out[i] = ls;
+      min_out[i] = mn;
+      max_out[i] = mx;
+      m_out[i] = m;
+    }
+  }
+  if (kCount && lane == 0) {
+    if (philox) atomicAdd(a.counters + 1, philox);
+    if (staged) atomicAdd(a.counters + 8, staged);
+  }
 }
 
 }  // namespace zks

@@ -41,6 +41,7 @@ constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory ca
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
 constexpr int64_t kBatchMaxN = 1024;                  // n up to which replicate_batch_kernel runs
+constexpr uint64_t kPreBytes = uint64_t(1) << 30;     // pre-drawn rows per chunk (bytes)
 constexpr uint32_t kBatchHist = 512;                  // its per-warp histogram bins
 
 }  // namespace
@@ -64,6 +65,8 @@ struct zks_engine {
   int mle_mode = ZKS_MLE_TABLE;
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
+  void* pre = nullptr;  // pre-drawn sample rows + their statistics (two-kernel path)
+  size_t pre_bytes = 0;
 };
 
 namespace {
@@ -141,6 +144,7 @@ void zks_engine_destroy(zks_engine* e) {
   cudaFree(e->slab);
   cudaFree(e->sel);
   cudaFree(e->sel_out);
+  if (e->pre) cudaFree(e->pre);
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
   for (int i = 0; i < kStagingSlots; ++i)
@@ -365,6 +369,71 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     }
     a.slab = e->slab;
     a.slab_cap = c->n;
+  }
+  a.pre_head = nullptr;
+  a.pre_tail = nullptr;
+  a.pre_m = nullptr;
+  a.pre_ls = nullptr;
+  a.pre_min = nullptr;
+  a.pre_max = nullptr;
+  a.pre_first = 0;
+  a.pre_page = a.H;
+  if (batched && c->n >= zks::kLaneDrawMaxN) {
+    // draw phase in its own high-occupancy kernel (head counts + tail values per replicate),
+    // chunk by chunk, then fit + score
+    const uint64_t row_bytes = uint64_t(a.vals_stride) * 2 + zks::kKsHead * 4 + 24;
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, kPreBytes / row_bytes));
+    const size_t need = size_t(chunk) * row_bytes;
+    if (need > e->pre_bytes) {
+      if (e->pre) ZKS_CUDA(cudaFreeAsync(e->pre, e->stream));
+      e->pre = nullptr;
+      e->pre_bytes = 0;
+      ZKS_CUDA(cudaMallocAsync(&e->pre, need, e->stream));
+      e->pre_bytes = need;
+    }
+    double* pls = reinterpret_cast<double*>(e->pre);
+    uint32_t* pmin = reinterpret_cast<uint32_t*>(pls + chunk);
+    uint32_t* pmax = pmin + chunk;
+    uint32_t* pm = pmax + chunk;
+    uint32_t* phead = pm + chunk;
+    uint16_t* ptail = reinterpret_cast<uint16_t*>(phead + chunk * zks::kKsHead);
+    auto draw = counting ? zks::draw_stats_kernel<true> : zks::draw_stats_kernel<false>;
+    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * (zks::kKsHead + 1) * 4;
+    {
+      const auto key = std::make_pair(reinterpret_cast<const void*>(draw), dsmem);
+      if (e->occupancy.find(key) == e->occupancy.end()) {
+        int optin = 0, per = 0;
+        ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+        ZKS_CUDA(cudaFuncSetAttribute(draw, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, draw, zks::kThreads, dsmem));
+        e->occupancy.emplace(key, std::max(per, 1));
+      }
+    }
+    const int dper = e->occupancy[std::make_pair(reinterpret_cast<const void*>(draw), dsmem)];
+    zks::ReplicateArgs sub = a;
+    for (uint64_t off = 0; off < c->count; off += chunk) {
+      const uint64_t cnt = std::min<uint64_t>(chunk, c->count - off);
+      sub.first = c->first + off;
+      sub.count = cnt;
+      sub.ks_out = ks_dev + off;
+      sub.gh_out = gh_dev + off;
+      sub.st_out = st_dev + off;
+      sub.pre_head = phead;
+      sub.pre_tail = ptail;
+      sub.pre_m = pm;
+      sub.pre_ls = pls;
+      sub.pre_min = pmin;
+      sub.pre_max = pmax;
+      sub.pre_first = sub.first;
+      const int64_t dblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)((cnt + 7) / 8)));
+      draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(sub, phead, ptail, pm, pls, pmin, pmax);
+      ZKS_CUDA(cudaGetLastError());
+      const int64_t fblocks = std::min<int64_t>(blocks, (int64_t)((cnt + per_block - 1) / per_block));
+      ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+      kernel<<<(unsigned)std::max<int64_t>(fblocks, 1), zks::kThreads, smem, e->stream>>>(sub);
+      ZKS_CUDA(cudaGetLastError());
+    }
+    return ZKS_OK;
   }
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
   kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);

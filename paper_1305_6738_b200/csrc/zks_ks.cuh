@@ -49,9 +49,10 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 struct KsParams {
   int64_t n;
   uint32_t H;          // histogram bins held in `hist` (values 1..H)
-  int hist_words;      // words of `hist` (>= H + 1, multiple of 4)
+  int hist_words;      // words of `hist` (>= max(H, P) + 1, multiple of 4)
   const double* logs;  // ln k, k = 0..65536
   bool exact;          // reference-exact forms (user-sample API)
+  uint32_t P = 0;      // page bins for values above H when they are many (0 = H)
 };
 
 struct KsOut {
@@ -223,6 +224,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
   c.qc = queue + kKsQueue;
   c.qn = queue + 2 * kKsQueue;
   const uint64_t H = p.H;
+  const uint64_t P = p.P ? p.P : p.H;
   KsState s{};
   s.kb = 0xffffffffu;
   KsOut out{0.0, 0u, false};
@@ -379,7 +381,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     uint64_t pa = H + 1;
     while (paged && !s.done && pa <= kmax) {
       out.used_pages = true;
-      const uint64_t pb = pa + H - 1 < kmax ? pa + H - 1 : kmax;
+      const uint64_t pb = pa + P - 1 < kmax ? pa + P - 1 : kmax;
       // page histogram of the values in [pa, pb]; next occupied value above pb
       for (int i = lane; i < p.hist_words; i += 32) hist[i] = 0u;
       __syncwarp();
