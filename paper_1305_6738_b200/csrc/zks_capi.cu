@@ -279,6 +279,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.hist_words = zks::round_up(std::max(a.H, 4) + 1, 4);
   a.gamma = c->gamma;
   a.n = c->n;
+  a.inv_n = 1.0 / static_cast<double>(c->n);
   a.seed = c->base_seed;
   a.rep = c->repetition;
   a.first = c->first;

@@ -53,6 +53,7 @@ struct KsParams {
   const double* logs;  // ln k, k = 0..65536
   bool exact;          // reference-exact forms (user-sample API)
   uint32_t P = 0;      // page bins for values above H when they are many (0 = H)
+  double inv_n = 0.0;  // 1/n when the caller has it (0 = divide here)
 };
 
 struct KsOut {
@@ -217,7 +218,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
   c.g = g;
   c.inv = 1.0 / norm;
   c.dn = static_cast<double>(p.n);
-  c.inv_n = 1.0 / c.dn;
+  c.inv_n = p.inv_n > 0.0 ? p.inv_n : 1.0 / c.dn;
   c.exact = p.exact;
   c.logs = p.logs;
   c.qk = queue;
@@ -406,6 +407,10 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     ks_flush<kArg>(s, c, q, lane, wk);
   }
   // warp result: max gap, smallest k among equal maxima
+  if (!kArg) {
+    out.D = warp_max(s.D);
+    return out;
+  }
   double D = s.D;
   uint32_t kb = s.kb;
 #pragma unroll

@@ -72,6 +72,7 @@ struct ReplicateArgs {
   const uint32_t* pre_max;
   uint64_t pre_first;
   int pre_page;  // page bins for long tails (histogram capacity)
+  double inv_n;  // 1 / n
 };
 
 // guide lookup: [lo, hi] brackets lower_bound(cdf, u)
@@ -323,6 +324,7 @@ __device__ __forceinline__ KsParams ks_params(const ReplicateArgs& a) {
   p.hist_words = a.hist_words;
   p.logs = a.logs;
   p.exact = false;
+  p.inv_n = a.inv_n;
   return p;
 }
 
