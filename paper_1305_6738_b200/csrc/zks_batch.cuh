@@ -191,6 +191,47 @@ __device__ __forceinline__ double ks_from_head_tail(const ReplicateArgs& a, doub
   return ko.D;
 }
 
+constexpr int kLaneHistWords = (kKsHead + 1) * 32 / 4;  // u8 counts [value 0..64][lane]
+
+// Lane-parallel KS for small samples: lane r builds a private u8 histogram of its values <= kKsHead
+// (value-major, so a warp's lanes touch neighbouring bytes) and walks k = 1..min(kmax, kKsHead)
+// with the dense form F(k) = S(k)/norm, S the running sum of k^-g in the reference's order.
+// Returns true when the replicate is fully scored (kmax <= kKsHead, or the exit bound held
+// before kKsHead); otherwise the caller scores it warp-cooperatively.
+__device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, double g, double norm, uint32_t kmax,
+                                             uint8_t* lh, const uint16_t* v, double& ks) {
+  const int lane = threadIdx.x & 31;
+  const int n = static_cast<int>(a.n);
+  if (on) {
+    for (int j = 0; j < n; ++j) {
+      const uint32_t x = v[j];
+      if (x <= kKsHead) ++lh[x * 32 + lane];
+    }
+  }
+  const uint32_t end = kmax < kKsHead ? kmax : kKsHead;
+  const double inv = 1.0 / norm;
+  double S = 0.0, D = 0.0;
+  uint32_t C = 0;
+  bool live = on;
+  bool done = false;
+  for (uint32_t k = 1; __any_sync(0xffffffffu, live && k <= end); ++k) {
+    if (live && k <= end) {
+      S += exp(-g * __ldg(a.logs + k));
+      C += lh[k * 32 + lane];
+      const double F = S * inv, E = static_cast<double>(C) * a.inv_n;
+      D = fmax(D, fabs(F - E));
+      if (D > fmax(1.0 - E, 1.0 - F) + kKsMargin) {
+        done = true;
+        live = false;
+      }
+    }
+  }
+  done = done || kmax <= kKsHead;
+  if (on && done) ks = D;
+  __syncwarp();
+  return on && done;
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -290,8 +331,15 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
 
     // 4. KS statistics
     double my_ks = __longlong_as_double(0x7ff8000000000000ll);
+    bool scored = false;
+    if (a.n < kLaneDrawMaxN) {
+      // small samples: each lane scores its own replicate over k = 1..min(kmax, kKsHead)
+      scored = ks_lane_head(a, ok && active, g, norm, my_max, reinterpret_cast<uint8_t*>(hist),
+                            vals + lane * a.vals_stride, my_ks);
+      clear_hist(hist, a.hist_words, lane);
+    }
     for (int r = 0; r < nrep; ++r) {
-      if (!__shfl_sync(0xffffffffu, ok, r)) continue;
+      if (!__shfl_sync(0xffffffffu, ok && !scored, r)) continue;
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, my_max, r);

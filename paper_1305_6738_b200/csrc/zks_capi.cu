@@ -320,7 +320,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   if (batched) {
     // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
     a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
-    a.hist_words = zks::round_up(std::max(a.H, 4) + 1, 4);
+    a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
     a.batch = std::min(32, zks::kBatchVals / a.vals_stride);
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
