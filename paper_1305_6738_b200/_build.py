@@ -11,7 +11,7 @@ HEADERS = [
     os.path.join(HERE, "csrc", f)
     for f in ("zks_stream.cuh", "zks_series.cuh", "zks_replicate.cuh", "zks_select.cuh", "zks_probe.cuh", "zks_fit.cuh", "zks_batch.cuh", "zks_ks.cuh", "zks_samples.cuh")
 ] + [os.path.join(os.path.dirname(HERE), "include", "zipfks_b200.h")]
-LIB = os.path.join(HERE, "libzks_b200.so")
+LIB = os.environ.get("ZKS_LIB") or os.path.join(HERE, "libzks_b200.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -39,7 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    extra = os.environ.get("ZKS_NVCC_EXTRA", "").split()  # tuning experiments, e.g. -DZKS_DRAW_MINB=3
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

@@ -18,6 +18,9 @@ namespace zks {
 #ifndef ZKS_BATCH_MINB
 #define ZKS_BATCH_MINB 2
 #endif
+#ifndef ZKS_DRAW_MINB
+#define ZKS_DRAW_MINB 4
+#endif
 #ifndef ZKS_BATCH_VALS
 #define ZKS_BATCH_VALS 4096
 #endif
@@ -42,7 +45,7 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
     uint32_t x[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, x);
+    draw_block(r, vb, guide, a, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -85,7 +88,7 @@ __device__ __forceinline__ DrawStats draw_sample_staged(const ReplicateArgs& a, 
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block_u(uu, vb, guide, a.cdf, a.L, two, x);
+    draw_block_u(uu, vb, guide, a, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -116,7 +119,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
     uint32_t x[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, x);
+    draw_block(r, vb, guide, a, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -428,22 +431,36 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // of the values 1..kKsHead and the list of values above it -- so replicate_batch_kernel (with
 // a.pre_head) never touches the n draws again.  Uniforms from Philox, or from a staged sweep
 // buffer (a.ubuf).
+//
+// Values 1..4 are counted without a search: with h = cdf[0..3] in the kernel parameters,
+// #{u > h_j} over the sample gives the counts by differences (lower_bound semantics; h_j = +inf
+// from L-1 on clamps to L, distribution.py:200-201).  Draws with u > h_3 -- 5 % of them at
+// gamma = 2.5, 36 % at 1.5 -- are pushed onto a warp queue and resolved 32 at a time by the
+// guide + cdf search with every lane busy, so divergence costs nothing.
+constexpr int kDrawQueue = 160;  // doubles per warp: < 32 left over + 4 x 32 pushed per step
+constexpr int kDrawWarpBytes = (kKsHead + 1) * 32 + kDrawQueue * 8;  // u8 bins [v][lane] + queue
+
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads, 4) draw_stats_kernel(ReplicateArgs a, uint32_t* head_out,
+__global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(ReplicateArgs a, uint32_t* head_out,
                                                                  uint16_t* tail_out, uint32_t* m_out, double* ls_out,
                                                                  uint32_t* min_out, uint32_t* max_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* bins = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * (kKsHead + 1);
+  unsigned char* wbase = smem + guide_bytes + warp * kDrawWarpBytes;
+  // lane-private u8 counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
+  // most one queued draw per pop and there are <= n/32 + 1 <= 33 pops, so u8 cannot overflow
+  uint8_t* bins = wbase;
+  double* queue = reinterpret_cast<double*>(wbase + (kKsHead + 1) * 32);
   for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
-  for (int i = lane; i <= static_cast<int>(kKsHead); i += 32) bins[i] = 0u;
+  for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const bool two = a.guide_levels == 2;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   const unsigned lt = (1u << lane) - 1u;
+  const double h0 = a.cdf_head[0], h1 = a.cdf_head[1], h2 = a.cdf_head[2], h3 = a.cdf_head[3];
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   unsigned long long philox = 0, staged = 0;
   for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.count; i += warps) {
@@ -459,62 +476,129 @@ __global__ void __launch_bounds__(kThreads, 4) draw_stats_kernel(ReplicateArgs a
       philox += n;
     }
     double ls = 0.0;
-    uint32_t mn = 0xffffffffu, mx = 0, m = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    uint32_t mn = 0xffffffffu, mx = 0, m = 0;
+    uint32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0;  // this lane's #{u > h_j}
+    int qn = 0;                               // queued draws (warp-uniform)
+    // one queued draw per lane: value by guide + search, then bin / tail
+    auto resolve = [&](double ur, bool ok) {
+      uint32_t lo, hi;
+      guide_bracket(ur, guide, two, lo, hi);
+      if (!ok) hi = lo;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a.cdf + mid) >= ur)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      const uint32_t v = min(lo + 1, a.L);
+      if (ok) {
+        mn = min(mn, v);
+        mx = max(mx, v);
+        if (v <= kKsHead) ++bins[v * 32 + lane];
+      }
+      const bool big = ok && v > kKsHead;
+      const unsigned bm = __ballot_sync(0xffffffffu, big);
+      if (big) {
+        tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+        ls += __ldg(a.logs + v);
+      }
+      m += __popc(bm);
+    };
+    // staged rows: the next block's 32-byte load is issued before this block is used
+    double2 p0 = make_double2(0.0, 0.0), p1 = p0;
+    if (u && lane < nb) {
+      p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane));
+      p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane + 2));
+    }
     for (int b0 = 0; b0 < nb; b0 += 32) {
       const int b = b0 + lane;
-      bool vb[4];
-      uint32_t x[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
+      double uu[4];
       if (u) {
-        double uu[4] = {1.0, 1.0, 1.0, 1.0};
-        if (b < nb) {
-          const double2 q0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * b));
-          const double2 q1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * b + 2));
-          uu[0] = q0.x;
-          uu[1] = q0.y;
-          uu[2] = q1.x;
-          uu[3] = q1.y;
+        uu[0] = p0.x;
+        uu[1] = p0.y;
+        uu[2] = p1.x;
+        uu[3] = p1.y;
+        if (b + 32 < nb) {
+          p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32)));
+          p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32) + 2));
+        } else {
+          p0 = p1 = make_double2(0.0, 0.0);
         }
-        draw_block_u(uu, vb, guide, a.cdf, a.L, two, x);
       } else {
         const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
-        draw_block(r, vb, guide, a.cdf, a.L, two, x);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) uu[w] = uniform_open_closed(r.w[w]);
+      }
+      if (4 * b + 4 > n) {  // past the sample: u = 0 counts nowhere (value 1 is n - #{u > h_0})
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (4 * b + w >= n) uu[w] = 0.0;
       }
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const uint32_t v = x[w];
-        if (vb[w]) {
-          ls += __ldg(a.logs + v);
-          mn = min(mn, v);
-          mx = max(mx, v);
-          c1 += v == 1u;
-          c2 += v == 2u;
-          c3 += v == 3u;
-          c4 += v == 4u;
-          if (v > 4u && v <= kKsHead) atomicAdd(bins + v, 1u);
-        }
-        const bool big = vb[w] && v > kKsHead;
+        g0 += uu[w] > h0;
+        g1 += uu[w] > h1;
+        g2 += uu[w] > h2;
+        const bool big = uu[w] > h3;
+        g3 += big;
         const unsigned bm = __ballot_sync(0xffffffffu, big);
-        if (big) tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
-        m += __popc(bm);
+        if (big) queue[qn + __popc(bm & lt)] = uu[w];
+        qn += __popc(bm);
+      }
+      __syncwarp();
+      while (qn >= 32) {
+        qn -= 32;
+        const double ur = queue[qn + lane];
+        __syncwarp();
+        resolve(ur, true);
       }
     }
-    ls = warp_sum(ls);
+    if (qn) {
+      const bool ok = lane < qn;
+      const double ur = ok ? queue[lane] : 0.0;
+      __syncwarp();
+      resolve(ur, ok);
+    }
+    // counts of 1..4 from the threshold counts
+    uint32_t c01 = g0 | (g1 << 16), c23 = g2 | (g3 << 16);  // n < 2^16
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c01 += __shfl_xor_sync(0xffffffffu, c01, o);
+      c23 += __shfl_xor_sync(0xffffffffu, c23, o);
+    }
+    const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c23 & 0xffffu, G3 = c23 >> 16;
+    __syncwarp();
+    // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
+    uint32_t hc0 = 0, hc1 = 0;
+    const uint8_t* r0 = bins + (lane + 1) * 32;
+    const uint8_t* r1 = bins + (lane + 33) * 32;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jj = (j + lane) & 7;  // rotate the word so the warp's loads spread over banks
+      const uint32_t w0 = reinterpret_cast<const uint32_t*>(r0)[jj];
+      const uint32_t w1 = reinterpret_cast<const uint32_t*>(r1)[jj];
+      hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
+      hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
+    }
+    hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
+    hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
+    __syncwarp();
+    if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;
+    if (lane == 1) hc0 = G0 - G1;
+    if (lane == 2) hc0 = G1 - G2;
+    if (lane == 3) hc0 = G2 - G3;
+    for (int v = 5; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
+    uint32_t* head = head_out + i * kKsHead;
+    head[lane] = hc0;
+    head[lane + 32] = hc1;
+    mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
+    mx = max(mx, hc1 ? lane + 33u : (hc0 ? lane + 1u : 0u));
     mn = warp_min_u32(mn);
     mx = warp_max_u32(mx);
-    c1 = warp_sum_u32(c1);
-    c2 = warp_sum_u32(c2);
-    c3 = warp_sum_u32(c3);
-    c4 = warp_sum_u32(c4);
-    __syncwarp();
-    uint32_t* head = head_out + i * kKsHead;  // head[k - 1] = count of value k
-    const uint32_t h0 = bins[lane + 1], h1 = bins[lane + 33];
-    head[lane] = lane == 0 ? c1 : lane == 1 ? c2 : lane == 2 ? c3 : lane == 3 ? c4 : h0;
-    head[lane + 32] = h1;
-    bins[lane + 1] = 0u;
-    bins[lane + 33] = 0u;
-    __syncwarp();
+    // log-sum: the head from its counts, the tail value by value (estimate.py:59-73 sums ln x_i)
+    ls += static_cast<double>(hc0) * __ldg(a.logs + lane + 1) + static_cast<double>(hc1) * __ldg(a.logs + lane + 33);
+    ls = warp_sum(ls);
     if (lane == 0) {
       ls_out[i] = ls;
       min_out[i] = mn;

@@ -96,6 +96,7 @@ struct zks_table {
   double* cdf = nullptr;
   uint16_t* guide = nullptr;
   uint32_t len = 0;
+  double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
 };
 
 extern "C" {
@@ -174,6 +175,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   zks_table* t = new zks_table();
   t->engine = e;
   t->len = static_cast<uint32_t>(len);
+  for (int j = 0; j < 4; ++j) t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
   cudaError_t err = cudaMallocAsync(&mem, len * sizeof(double) + 2 * zks::kGuideLevel * sizeof(uint16_t), e->stream);
@@ -272,6 +274,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   zks::ReplicateArgs a;
   a.cdf = t->cdf;
   a.guide = t->guide;
+  for (int j = 0; j < 4; ++j) a.cdf_head[j] = t->head[j];
   a.logs = e->logs;
   a.L = L;
   a.K = c->support_k;
@@ -399,7 +402,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     uint32_t* phead = pm + chunk;
     uint16_t* ptail = reinterpret_cast<uint16_t*>(phead + chunk * zks::kKsHead);
     auto draw = counting ? zks::draw_stats_kernel<true> : zks::draw_stats_kernel<false>;
-    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * (zks::kKsHead + 1) * 4;
+    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::kDrawWarpBytes;
     {
       const auto key = std::make_pair(reinterpret_cast<const void*>(draw), dsmem);
       if (e->occupancy.find(key) == e->occupancy.end()) {

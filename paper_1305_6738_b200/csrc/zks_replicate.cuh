@@ -73,6 +73,7 @@ struct ReplicateArgs {
   uint64_t pre_first;
   int pre_page;  // page bins for long tails (histogram capacity)
   double inv_n;  // 1 / n
+  double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
 };
 
 // guide lookup: [lo, hi] brackets lower_bound(cdf, u)
@@ -105,7 +106,14 @@ __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restr
 // The four draws of one Philox block, their lower_bound searches interleaved so that up to four
 // independent cdf loads are in flight per lane.  Lanes with valid[w] false yield 0.
 __device__ __forceinline__ void draw_block_u(const double u[4], const bool valid[4], const uint16_t* __restrict__ guide,
-                                             const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
+                                             const struct ReplicateArgs& a, uint32_t out[4]);
+
+__device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
+                                           const struct ReplicateArgs& a, uint32_t out[4]);
+
+__device__ __forceinline__ void draw_block_u(const double u[4], const bool valid[4], const uint16_t* __restrict__ guide,
+                                             const ReplicateArgs& a, uint32_t out[4]) {
+  const bool two = a.guide_levels == 2;
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
@@ -122,7 +130,7 @@ __device__ __forceinline__ void draw_block_u(const double u[4], const bool valid
       act[w] = lo[w] < hi[w];
       any |= act[w];
       mid[w] = (lo[w] + hi[w]) >> 1;
-      cv[w] = act[w] ? __ldg(cdf + mid[w]) : 0.0;
+      cv[w] = act[w] ? __ldg(a.cdf + mid[w]) : 0.0;
     }
     if (!any) break;
 #pragma unroll
@@ -136,15 +144,15 @@ __device__ __forceinline__ void draw_block_u(const double u[4], const bool valid
     }
   }
 #pragma unroll
-  for (int w = 0; w < 4; ++w) out[w] = valid[w] ? min(lo[w] + 1, L) : 0u;
+  for (int w = 0; w < 4; ++w) out[w] = valid[w] ? min(lo[w] + 1, a.L) : 0u;
 }
 
 __device__ __forceinline__ void draw_block(const Block4& r, const bool valid[4], const uint16_t* __restrict__ guide,
-                                           const double* __restrict__ cdf, uint32_t L, bool two, uint32_t out[4]) {
+                                           const ReplicateArgs& a, uint32_t out[4]) {
   double u[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) u[w] = uniform_open_closed(r.w[w]);
-  draw_block_u(u, valid, guide, cdf, L, two, out);
+  draw_block_u(u, valid, guide, a, out);
 }
 
 struct SampleStats {
@@ -172,7 +180,7 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
     uint32_t vv[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = (4 * b + w) < n;
-    draw_block(r, vb, guide, a.cdf, a.L, a.guide_levels == 2, vv);
+    draw_block(r, vb, guide, a, vv);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const bool valid = vb[w];
