@@ -68,6 +68,10 @@ void zks_engine_destroy(zks_engine* engine);
 int zks_engine_set_stream(zks_engine* engine, void* stream);
 int zks_engine_sync(zks_engine* engine);
 
+/* Number of CUDA kernels this engine has enqueued since it was created (every launch of every
+ * entry point).  Diagnostics: bench.py reports the timed-region delta as gpu_launches. */
+int zks_engine_launches(zks_engine* engine, unsigned long long* out);
+
 /* Upload a host-built sampling CDF (ZipfModel._sampling_cdf, distribution.py:99-105):
  * cdf_host[k-1] = P(X <= k) for k = 1..len, len = K or 65535, and build its guide table.
  * Replaces the per-process lru_cache'd table build of _generating_model (montecarlo.py:82-86). */

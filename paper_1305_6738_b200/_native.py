@@ -23,6 +23,7 @@ EXPORTS = (
     "zks_engine_destroy",
     "zks_engine_set_stream",
     "zks_engine_sync",
+    "zks_engine_launches",
     "zks_table_create",
     "zks_table_destroy",
     "zks_run_replicates",
@@ -94,6 +95,7 @@ def load() -> ctypes.CDLL:
     lib.zks_engine_destroy.restype = None
     lib.zks_engine_set_stream.argtypes = [vp, vp]
     lib.zks_engine_sync.argtypes = [vp]
+    lib.zks_engine_launches.argtypes = [vp, dp]
     lib.zks_table_create.argtypes = [vp, dp, i64, ctypes.POINTER(vp)]
     lib.zks_table_destroy.argtypes = [vp]
     lib.zks_table_destroy.restype = None

@@ -1,15 +1,16 @@
-// Batched replicate kernel for small and moderate n (n <= kBatchVals / 4).
+// Batched replicate kernels for n <= 1024 (table-mode MLE).
 //
 // Same per-replicate pipeline as replicate_kernel (montecarlo.py:89-116), re-phased so that no
-// phase is serial on a warp: a warp takes a batch of B consecutive replicate indices and
-//   1. derives the B stream keys lane-parallel (SeedSequence -> Philox key, one per lane);
-//   2. draws each replicate's sample warp-cooperatively into shared memory (u16 values),
-//      forming its log-sum / min / max on the way;
-//   3. runs the B Newton/bisection fits lane-parallel (one replicate per lane) on the fit
-//      tables, and the fitted normalisers;
-//   4. scores each replicate's KS statistic warp-cooperatively from its stored sample;
-//   5. retries the (rare) NoRootError replicates on stream idx + 2^32, warp-cooperatively.
-// B = min(32, kBatchVals / n): the sample store is 8 KB per warp.
+// phase is serial on a warp:
+//   * n < kLaneDrawMaxN (replicate_batch_kernel): a warp takes 32 consecutive replicate
+//     indices; each lane derives its stream key, draws its sample into shared memory (u16),
+//     fits it (Newton/bisection on the fit tables) and walks its KS head k <= kKsHead; the tails
+//     that outlive the head are scored warp-cooperatively; NoRootError replicates are retried
+//     on stream idx + 2^32 warp-cooperatively;
+//   * kLaneDrawMaxN <= n <= 1024: draw_stats_kernel draws (one warp per replicate, at high
+//     occupancy) and keeps only head counts, the tail values, log-sum / min / max; then
+//     fit_ks_kernel fits and scores 32 rows per warp the same way, and retry_kernel takes the
+//     listed first-attempt failures.
 #pragma once
 #include "zks_replicate.cuh"
 
@@ -20,6 +21,9 @@ namespace zks {
 #endif
 #ifndef ZKS_DRAW_MINB
 #define ZKS_DRAW_MINB 4
+#endif
+#ifndef ZKS_FIT_MINB
+#define ZKS_FIT_MINB 3
 #endif
 #ifndef ZKS_BATCH_VALS
 #define ZKS_BATCH_VALS 4096
@@ -46,49 +50,6 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
 #pragma unroll
     for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
     draw_block(r, vb, guide, a, x);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      if (vb[w]) {
-        ls += __ldg(a.logs + x[w]);
-        mn = min(mn, x[w]);
-        mx = max(mx, x[w]);
-      }
-    }
-    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
-  }
-  DrawStats s;
-  s.log_sum = warp_sum(ls);
-  s.vmin = warp_min_u32(mn);
-  s.vmax = warp_max_u32(mx);
-  return s;
-}
-
-// The same draws from staged uniforms (row u of this replicate), warp-cooperative.
-__device__ __forceinline__ DrawStats draw_sample_staged(const ReplicateArgs& a, const double* __restrict__ u,
-                                                        const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
-  const int n = static_cast<int>(a.n);
-  const int nb = (n + 3) >> 2;
-  const bool two = a.guide_levels == 2;
-  double ls = 0.0;
-  uint32_t mn = 0xffffffffu, mx = 0;
-  // rows hold whole Philox blocks (the staging kernel writes all 4 words of the last block), so
-  // every block is one 32-byte load; the next block's load is issued before this one is used
-  double2 p0 = make_double2(1.0, 1.0), p1 = p0;
-  if (lane < nb) {
-    p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane));
-    p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane + 2));
-  }
-  for (int b = lane; b < nb; b += 32) {
-    bool vb[4];
-    uint32_t x[4];
-    const double uu[4] = {p0.x, p0.y, p1.x, p1.y};
-    if (b + 32 < nb) {
-      p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32)));
-      p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32) + 2));
-    }
-#pragma unroll
-    for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block_u(uu, vb, guide, a, x);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
@@ -179,38 +140,15 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
   return ko.D;
 }
 
-// KS from pre-drawn head counts (values 1..kKsHead) and the list of values above kKsHead.
-__device__ __forceinline__ double ks_from_head_tail(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
-                                                    uint32_t* hist, uint32_t* queue, const uint32_t* head,
-                                                    const uint16_t* tail, uint32_t m, int lane, Work& wk) {
-  hist[lane + 1] = head[lane];
-  hist[lane + 33] = head[lane + 32];
-  __syncwarp();
-  KsParams p = ks_params(a);
-  p.H = kKsHead;
-  p.P = static_cast<uint32_t>(a.pre_page);
-  const KsOut ko = ks_scan<uint16_t, false>(p, g, norm, kmax, hist, tail, m, queue, lane, wk);
-  clear_hist(hist, ko.used_pages ? a.hist_words : round_up(static_cast<int>(kKsHead) + 1, 4), lane);
-  return ko.D;
-}
-
-constexpr int kLaneHistWords = (kKsHead + 1) * 32 / 4;  // u8 counts [value 0..64][lane]
-
-// Lane-parallel KS for small samples: lane r builds a private u8 histogram of its values <= kKsHead
-// (value-major, so a warp's lanes touch neighbouring bytes) and walks k = 1..min(kmax, kKsHead)
-// with the dense form F(k) = S(k)/norm, S the running sum of k^-g in the reference's order.
-// Returns true when the replicate is fully scored (kmax <= kKsHead, or the exit bound held
-// before kKsHead); otherwise the caller scores it warp-cooperatively.
-__device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, double g, double norm, uint32_t kmax,
-                                             uint8_t* lh, const uint16_t* v, double& ks) {
-  const int lane = threadIdx.x & 31;
-  const int n = static_cast<int>(a.n);
-  if (on) {
-    for (int j = 0; j < n; ++j) {
-      const uint32_t x = v[j];
-      if (x <= kKsHead) ++lh[x * 32 + lane];
-    }
-  }
+// Lane-parallel KS head: lane r walks k = 1..min(kmax, kKsHead) of its own replicate with the
+// dense form F(k) = S(k)/norm, S the running sum of k^-g in the reference's order, and the
+// counts count(k).  Returns true when the replicate is fully scored (kmax <= kKsHead, or the
+// exit bound held); otherwise (S, C, D) at k = kKsHead seed the warp-cooperative tail
+// (KsParams::from_head).
+template <typename CountFn>
+__device__ __forceinline__ bool ks_lane_walk(const ReplicateArgs& a, bool on, double g, double norm, uint32_t kmax,
+                                             CountFn count, double& ks, double& S_out, uint32_t& C_out,
+                                             double& D_out) {
   const uint32_t end = kmax < kKsHead ? kmax : kKsHead;
   const double inv = 1.0 / norm;
   double S = 0.0, D = 0.0;
@@ -220,7 +158,7 @@ __device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, do
   for (uint32_t k = 1; __any_sync(0xffffffffu, live && k <= end); ++k) {
     if (live && k <= end) {
       S += exp(-g * __ldg(a.logs + k));
-      C += lh[k * 32 + lane];
+      C += count(k);
       const double F = S * inv, E = static_cast<double>(C) * a.inv_n;
       D = fmax(D, fabs(F - E));
       if (D > fmax(1.0 - E, 1.0 - F) + kKsMargin) {
@@ -231,10 +169,75 @@ __device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, do
   }
   done = done || kmax <= kKsHead;
   if (on && done) ks = D;
+  S_out = S;
+  C_out = C;
+  D_out = D;
   __syncwarp();
   return on && done;
 }
 
+constexpr int kLaneHistWords = (kKsHead + 1) * 32 / 4;  // u8 counts [value 0..64][lane]
+
+// Small samples: lane r's values <= kKsHead into a private u8 histogram (value-major, so a
+// warp's lanes touch neighbouring bytes), then the lane walk.
+__device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, double g, double norm, uint32_t kmax,
+                                             uint8_t* lh, const uint16_t* v, double& ks, double& S, uint32_t& C,
+                                             double& D) {
+  const int lane = threadIdx.x & 31;
+  const int n = static_cast<int>(a.n);
+  if (on) {
+    for (int j = 0; j < n; ++j) {
+      const uint32_t x = v[j];
+      if (x <= kKsHead) ++lh[x * 32 + lane];
+    }
+  }
+  return ks_lane_walk(a, on, g, norm, kmax, [&](uint32_t k) { return static_cast<uint32_t>(lh[k * 32 + lane]); }, ks,
+                      S, C, D);
+}
+
+// Tail of replicate r of the warp (kmax > kKsHead) from its lane-walk state: the values above
+// kKsHead among over[0..over_n), warp-cooperatively.
+__device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r, double g, double norm, uint32_t kmax,
+                                                   double S, uint32_t C, double D, uint32_t* hist, int hist_words,
+                                                   uint32_t page, uint32_t* queue, const uint16_t* over,
+                                                   uint32_t over_n, int lane, Work& wk) {
+  KsParams p = ks_params(a);
+  p.H = kKsHead;
+  p.hist_words = hist_words;
+  p.P = page;
+  p.from_head = true;
+  p.S0 = __shfl_sync(0xffffffffu, S, r);
+  p.C0 = __shfl_sync(0xffffffffu, C, r);
+  p.D0 = __shfl_sync(0xffffffffu, D, r);
+  return ks_scan<uint16_t, false>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
+}
+
+// One replicate's second attempt on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative:
+// draw into v, fit, score.  Returns the status (1 retried, 2 failed twice).
+template <bool kCount>
+__device__ __forceinline__ uint8_t retry_replicate(const ReplicateArgs& a, const ModelFns& M, uint64_t rel,
+                                                   const uint16_t* guide, uint16_t* v, uint32_t* hist,
+                                                   uint32_t* queue, int lane, double& ks, double& g, Work& wk) {
+  uint64_t q0, q1;
+  stream_key(a.seed, a.rep, a.first + rel + (1ull << 32), q0, q1);
+  const DrawStats st = draw_sample(a, q0, q1, guide, v, lane);
+  __syncwarp();
+  const double t2 = fit_target(st.log_sum, st.vmin, a.K, static_cast<double>(a.n));
+  double g2 = 0.0;
+  const bool ok2 = fit_exponent(M, t2, lane, g2, wk);  // uniform: same inputs on every lane
+  ks = __longlong_as_double(0x7ff8000000000000ll);
+  if (ok2) ks = ks_from_sample(a, g2, fit_norm(a.fit, g2), st.vmax, hist, queue, v, lane, wk);
+  if (kCount) {
+    ++wk.attempts;
+    wk.draws += a.n;
+  }
+  g = ok2 ? g2 : t2;  // failed twice: report the retry sample's mean log (diagnostics)
+  return ok2 ? 1 : 2;
+}
+
+// Small samples (n < kLaneDrawMaxN): a warp takes B = 32 consecutive replicate indices;
+// each lane draws, fits and scores the head of its own replicate; tails that outlive the head
+// are scored warp-cooperatively from the lane's head state.
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -267,63 +270,29 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     const int nrep = left < static_cast<uint64_t>(B) ? static_cast<int>(left) : B;
     const bool active = lane < nrep;
 
-    // 1. stream keys, one replicate per lane
-    uint64_t k0 = 0, k1 = 0;
-    if (active) stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
-
-    // 2. samples into shared memory
-    double my_ls = 0.0;
-    uint32_t my_min = 0, my_max = 0;
-    if (a.n < kLaneDrawMaxN) {
-      // few Philox blocks per replicate: each lane draws its own replicate's sample
-      if (active) {
-        const DrawStats st = draw_sample_lane(a, k0, k1, guide, vals + lane * a.vals_stride);
-        my_ls = st.log_sum;
-        my_min = st.vmin;
-        my_max = st.vmax;
-      }
-    } else if (a.pre_head) {
-      // drawn by draw_stats_kernel: only the per-replicate statistics are read here
-      if (active) {
-        const uint64_t row = a.first + r0 + lane - a.pre_first;
-        my_ls = a.pre_ls[row];
-        my_min = a.pre_min[row];
-        my_max = a.pre_max[row];
-      }
-    } else {
-      for (int r = 0; r < nrep; ++r) {
-        const uint64_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
-        const DrawStats st =
-            a.ubuf ? draw_sample_staged(a, a.ubuf + (a.first + r0 + r - a.ubuf_first) * a.ubuf_stride, guide,
-                                        vals + r * a.vals_stride, lane)
-                   : draw_sample(a, q0, q1, guide, vals + r * a.vals_stride, lane);
-        if (lane == r) {
-          my_ls = st.log_sum;
-          my_min = st.vmin;
-          my_max = st.vmax;
-        }
-      }
+    // 1-2. stream key and sample of this lane's replicate
+    uint16_t* mv = vals + lane * a.vals_stride;
+    DrawStats st{0.0, 0u, 0u};
+    if (active) {
+      uint64_t k0, k1;
+      stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
+      st = draw_sample_lane(a, k0, k1, guide, mv);
     }
     __syncwarp();
     if (kCount) {
       wk.attempts += nrep;
-      const unsigned long long d = static_cast<unsigned long long>(nrep) * a.n;
-      if (a.pre_head && a.n >= kLaneDrawMaxN)
-        ;  // counted by draw_stats_kernel
-      else if (a.ubuf && a.n >= kLaneDrawMaxN)
-        wk.staged += d;
-      else
-        wk.draws += d;
+      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
     }
 
     // 3. exponent fits, one replicate per lane
-    double g = 0.0, norm = 1.0, target = 0.0;
+    double g = 0.0, norm = 1.0;
     bool ok = false;
     Work lw{};
     if (active) {
-      target = fit_target(my_ls, my_min, K, dn);
+      const double target = fit_target(st.log_sum, st.vmin, K, dn);
       ok = fit_exponent(M, target, lane, g, lw);
       if (ok) norm = fit_norm(a.fit, g);
+      if (!ok) g = target;
     }
     if (kCount) {
       unsigned long long e = lw.evals;
@@ -332,55 +301,35 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
       wk.evals += e;
     }
 
-    // 4. KS statistics
+    // 4. KS: the head lane by lane, long tails warp-cooperatively
     double my_ks = __longlong_as_double(0x7ff8000000000000ll);
-    bool scored = false;
-    if (a.n < kLaneDrawMaxN) {
-      // small samples: each lane scores its own replicate over k = 1..min(kmax, kKsHead)
-      scored = ks_lane_head(a, ok && active, g, norm, my_max, reinterpret_cast<uint8_t*>(hist),
-                            vals + lane * a.vals_stride, my_ks);
-      clear_hist(hist, a.hist_words, lane);
-    }
-    for (int r = 0; r < nrep; ++r) {
-      if (!__shfl_sync(0xffffffffu, ok && !scored, r)) continue;
+    double hS, hD;
+    uint32_t hC;
+    const bool scored = ks_lane_head(a, ok && active, g, norm, st.vmax, reinterpret_cast<uint8_t*>(hist), mv, my_ks,
+                                     hS, hC, hD);
+    clear_hist(hist, kLaneHistWords, lane);
+    for (unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored); need; need &= need - 1) {
+      const int r = __ffs(need) - 1;
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
-      const uint32_t kmax = __shfl_sync(0xffffffffu, my_max, r);
-      double ks;
-      if (a.pre_head && a.n >= kLaneDrawMaxN) {
-        const uint64_t row = a.first + r0 + r - a.pre_first;
-        ks = ks_from_head_tail(a, gr, nr, kmax, hist, queue, a.pre_head + row * kKsHead,
-                               a.pre_tail + row * a.vals_stride, a.pre_m[row], lane, wk);
-      } else {
-        ks = ks_from_sample(a, gr, nr, kmax, hist, queue, vals + r * a.vals_stride, lane, wk);
-      }
-      if (lane == r) my_ks = ks;
+      const uint32_t kmax = __shfl_sync(0xffffffffu, st.vmax, r);
+      // n < kOverCap: the values above the head always fit the register sort (no pages)
+      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, a.hist_words, 0u, queue,
+                                         vals + r * a.vals_stride, static_cast<uint32_t>(a.n), lane, wk);
+      if (lane == r) my_ks = ko.D;
     }
 
     // 5. retries on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative
     uint8_t status = ok ? 0 : 2;
-    unsigned fails = __ballot_sync(0xffffffffu, active && !ok);
-    while (fails) {
+    for (unsigned fails = __ballot_sync(0xffffffffu, active && !ok); fails; fails &= fails - 1) {
       const int r = __ffs(fails) - 1;
-      fails &= fails - 1;
-      uint64_t q0, q1;
-      stream_key(a.seed, a.rep, a.first + r0 + r + (1ull << 32), q0, q1);
-      uint16_t* v = vals + r * a.vals_stride;
-      const DrawStats st = draw_sample(a, q0, q1, guide, v, lane);
-      __syncwarp();
-      const double t2 = fit_target(st.log_sum, st.vmin, K, dn);
-      double g2 = 0.0;
-      const bool ok2 = fit_exponent(M, t2, lane, g2, wk);  // uniform: same inputs on every lane
-      double ks2 = __longlong_as_double(0x7ff8000000000000ll);
-      if (ok2) ks2 = ks_from_sample(a, g2, fit_norm(a.fit, g2), st.vmax, hist, queue, v, lane, wk);
-      if (kCount) {
-        ++wk.attempts;
-        wk.draws += a.n;
-      }
+      double ks2, g2;
+      const uint8_t s2 = retry_replicate<kCount>(a, M, r0 + r, guide, vals + r * a.vals_stride, hist, queue, lane, ks2,
+                                                 g2, wk);
       if (lane == r) {
-        status = ok2 ? 1 : 2;
+        status = s2;
         my_ks = ks2;
-        g = ok2 ? g2 : t2;  // failed twice: report the retry sample's mean log (diagnostics)
+        g = g2;
       }
     }
 
@@ -389,6 +338,144 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
       a.gh_out[r0 + lane] = g;
       a.st_out[r0 + lane] = status;
     }
+  }
+  if (kCount && lane == 0) {
+    const unsigned long long* f = &wk.attempts;
+    for (int i = 0; i < kWorkFields; ++i)
+      if (f[i]) atomicAdd(a.counters + i, f[i]);
+  }
+}
+
+constexpr int kHeadRowWords = kKsHead / 2 + 1;        // u16 counts of 1..kKsHead + pad: conflict-free columns
+constexpr int kFitHistWords = 32 * kHeadRowWords;      // the head rows, reused as page histogram
+constexpr int kFitWarpWords = kFitHistWords + kKsQueueWords;
+
+// Fit + score of pre-drawn replicates (draw_stats_kernel): a warp takes 32 consecutive rows,
+// fits them lane-parallel, walks each head k <= kKsHead lane by lane from the counts, and
+// scores the tails that outlive the head warp-cooperatively from the tail lists.  First-attempt
+// failures go to retry_list (count at [0], row offsets after) for retry_kernel.
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(ReplicateArgs a, uint32_t* retry_list) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* heads = reinterpret_cast<uint32_t*>(smem) + warp * kFitWarpWords;
+  uint32_t* hist = heads;  // page histogram once the lane walks are done
+  uint32_t* queue = heads + kFitHistWords;
+  const int K = a.K;
+  const double dn = static_cast<double>(a.n);
+  const uint64_t nbatches = (a.count + 31) / 32;
+  Work wk{};
+  const ModelFns M{K, a.logs, a.fit, true};
+
+  for (;;) {
+    unsigned long long bid = 0;
+    if (lane == 0) bid = atomicAdd(a.work, 1ull);
+    bid = __shfl_sync(0xffffffffu, bid, 0);
+    if (bid >= nbatches) break;
+    const uint64_t r0 = bid * 32;
+    const uint64_t left = a.count - r0;
+    const int nrep = left < 32u ? static_cast<int>(left) : 32;
+    const bool active = lane < nrep;
+    const uint64_t row = a.first + r0 + lane - a.pre_first;
+
+    // head counts of the 32 rows into shared memory (128-byte rows, 16-byte loads)
+    const uint4* src = reinterpret_cast<const uint4*>(a.pre_head + (a.first + r0 - a.pre_first) * kKsHead);
+    for (int e = lane; e < nrep * 8; e += 32) {
+      const uint4 q = __ldcs(src + e);
+      uint32_t* d = heads + (e >> 3) * kHeadRowWords + (e & 7) * 4;
+      d[0] = q.x;
+      d[1] = q.y;
+      d[2] = q.z;
+      d[3] = q.w;
+    }
+
+    // exponent fits, one replicate per lane
+    double g = 0.0, norm = 1.0;
+    uint32_t vmax = 0;
+    bool ok = false;
+    Work lw{};
+    if (active) {
+      vmax = a.pre_max[row];
+      const double target = fit_target(a.pre_ls[row], a.pre_min[row], K, dn);
+      ok = fit_exponent(M, target, lane, g, lw);
+      if (ok) norm = fit_norm(a.fit, g);
+      if (!ok) g = target;
+    }
+    if (kCount) {
+      unsigned long long e = lw.evals;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+      wk.evals += e;
+      wk.attempts += nrep;
+    }
+    __syncwarp();
+
+    // heads lane by lane
+    double my_ks = __longlong_as_double(0x7ff8000000000000ll);
+    double hS, hD;
+    uint32_t hC;
+    const uint32_t* hr = heads + lane * kHeadRowWords;
+    const bool scored = ks_lane_walk(a, ok && active, g, norm, vmax,
+                                     [&](uint32_t k) { return (hr[(k - 1) >> 1] >> (((k - 1) & 1) * 16)) & 0xffffu; },
+                                     my_ks, hS, hC, hD);
+    // long tails, warp-cooperatively (the head rows are free now: pages reuse them)
+    for (unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored); need; need &= need - 1) {
+      const int r = __ffs(need) - 1;
+      const double gr = __shfl_sync(0xffffffffu, g, r);
+      const double nr = __shfl_sync(0xffffffffu, norm, r);
+      const uint32_t kmax = __shfl_sync(0xffffffffu, vmax, r);
+      const uint64_t rr = a.first + r0 + r - a.pre_first;
+      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, kFitHistWords, kFitHistWords, queue,
+                                         a.pre_tail + rr * a.vals_stride, a.pre_m[rr], lane, wk);
+      if (lane == r) my_ks = ko.D;
+    }
+    __syncwarp();
+
+    if (active) {
+      if (!ok) retry_list[1 + atomicAdd(retry_list, 1u)] = static_cast<uint32_t>(r0 + lane);
+      a.ks_out[r0 + lane] = my_ks;
+      a.gh_out[r0 + lane] = g;
+      a.st_out[r0 + lane] = ok ? 0 : 2;
+    }
+  }
+  if (kCount && lane == 0) {
+    const unsigned long long* f = &wk.attempts;
+    for (int i = 0; i < kWorkFields; ++i)
+      if (f[i]) atomicAdd(a.counters + i, f[i]);
+  }
+}
+
+// Second attempts of the rows fit_ks_kernel listed (montecarlo.py:106-115), one warp each; exits
+// at once when the list is empty (the common case).
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads) retry_kernel(ReplicateArgs a, const uint32_t* retry_list) {
+  const uint32_t cnt = *retry_list;
+  if (cnt == 0) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
+  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp_bytes = a.hist_words * 4 + 3 * kKsQueue * 4 + a.vals_stride * 2;
+  unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
+  uint32_t* queue = hist + a.hist_words;
+  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
+  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  clear_hist(hist, a.hist_words, lane);
+  __syncthreads();
+  Work wk{};
+  const ModelFns M{a.K, a.logs, a.fit, true};
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t j = blockIdx.x * (blockDim.x >> 5) + warp; j < cnt; j += warps) {
+    const uint32_t rel = retry_list[1 + j];
+    double ks, g;
+    const uint8_t s = retry_replicate<kCount>(a, M, rel, guide, vals, hist, queue, lane, ks, g, wk);
+    if (lane == 0) {
+      a.ks_out[rel] = ks;
+      a.gh_out[rel] = g;
+      a.st_out[rel] = s;
+    }
+    __syncwarp();
   }
   if (kCount && lane == 0) {
     const unsigned long long* f = &wk.attempts;
@@ -441,7 +528,7 @@ constexpr int kDrawQueue = 160;  // doubles per warp: < 32 left over + 4 x 32 pu
 constexpr int kDrawWarpBytes = (kKsHead + 1) * 32 + kDrawQueue * 8;  // u8 bins [v][lane] + queue
 
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(ReplicateArgs a, uint32_t* head_out,
+__global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(ReplicateArgs a, uint16_t* head_out,
                                                                  uint16_t* tail_out, uint32_t* m_out, double* ls_out,
                                                                  uint32_t* min_out, uint32_t* max_out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -589,9 +676,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
     if (lane == 2) hc0 = G1 - G2;
     if (lane == 3) hc0 = G2 - G3;
     for (int v = 5; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
-    uint32_t* head = head_out + i * kKsHead;
-    head[lane] = hc0;
-    head[lane + 32] = hc1;
+    uint16_t* head = head_out + i * kKsHead;  // n <= 1024: u16 counts
+    head[lane] = static_cast<uint16_t>(hc0);
+    head[lane + 32] = static_cast<uint16_t>(hc1);
     mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
     mx = max(mx, hc1 ? lane + 33u : (hc0 ? lane + 1u : 0u));
     mn = warp_min_u32(mn);

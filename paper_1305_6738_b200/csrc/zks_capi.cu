@@ -67,9 +67,16 @@ struct zks_engine {
   std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
   void* pre = nullptr;  // pre-drawn sample rows + their statistics (two-kernel path)
   size_t pre_bytes = 0;
+  unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
 };
 
 namespace {
+
+// every kernel launch goes through here: the error check and the engine's launch count
+cudaError_t launched(zks_engine* e) {
+  ++e->launches;
+  return cudaGetLastError();
+}
 
 // exponent-fit table of support K, built on the engine stream on first use
 int fit_table_for(zks_engine* e, int K, zks::FitTable** out) {
@@ -82,7 +89,7 @@ int fit_table_for(zks_engine* e, int K, zks::FitTable** out) {
     const int threads = 128;
     const int blocks = (T.intervals * 32 + threads - 1) / threads;
     zks::fit_table_kernel<<<blocks, threads, 0, e->stream>>>(T, coef, e->logs);
-    ZKS_CUDA(cudaGetLastError());
+    ZKS_CUDA(launched(e));
     it = e->fit_tables.emplace(K, T).first;
   }
   *out = &it->second;
@@ -167,6 +174,12 @@ int zks_engine_sync(zks_engine* e) {
   return ZKS_OK;
 }
 
+int zks_engine_launches(zks_engine* e, unsigned long long* out) {
+  if (!e || !out) return fail(ZKS_EINVAL, "engine/out is NULL");
+  *out = e->launches;
+  return ZKS_OK;
+}
+
 int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_table** out) {
   if (!e || !out) return fail(ZKS_EINVAL, "engine/out is NULL");
   *out = nullptr;
@@ -197,7 +210,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   }
   if (err == cudaSuccess) {
     zks::guide_kernel<<<(2 * zks::kGuideLevel + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
-    err = cudaGetLastError();
+    err = launched(e);
   }
   if (err != cudaSuccess) {
     zks_table_destroy(t);
@@ -243,7 +256,7 @@ int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (int64_t)((count + 7) / 8)));
   zks::stage_uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, repetition, first, count, n,
                                                                      zks_staging_stride(n), u_dev, e->counters);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -381,13 +394,13 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.pre_min = nullptr;
   a.pre_max = nullptr;
   a.pre_first = 0;
-  a.pre_page = a.H;
   if (batched && c->n >= zks::kLaneDrawMaxN) {
     // draw phase in its own high-occupancy kernel (head counts + tail values per replicate),
-    // chunk by chunk, then fit + score
-    const uint64_t row_bytes = uint64_t(a.vals_stride) * 2 + zks::kKsHead * 4 + 24;
+    // then fit + score, then the listed retries; chunk by chunk.  Per row: u16 head counts
+    // (128 B), log-sum, min / max / m, the tail values, a retry-list slot.
+    const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(a.vals_stride) * 2 + 4;
     const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, kPreBytes / row_bytes));
-    const size_t need = size_t(chunk) * row_bytes;
+    const size_t need = size_t(chunk) * row_bytes + 16;
     if (need > e->pre_bytes) {
       if (e->pre) ZKS_CUDA(cudaFreeAsync(e->pre, e->stream));
       e->pre = nullptr;
@@ -395,25 +408,37 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
       ZKS_CUDA(cudaMallocAsync(&e->pre, need, e->stream));
       e->pre_bytes = need;
     }
-    double* pls = reinterpret_cast<double*>(e->pre);
+    uint16_t* phead = reinterpret_cast<uint16_t*>(e->pre);
+    double* pls = reinterpret_cast<double*>(phead + chunk * zks::kKsHead);
     uint32_t* pmin = reinterpret_cast<uint32_t*>(pls + chunk);
     uint32_t* pmax = pmin + chunk;
     uint32_t* pm = pmax + chunk;
-    uint32_t* phead = pm + chunk;
-    uint16_t* ptail = reinterpret_cast<uint16_t*>(phead + chunk * zks::kKsHead);
+    uint16_t* ptail = reinterpret_cast<uint16_t*>(pm + chunk);
+    uint32_t* retry = reinterpret_cast<uint32_t*>(ptail + chunk * a.vals_stride);  // vals_stride % 4 == 0
     auto draw = counting ? zks::draw_stats_kernel<true> : zks::draw_stats_kernel<false>;
+    auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
+    auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
     const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::kDrawWarpBytes;
+    const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
+    const size_t rsmem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + zks::kKsQueueWords * 4 + a.vals_stride * 2);
+    int dper = 0, fper = 0;
     {
-      const auto key = std::make_pair(reinterpret_cast<const void*>(draw), dsmem);
-      if (e->occupancy.find(key) == e->occupancy.end()) {
-        int optin = 0, per = 0;
-        ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-        ZKS_CUDA(cudaFuncSetAttribute(draw, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-        ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, draw, zks::kThreads, dsmem));
-        e->occupancy.emplace(key, std::max(per, 1));
+      int optin = 0;
+      ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+      const std::pair<const void*, size_t> keys[3] = {{reinterpret_cast<const void*>(draw), dsmem},
+                                                      {reinterpret_cast<const void*>(fit), fsmem},
+                                                      {reinterpret_cast<const void*>(again), rsmem}};
+      for (const auto& key : keys) {
+        if (e->occupancy.find(key) != e->occupancy.end()) continue;
+        int per = 0;
+        ZKS_CUDA(cudaFuncSetAttribute(key.first, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, key.first, zks::kThreads, key.second));
+        if (per < 1) return fail(ZKS_ECUDA, "batch kernel does not fit (smem %zu)", key.second);
+        e->occupancy.emplace(key, per);
       }
+      dper = e->occupancy[keys[0]];
+      fper = e->occupancy[keys[1]];
     }
-    const int dper = e->occupancy[std::make_pair(reinterpret_cast<const void*>(draw), dsmem)];
     zks::ReplicateArgs sub = a;
     for (uint64_t off = 0; off < c->count; off += chunk) {
       const uint64_t cnt = std::min<uint64_t>(chunk, c->count - off);
@@ -431,17 +456,21 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
       sub.pre_first = sub.first;
       const int64_t dblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)((cnt + 7) / 8)));
       draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(sub, phead, ptail, pm, pls, pmin, pmax);
-      ZKS_CUDA(cudaGetLastError());
-      const int64_t fblocks = std::min<int64_t>(blocks, (int64_t)((cnt + per_block - 1) / per_block));
+      ZKS_CUDA(launched(e));
+      const int64_t fblocks =
+          std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * fper, (int64_t)((cnt + 255) / 256)));
       ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
-      kernel<<<(unsigned)std::max<int64_t>(fblocks, 1), zks::kThreads, smem, e->stream>>>(sub);
-      ZKS_CUDA(cudaGetLastError());
+      ZKS_CUDA(cudaMemsetAsync(retry, 0, sizeof(uint32_t), e->stream));
+      fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub, retry);
+      ZKS_CUDA(launched(e));
+      again<<<(unsigned)e->sms, zks::kThreads, rsmem, e->stream>>>(sub, retry);
+      ZKS_CUDA(launched(e));
     }
     return ZKS_OK;
   }
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
   kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -463,12 +492,12 @@ int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t coun
   }
   ZKS_CUDA(cudaSetDevice(e->device));
   zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->sel, rl, nranks);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
   for (int shift = 56; shift >= 0; shift -= 8) {
     zks::select_pass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(
         reinterpret_cast<const unsigned long long*>(values_dev), count, shift, e->sel, nranks, out_dev);
-    ZKS_CUDA(cudaGetLastError());
+    ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
 }
@@ -495,7 +524,7 @@ int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_h
   ZKS_CUDA(cudaSetDevice(e->device));
   if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
   zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, e->sel_out);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
   return ZKS_OK;
@@ -520,7 +549,7 @@ int zks_fit_eval(zks_engine* e, int32_t support_k, const double* x_dev, int64_t 
   if (rc) return rc;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
   zks::fit_eval_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(*T, x_dev, count, mu_dev, m2_dev, norm_dev);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -544,7 +573,7 @@ int zks_stream_uniforms(zks_engine* e, uint64_t seed, uint64_t rep, uint64_t idx
   const int64_t nb = (count + 3) / 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (nb + 255) / 256));
   zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, count, out_dev);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -555,7 +584,7 @@ int zks_draw(zks_engine* e, const zks_table* t, const double* u_dev, int64_t cou
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (count + 255) / 256));
   zks::draw_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(t->cdf, t->guide, t->len, u_dev, count, out_dev);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -628,7 +657,7 @@ int zks_fit_samples(zks_engine* e, int32_t support_k, const int64_t* values_dev,
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (nsamples + zks::kWarps - 1) / zks::kWarps));
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
   zks::samples_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -639,7 +668,7 @@ int zks_series_eval(zks_engine* e, int32_t support_k, const double* gamma_dev, i
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = (count * 32 + 255) / 256;
   zks::series_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(gamma_dev, count, support_k, e->logs, out_dev);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 
@@ -652,7 +681,7 @@ int zks_solve_exponents(zks_engine* e, int32_t support_k, const double* target_d
   const int64_t blocks = (count * 32 + 255) / 256;
   zks::solve_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(target_dev, count, support_k, e->logs, mle_params(settings),
                                                              bisect_only, gamma_dev, status_dev);
-  ZKS_CUDA(cudaGetLastError());
+  ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
 

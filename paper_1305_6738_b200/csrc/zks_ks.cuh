@@ -54,6 +54,11 @@ struct KsParams {
   bool exact;          // reference-exact forms (user-sample API)
   uint32_t P = 0;      // page bins for values above H when they are many (0 = H)
   double inv_n = 0.0;  // 1/n when the caller has it (0 = divide here)
+  // continue from a head k = 1..kKsHead already scored lane by lane (ks_lane_head): its running
+  // sum S(kKsHead), count C(kKsHead) and max gap; requires H == kKsHead and !kArg
+  bool from_head = false;
+  double S0 = 0.0, D0 = 0.0;
+  uint32_t C0 = 0;
 };
 
 struct KsOut {
@@ -77,6 +82,8 @@ struct KsState {
 struct KsCtx {
   double g, inv, inv_n, dn;
   double fa, a_pow, La;  // f(a) = a^-g, a^(1-g), ln a for a = kKsHead + 1
+  double inv_om, g3, fa1, fa3;  // 1/(1-g), g(g+1)(g+2), f(a)/a, f(a)/a^3
+  bool direct;                  // |1-g| large enough for the integral as (v f(v) - a f(a))/(1-g)
   bool exact;
   const double* logs;
   uint32_t* qk;  // queue: value v
@@ -108,15 +115,18 @@ __device__ __forceinline__ void take(KsState& s, double gap, uint32_t k) {
 __device__ __forceinline__ double em_block(const KsCtx& c, uint64_t v, double& fv) {
   const double Lv = ln_of(c.logs, v);
   const double b = static_cast<double>(v);
-  const double a = static_cast<double>(kKsHead + 1);
+  const double ib = 1.0 / b;
   fv = exp(-c.g * Lv);
-  const double om = 1.0 - c.g;
-  // integral_a^v x^-g dx = a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
-  const double integral = (om == 0.0) ? (Lv - c.La) : c.a_pow * expm1(om * (Lv - c.La)) / om;
-  const double d1 = -c.g * (fv / b - c.fa / a);  // f'(v) - f'(a)
-  const double g3 = c.g * (c.g + 1.0) * (c.g + 2.0);
-  const double d3 = -g3 * (fv / (b * b * b) - c.fa / (a * a * a));  // f'''(v) - f'''(a)
-  return integral + 0.5 * (c.fa + fv) + d1 / 12.0 - d3 / 720.0;
+  // integral_a^v x^-g dx = (v^(1-g) - a^(1-g)) / (1-g); near g = 1 that difference cancels, so
+  // there it is a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
+  double integral;
+  if (c.direct)
+    integral = (b * fv - c.a_pow) * c.inv_om;
+  else
+    integral = (c.g == 1.0) ? (Lv - c.La) : c.a_pow * expm1((1.0 - c.g) * (Lv - c.La)) * c.inv_om;
+  const double d1 = -c.g * (fv * ib - c.fa1);               // f'(v) - f'(a)
+  const double d3 = -c.g3 * (fv * (ib * ib * ib) - c.fa3);  // f'''(v) - f'''(a)
+  return integral + 0.5 * (c.fa + fv) + d1 * (1.0 / 12.0) - d3 * (1.0 / 720.0);
 }
 
 struct FlushTail {
@@ -232,7 +242,12 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
 
   // head: dense, the reference's cumulative form
   const uint32_t head_end = static_cast<uint32_t>(kmax < kKsHead ? kmax : kKsHead);
-  for (uint32_t k0 = 1; k0 <= head_end && !s.done; k0 += 32) {
+  if (p.from_head) {
+    s.S = p.S0;
+    s.Cb = p.C0;
+    s.D = p.D0;
+  }
+  for (uint32_t k0 = 1; k0 <= head_end && !s.done && !p.from_head; k0 += 32) {
     ++wk.ks_tiles;
     const uint32_t k = k0 + lane;
     const bool in = k <= head_end;
@@ -259,7 +274,14 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     s.Dw = warp_max(s.D);
     c.La = __ldg(p.logs + kKsHead + 1);
     c.fa = exp(-g * c.La);
-    c.a_pow = static_cast<double>(kKsHead + 1) * c.fa;
+    constexpr double a = static_cast<double>(kKsHead + 1);
+    c.a_pow = a * c.fa;
+    const double om = 1.0 - g;
+    c.direct = fabs(om) >= 0.125;
+    c.inv_om = om == 0.0 ? 0.0 : 1.0 / om;
+    c.g3 = g * (g + 1.0) * (g + 2.0);
+    c.fa1 = c.fa * (1.0 / a);
+    c.fa3 = c.fa * (1.0 / (a * a * a));
 
     // above the head: endpoints of the observed values
     int q = 0;
@@ -287,6 +309,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       if (m <= kOverCap) {
         paged = false;
         constexpr int kSlots = kOverCap / 32;
+        const int size = m <= 32u ? 32 : m <= 64u ? 64 : 128;  // sort only the occupied slots
         uint32_t r[kSlots];  // element i = slot * 32 + lane
 #pragma unroll
         for (int j = 0; j < kSlots; ++j) {
@@ -297,10 +320,12 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
         // bitonic sort of the kOverCap values across the warp (padding 0xffffffff sorts last)
 #pragma unroll
         for (int k = 2; k <= static_cast<int>(kOverCap); k <<= 1) {
+          if (k > size) break;
 #pragma unroll
           for (int jj = k >> 1; jj > 0; jj >>= 1) {
 #pragma unroll
             for (int sl = 0; sl < kSlots; ++sl) {
+              if (sl * 32 >= size) break;
               const int i = sl * 32 + lane;
               const bool up = (i & k) == 0;
               if (jj >= 32) {
@@ -323,7 +348,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
         const unsigned lt = (1u << lane) - 1u;
         int ne = 0;
         uint32_t run_start = 0;  // prefix max of start indices, carried across slots
-        for (int sl = 0; sl < kSlots && !s.done; ++sl) {
+        for (int sl = 0; sl < kSlots && sl * 32 < size && !s.done; ++sl) {
           const uint32_t v = r[sl];
           const uint32_t i = sl * 32 + lane;
           uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);

@@ -61,17 +61,16 @@ struct ReplicateArgs {
   const double* ubuf;
   int64_t ubuf_stride;
   uint64_t ubuf_first;
-  // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: counts of the
-  // values 1..kKsHead at pre_head[i * kKsHead], the m = pre_m[i] values above kKsHead at
-  // pre_tail[i * vals_stride], log-sum / min / max; pre_head NULL = draw in-kernel
-  const uint32_t* pre_head;
+  // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: u16 counts of
+  // the values 1..kKsHead at pre_head[i * kKsHead] (128-byte rows), the m = pre_m[i] values
+  // above kKsHead at pre_tail[i * vals_stride], log-sum / min / max
+  const uint16_t* pre_head;
   const uint16_t* pre_tail;
   const uint32_t* pre_m;
   const double* pre_ls;
   const uint32_t* pre_min;
   const uint32_t* pre_max;
   uint64_t pre_first;
-  int pre_page;  // page bins for long tails (histogram capacity)
   double inv_n;  // 1 / n
   double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
 };

@@ -65,7 +65,6 @@ class Engine:
         self.handle = handle
         self._tables: OrderedDict[tuple, DrawTable] = OrderedDict()
         self._lock = threading.Lock()
-        self.launches = 0  # kernels this engine has launched (bench.py reports the timed-region delta)
 
     # -- streams -------------------------------------------------------------
     def bind_stream(self):
@@ -78,6 +77,14 @@ class Engine:
     def sync(self) -> None:
         _native.check(self.lib.zks_engine_sync(self.handle))
 
+    @property
+    def launches(self) -> int:
+        """CUDA kernels this engine has enqueued so far (counted in the native library; bench.py
+        reports the timed-region delta)."""
+        out = ctypes.c_ulonglong()
+        _native.check(self.lib.zks_engine_launches(self.handle, ctypes.byref(out)))
+        return out.value
+
     # -- tables --------------------------------------------------------------
     def table(self, gamma: float, support_k: int | None, cdf_builder) -> DrawTable:
         """Cached device table for the generating model (montecarlo.py:82-86 lru_cache)."""
@@ -88,7 +95,6 @@ class Engine:
                 self._tables.move_to_end(key)
                 return t
             t = DrawTable(self, cdf_builder())
-            self.launches += 1  # guide table
             self._tables[key] = t
             while len(self._tables) > 64:
                 _, old = self._tables.popitem(last=False)
@@ -110,7 +116,6 @@ class Engine:
             count=int(count),
         )
         self.bind_stream()
-        self.launches += 1
         _native.check(
             self.lib.zks_run_replicates(
                 self.handle, table.handle, ctypes.byref(cell), ks.data_ptr(), gamma_hat.data_ptr(), status.data_ptr()
@@ -123,7 +128,6 @@ class Engine:
     def stage_uniforms(self, seed: int, repetition: int, first: int, count: int, n: int, out) -> None:
         """Uniform rows of replicate indices [first, first+count) into device float64 ``out``."""
         self.bind_stream()
-        self.launches += 1
         _native.check(self.lib.zks_stage_uniforms(self.handle, int(seed), int(repetition), int(first), int(count),
                                                   int(n), out.data_ptr()))
 
@@ -133,7 +137,6 @@ class Engine:
                                n=int(n), base_seed=int(base_seed), repetition=int(repetition), first=int(first),
                                count=int(count))
         self.bind_stream()
-        self.launches += 1
         _native.check(self.lib.zks_run_replicates_staged(self.handle, table.handle, ctypes.byref(cell), u.data_ptr(),
                                                          int(u_first), int(u_count), ks.data_ptr(),
                                                          gamma_hat.data_ptr(), status.data_ptr()))
@@ -146,7 +149,6 @@ class Engine:
         """
         r = np.ascontiguousarray(ranks, dtype=np.int64)
         self.bind_stream()
-        self.launches += 9  # init + 8 radix passes
         if out is not None:
             _native.check(
                 self.lib.zks_select_ranks_async(self.handle, values.data_ptr(), values.numel(), r.ctypes.data, r.size,
