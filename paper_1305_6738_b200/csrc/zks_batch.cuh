@@ -445,6 +445,11 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
   }
 }
 
+// per-warp shared memory of retry_kernel: histogram, queue, one sample (16-byte aligned)
+__host__ __device__ constexpr int retry_warp_bytes(int hist_words, int vals_stride) {
+  return round_up(hist_words * 4 + kKsQueueWords * 4 + vals_stride * 2, 16);
+}
+
 // Second attempts of the rows fit_ks_kernel listed (montecarlo.py:106-115), one warp each; exits
 // at once when the list is empty (the common case).
 template <bool kCount>
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) retry_kernel(ReplicateArgs a, const 
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int warp_bytes = a.hist_words * 4 + 3 * kKsQueue * 4 + a.vals_stride * 2;
+  const int warp_bytes = retry_warp_bytes(a.hist_words, a.vals_stride);
   unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;

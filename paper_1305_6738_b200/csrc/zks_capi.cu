@@ -420,7 +420,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
     const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::kDrawWarpBytes;
     const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
-    const size_t rsmem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + zks::kKsQueueWords * 4 + a.vals_stride * 2);
+    const size_t rsmem = guide_bytes + size_t(zks::kWarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
     int dper = 0, fper = 0;
     {
       int optin = 0;

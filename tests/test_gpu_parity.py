@@ -152,6 +152,29 @@ def test_replicates_match_oracle(zk, mle_mode, K, gamma, n, seed, rep, count):
         assert close(gh[j], want_gh), (j, gh[j], want_gh)
 
 
+@pytest.mark.parametrize("K,gamma,n", [(6, -20.0, 140), (8, -20.0, 128), (8, -22.0, 60), (8, -22.0, 1000)])
+def test_retries_match_oracle(zk, mle_mode, K, gamma, n):
+    # cells where first attempts fail often (NoRootError): retried replicates (status 1) take
+    # stream idx + 2^32 -- for n >= 128 through retry_kernel -- and double failures report 2
+    from oracle import port
+
+    count = 48
+    ks, gh, st = run_cell(K, gamma, n, 7, 0, 0, count)
+    seen = set()
+    for j in range(count):
+        try:
+            want_ks, want_gh, want_st = port.replicate(gamma, K, n, 7, j, 0)
+        except port.FailedTwice:
+            assert st[j] == 2, j
+            seen.add(2)
+            continue
+        assert st[j] == want_st, j
+        assert close(ks[j], want_ks), (j, ks[j], want_ks)
+        assert close(gh[j], want_gh), (j, gh[j], want_gh)
+        seen.add(int(want_st))
+    assert 1 in seen
+
+
 def test_run_simulation_matches_reference_golden(zk, golden):
     for si, row in enumerate(golden["sims"]):
         k, gamma, n, seed, reps_r, reps = row
