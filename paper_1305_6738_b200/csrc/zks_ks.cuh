@@ -218,6 +218,36 @@ __device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int&
   }
 }
 
+// Ascending bitonic sort of 32 * kSl values held as r[slot] (element slot * 32 + lane), fully
+// unrolled: shuffles within a slot, register exchanges across slots.
+template <int kSl>
+__device__ __forceinline__ void bitonic_sort_warp(uint32_t (&r)[kOverCap / 32], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * kSl; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+      for (int sl = 0; sl < kSl; ++sl) {
+        const int i = sl * 32 + lane;
+        const bool up = (i & k) == 0;
+        if (jj >= 32) {
+          const int ps = sl ^ (jj >> 5);
+          if (ps > sl) {
+            const uint32_t a0 = r[sl], a1 = r[ps];
+            const bool sw = up ? a0 > a1 : a0 < a1;
+            r[sl] = sw ? a1 : a0;
+            r[ps] = sw ? a0 : a1;
+          }
+        } else {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, r[sl], jj);
+          const bool low = (lane & jj) == 0;
+          r[sl] = (low == up) ? min(r[sl], o) : max(r[sl], o);
+        }
+      }
+    }
+  }
+}
+
 // KS of one sample with counts of 1..H in `hist`; values above H are found in
 // over_vals[0..over_n) (which may also hold values <= H: they are ignored).  `queue` is
 // kKsQueueWords u32 of per-warp shared memory.  `hist` is left dirty (see used_pages).
@@ -271,7 +301,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
   }
   if (!s.done && kmax > kKsHead) {
     s.S_head = s.S;
-    s.Dw = warp_max(s.D);
+    s.Dw = p.from_head ? p.D0 : warp_max(s.D);  // from_head: D0 is the warp's value
     c.La = __ldg(p.logs + kKsHead + 1);
     c.fa = exp(-g * c.La);
     constexpr double a = static_cast<double>(kKsHead + 1);
@@ -290,10 +320,12 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     if (!s.done && kmax > H) {
       // Values above H are few unless the tail is very heavy: with at most kOverCap of them,
       // take them in increasing order by repeated warp minimum over registers (no pages).
-      ks_flush<kArg>(s, c, q, lane, wk);  // the emptied queue stages the values
-      q = 0;
-      __syncwarp();
-      s.Dw = warp_max(s.D);
+      if (q) {
+        ks_flush<kArg>(s, c, q, lane, wk);  // the emptied queue stages the values
+        q = 0;
+        __syncwarp();
+        s.Dw = warp_max(s.D);
+      }
       const unsigned lt = (1u << lane) - 1u;
       uint32_t m = 0;
       for (uint32_t i0 = 0; i0 < over_n; i0 += 32) {
@@ -317,33 +349,13 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
           r[j] = idx < m ? queue[idx] : 0xffffffffu;
         }
         __syncwarp();
-        // bitonic sort of the kOverCap values across the warp (padding 0xffffffff sorts last)
-#pragma unroll
-        for (int k = 2; k <= static_cast<int>(kOverCap); k <<= 1) {
-          if (k > size) break;
-#pragma unroll
-          for (int jj = k >> 1; jj > 0; jj >>= 1) {
-#pragma unroll
-            for (int sl = 0; sl < kSlots; ++sl) {
-              if (sl * 32 >= size) break;
-              const int i = sl * 32 + lane;
-              const bool up = (i & k) == 0;
-              if (jj >= 32) {
-                const int ps = sl ^ (jj >> 5);
-                if (ps > sl) {
-                  const uint32_t a0 = r[sl], a1 = r[ps];
-                  const bool sw = up ? a0 > a1 : a0 < a1;
-                  r[sl] = sw ? a1 : a0;
-                  r[ps] = sw ? a0 : a1;
-                }
-              } else {
-                const uint32_t o = __shfl_xor_sync(0xffffffffu, r[sl], jj);
-                const bool low = (lane & jj) == 0;
-                r[sl] = (low == up) ? min(r[sl], o) : max(r[sl], o);
-              }
-            }
-          }
-        }
+        // bitonic sort of the occupied slots across the warp (padding 0xffffffff sorts last)
+        if (size == 32)
+          bitonic_sort_warp<1>(r, lane);
+        else if (size == 64)
+          bitonic_sort_warp<2>(r, lane);
+        else
+          bitonic_sort_warp<4>(r, lane);
         // runs of equal values: each run's last element becomes an endpoint entry
         const unsigned lt = (1u << lane) - 1u;
         int ne = 0;
