@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;
   uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
-  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  load_guide(guide, a.guide, a.guide_levels);
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
 
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kThreads) retry_kernel(ReplicateArgs a, const 
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;
   uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
-  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  load_guide(guide, a.guide, a.guide_levels);
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
   Work wk{};
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   // most one queued draw per pop and there are <= n/32 + 1 <= 33 pops, so u8 cannot overflow
   uint8_t* bins = wbase;
   double* queue = reinterpret_cast<double*>(wbase + (kKsHead + 1) * 32);
-  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  load_guide(guide, a.guide, a.guide_levels);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const bool two = a.guide_levels == 2;

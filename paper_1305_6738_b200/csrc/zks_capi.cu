@@ -191,10 +191,11 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   for (int j = 0; j < 4; ++j) t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
-  cudaError_t err = cudaMallocAsync(&mem, len * sizeof(double) + 2 * zks::kGuideLevel * sizeof(uint16_t), e->stream);
+  const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
+  cudaError_t err = cudaMallocAsync(&mem, cdf_slots * sizeof(double) + 2 * zks::kGuideLevel * sizeof(uint16_t), e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
-    t->guide = reinterpret_cast<uint16_t*>(t->cdf + len);
+    t->guide = reinterpret_cast<uint16_t*>(t->cdf + cdf_slots);
   }
   if (err == cudaSuccess) {
     // stage through a pinned slot so the copy never waits for kernels already queued

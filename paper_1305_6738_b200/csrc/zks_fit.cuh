@@ -63,15 +63,20 @@ __device__ __forceinline__ int fit_locate(const FitTable& T, double x, double& t
   return g.base + i;
 }
 
+// Interval layout (kFitStride doubles, 16-byte aligned): (mu_j, m2_j) pairs for j = 0..kFitDeg,
+// then norm_0..norm_kFitDeg -- one 16-byte load per Horner step of the Newton pair.
+
 // mean and slope of ln X at x (estimate.py:76-83)
 __device__ __forceinline__ void fit_mean_slope(const FitTable& T, double x, double& mean, double& slope) {
   double t;
-  const double* c = T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride;
-  double mu = __ldg(c + kFitDeg), m2 = __ldg(c + kFitCoef + kFitDeg);
+  const double2* c = reinterpret_cast<const double2*>(T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride);
+  const double2 top = __ldg(c + kFitDeg);
+  double mu = top.x, m2 = top.y;
 #pragma unroll
   for (int j = kFitDeg - 1; j >= 0; --j) {
-    mu = fma(mu, t, __ldg(c + j));
-    m2 = fma(m2, t, __ldg(c + kFitCoef + j));
+    const double2 cj = __ldg(c + j);
+    mu = fma(mu, t, cj.x);
+    m2 = fma(m2, t, cj.y);
   }
   mean = mu;
   slope = m2 - mu * mu;
@@ -80,9 +85,9 @@ __device__ __forceinline__ void fit_mean_slope(const FitTable& T, double x, doub
 __device__ __forceinline__ double fit_mean(const FitTable& T, double x) {
   double t;
   const double* c = T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride;
-  double mu = __ldg(c + kFitDeg);
+  double mu = __ldg(c + 2 * kFitDeg);
 #pragma unroll
-  for (int j = kFitDeg - 1; j >= 0; --j) mu = fma(mu, t, __ldg(c + j));
+  for (int j = kFitDeg - 1; j >= 0; --j) mu = fma(mu, t, __ldg(c + 2 * j));
   return mu;
 }
 
@@ -204,8 +209,13 @@ __global__ void fit_table_kernel(FitTable T, double* coef, const double* __restr
       tm1[i] = tj[i];
     }
   }
-  double* out = coef + static_cast<int64_t>(warp) * kFitStride + lane * kFitCoef;
-  for (int i = 0; i < kFitCoef; ++i) out[i] = mono[i];
+  double* out = coef + static_cast<int64_t>(warp) * kFitStride;
+  for (int i = 0; i < kFitCoef; ++i) {
+    if (lane < 2)
+      out[2 * i + lane] = mono[i];  // mu / m2 pairs
+    else
+      out[2 * kFitCoef + i] = mono[i];  // norm
+  }
 }
 
 // diagnostics: evaluate a table at arbitrary points

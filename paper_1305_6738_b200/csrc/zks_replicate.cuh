@@ -86,6 +86,14 @@ __device__ __forceinline__ void guide_bracket(double u, const uint16_t* guide, b
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// block-cooperative copy of the guide table (levels x kGuideLevel u16, 16-byte aligned) to smem
+__device__ __forceinline__ void load_guide(uint16_t* dst, const uint16_t* __restrict__ src, int levels) {
+  const int n = levels * kGuideLevel, n16 = n / 8;
+  for (int i = threadIdx.x; i < n16; i += blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+  for (int i = n16 * 8 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 // smallest k (1-based) with cdf[k-1] >= u, clamped to L (distribution.py:200-201)
 __device__ __forceinline__ uint32_t draw_value(double u, const uint16_t* __restrict__ guide,
                                                const double* __restrict__ cdf, uint32_t L, bool two) {
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + guide_bytes) + warp * (a.hist_words + 3 * kKsQueue);
   uint32_t* queue = hist + a.hist_words;
-  for (int i = threadIdx.x; i < a.guide_levels * kGuideLevel; i += blockDim.x) guide[i] = a.guide[i];
+  load_guide(guide, a.guide, a.guide_levels);
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
