@@ -209,7 +209,7 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
 
     # work counters for the roofline: one instrumented sweep outside the timed region
-    counters = torch.zeros(10, dtype=torch.int64, device=dev)
+    counters = torch.zeros(11, dtype=torch.int64, device=dev)
     eng.set_counters(counters)
     sweep()
     torch.cuda.synchronize()
@@ -247,13 +247,13 @@ def run_b200(args, world, rank, local):
         assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
 
     # roofline of the replicate kernel (dominant kernel)
-    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made = work
+    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made, redrawn = work
     exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
     terms = eval_terms + norm_terms + ks_terms
     # endpoint scoring: one exp + one expm1 per value (Euler-Maclaurin block)
     fp64_flops = terms * (exp_flops + 6.0) + ks_tails * (2 * exp_flops + 20.0)
     mul64 = 5.0 * draws  # Philox draws inside replicate kernels: 20 mulhilo per block of 4
-    hbm_bytes = 8.0 * staged + 17.0 * attempts  # staged uniforms read + (ks, gamma_hat, status) written
+    hbm_bytes = 4.0 * staged + 17.0 * attempts  # staged words read + (ks, gamma_hat, status) written
     launches = len(kernel_events) // max(args.steps, 1)  # replicate-kernel launches per sweep
     kernel_s = kernel_ms / 1e3 / args.steps  # per sweep
     hbm_peak = 6532.5e9

@@ -89,14 +89,15 @@ int zks_run_replicates(zks_engine* engine, const zks_table* table, const zks_cel
 
 /* Sweeps: the cells of build_table share base_seed (montecarlo.py:276-277), so cells with the
  * same n and repetition consume identical uniform streams.  zks_stage_uniforms writes the
- * uniforms of replicate indices [first, first+count) once (row i = index first+i, n draws,
- * row stride zks_staging_stride(n) doubles); zks_run_replicates_staged then runs one cell's
- * replicates from them instead of regenerating the streams.  Results are identical to
- * zks_run_replicates.  Both asynchronous. */
+ * draws of replicate indices [first, first+count) once as 32-bit words -- the top half of each
+ * Philox word, t = x >> 32 (row i = index first+i, n words, row stride zks_staging_stride(n)
+ * words); zks_run_replicates_staged then runs one cell's replicates from them instead of
+ * regenerating the streams (a replicate whose words leave a draw undecided is redrawn from
+ * Philox).  Results are identical to zks_run_replicates.  Both asynchronous. */
 int64_t zks_staging_stride(int64_t n);
 int zks_stage_uniforms(zks_engine* engine, uint64_t base_seed, uint64_t repetition, uint64_t first, uint64_t count,
-                       int64_t n, double* u_dev);
-int zks_run_replicates_staged(zks_engine* engine, const zks_table* table, const zks_cell* cell, const double* u_dev,
+                       int64_t n, uint32_t* words_dev);
+int zks_run_replicates_staged(zks_engine* engine, const zks_table* table, const zks_cell* cell, const uint32_t* words_dev,
                               uint64_t u_first, uint64_t u_count, double* ks_dev, double* gamma_hat_dev,
                               uint8_t* status_dev);
 
@@ -177,10 +178,10 @@ int zks_engine_set_mle_mode(zks_engine* engine, int mode);
 int zks_fit_eval(zks_engine* engine, int32_t support_k, const double* x_dev, int64_t count, double* mu_dev,
                  double* m2_dev, double* norm_dev);
 
-/* Accumulate the replicate kernels' work counters into counters_dev[0..10) (u64, caller
+/* Accumulate the replicate kernels' work counters into counters_dev[0..11) (u64, caller
  * zeroes): attempts, Philox draws, moment evaluations, moment terms, normaliser terms, KS
- * dense terms, KS endpoints, KS tiles, draws read from staged uniforms, Philox draws made by
- * the staging kernel.  NULL switches counting off. */
+ * dense terms, KS endpoints, KS tiles, draws read from staged words, Philox draws made by
+ * the staging kernel, staged replicates redrawn from Philox.  NULL switches counting off. */
 int zks_engine_set_counters(zks_engine* engine, unsigned long long* counters_dev);
 
 /* On-device pipe peaks measured by micro-kernels: out_host[0] = FP64 DFMA FLOP/s,

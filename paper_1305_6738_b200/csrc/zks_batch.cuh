@@ -12,6 +12,8 @@
 //     fit_ks_kernel fits and scores 32 rows per warp the same way, and retry_kernel takes the
 //     listed first-attempt failures.
 #pragma once
+#include <type_traits>
+
 #include "zks_replicate.cuh"
 
 namespace zks {
@@ -489,12 +491,15 @@ __global__ void __launch_bounds__(kThreads) retry_kernel(ReplicateArgs a, const 
   }
 }
 
-// Uniforms of replicate indices [first, first + count) of stream (seed, rep, .): row i holds the
-// n draws of index first + i (padded to `stride`), one warp per replicate.  Shared by every
-// cell of a sweep with the same (n, base_seed, repetition): build_table reuses base_seed for
-// all cells (montecarlo.py:276-277), so they consume identical streams.
+// Staged draw words of replicate indices [first, first + count) of stream (seed, rep, .): row i
+// holds, for the n draws of index first + i (padded to `stride`), the top 32 bits t = x >> 32 of
+// each Philox word x -- u = 1 - (x >> 11) 2^-53 lies in [1 - (t+1) 2^-32 + 2^-53, 1 - t 2^-32].
+// One warp per replicate.  Shared by every cell of a sweep with the same (n, base_seed,
+// repetition): build_table reuses base_seed for all cells (montecarlo.py:276-277), so they
+// consume identical streams.  Half the bytes of staged doubles; the rare draw whose 32 bits do
+// not decide its value sends its replicate back to the exact Philox path (draw_stats_kernel).
 __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t first,
-                                                             uint64_t count, int64_t n, int64_t stride, double* out,
+                                                             uint64_t count, int64_t n, int64_t stride, uint32_t* out,
                                                              unsigned long long* counters) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -503,15 +508,15 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
   for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < count; i += warps) {
     uint64_t k0, k1;
     stream_key(seed, rep, first + i, k0, k1);
-    double* row = out + i * stride;
+    uint32_t* row = out + i * stride;
     for (int64_t b = lane; b < nb; b += 32) {
       const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
-      double4 q;
-      q.x = uniform_open_closed(r.w[0]);
-      q.y = uniform_open_closed(r.w[1]);
-      q.z = uniform_open_closed(r.w[2]);
-      q.w = uniform_open_closed(r.w[3]);
-      *reinterpret_cast<double4*>(row + 4 * b) = q;
+      uint4 q;
+      q.x = static_cast<uint32_t>(r.w[0] >> 32);
+      q.y = static_cast<uint32_t>(r.w[1] >> 32);
+      q.z = static_cast<uint32_t>(r.w[2] >> 32);
+      q.w = static_cast<uint32_t>(r.w[3] >> 32);
+      __stcs(reinterpret_cast<uint4*>(row + 4 * b), q);
     }
     made += 4 * nb;
   }
@@ -520,17 +525,180 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 
 // The draw phase on its own, at high occupancy: one warp per replicate of [first, first+count)
 // draws its sample and writes what the fit and the KS scan need -- log-sum, min, max, the counts
-// of the values 1..kKsHead and the list of values above it -- so replicate_batch_kernel (with
-// a.pre_head) never touches the n draws again.  Uniforms from Philox, or from a staged sweep
-// buffer (a.ubuf).
+// of the values 1..kKsHead and the list of values above it -- so fit_ks_kernel never touches the
+// n draws again.  Draws from Philox, or from a staged sweep buffer of 32-bit words (a.ubuf).
 //
 // Values 1..4 are counted without a search: with h = cdf[0..3] in the kernel parameters,
 // #{u > h_j} over the sample gives the counts by differences (lower_bound semantics; h_j = +inf
-// from L-1 on clamps to L, distribution.py:200-201).  Draws with u > h_3 -- 5 % of them at
-// gamma = 2.5, 36 % at 1.5 -- are pushed onto a warp queue and resolved 32 at a time by the
-// guide + cdf search with every lane busy, so divergence costs nothing.
-constexpr int kDrawQueue = 160;  // doubles per warp: < 32 left over + 4 x 32 pushed per step
+// from L-1 on clamps to L, distribution.py:200-201).  On staged words the test is u > h_j <=>
+// t < a.tcut[j] (exact unless t == tcut[j]).  Draws above h_3 -- 5 % of them at gamma = 2.5,
+// 36 % at 1.5 -- are pushed onto a warp queue and resolved 32 at a time by the guide + cdf
+// search with every lane busy, so divergence costs nothing; a staged word is searched with its
+// largest u and accepted when the cdf entry below lies under its smallest u.  A replicate with
+// an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
+constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
 constexpr int kDrawWarpBytes = (kKsHead + 1) * 32 + kDrawQueue * 8;  // u8 bins [v][lane] + queue
+
+struct DrawRowOut {
+  double ls;
+  uint32_t mn, mx, m;
+};
+
+// One replicate row (warp-cooperative).  kStaged: 32-bit staged words (returns false when some
+// word was undecided: the caller redraws the row with kStaged = false).
+template <bool kStaged>
+__device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, const uint32_t* __restrict__ urow,
+                                         const uint16_t* __restrict__ guide, uint8_t* bins, void* qmem,
+                                         uint16_t* tail, uint16_t* head, DrawRowOut& o, int lane) {
+  using Q = typename std::conditional<kStaged, uint32_t, double>::type;
+  Q* queue = reinterpret_cast<Q*>(qmem);
+  const bool two = a.guide_levels == 2;
+  const int n = static_cast<int>(a.n);
+  const int nb = (n + 3) >> 2;
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t k0 = 0, k1 = 0;
+  if (!kStaged) stream_key(a.seed, a.rep, idx, k0, k1);
+  double ls = 0.0;
+  uint32_t mn = 0xffffffffu, mx = 0, m = 0;
+  uint32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0;  // this lane's #{u > h_j}
+  bool amb = false;                         // staged: some word undecided
+  int qn = 0;                               // queued draws (warp-uniform)
+  // one queued draw per lane: value by guide + search, then bin / tail
+  auto resolve = [&](Q q, bool ok) {
+    double ur, ulo = 0.0;
+    if (kStaged) {
+      ur = 1.0 - static_cast<double>(q) * 0x1p-32;  // largest u of the word (exact)
+      ulo = ur - (0x1p-32 - 0x1p-53);                // smallest u (exact)
+    } else {
+      ur = q;
+    }
+    uint32_t lo, hi;
+    guide_bracket(ur, guide, two, lo, hi);
+    if (!ok) hi = lo;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a.cdf + mid) >= ur)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    if (kStaged && ok && lo > 0u && __ldg(a.cdf + lo - 1) >= ulo) amb = true;
+    const uint32_t v = min(lo + 1, a.L);
+    if (ok) {
+      mn = min(mn, v);
+      mx = max(mx, v);
+      if (v <= kKsHead) ++bins[v * 32 + lane];
+    }
+    const bool big = ok && v > kKsHead;
+    const unsigned bm = __ballot_sync(0xffffffffu, big);
+    if (big) {
+      tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+      ls += __ldg(a.logs + v);
+    }
+    m += __popc(bm);
+  };
+  // staged rows: the next block's 16-byte load is issued before this block is used
+  uint4 p = make_uint4(0u, 0u, 0u, 0u);
+  if (kStaged && lane < nb) p = __ldcs(reinterpret_cast<const uint4*>(urow) + lane);
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    Q w4[4];
+    if (kStaged) {
+      w4[0] = p.x;
+      w4[1] = p.y;
+      w4[2] = p.z;
+      w4[3] = p.w;
+      p = b + 32 < nb ? __ldcs(reinterpret_cast<const uint4*>(urow) + b + 32) : make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) w4[w] = uniform_open_closed(r.w[w]);
+    }
+    if (4 * b + 4 > n) {  // past the sample: counts nowhere (value 1 is n - #{u > h_0})
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (4 * b + w >= n) w4[w] = kStaged ? Q(0xffffffffu) : Q(0);
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      bool big;
+      if (kStaged) {
+        const uint32_t t = static_cast<uint32_t>(w4[w]);
+        g0 += t < a.tcut[0];
+        g1 += t < a.tcut[1];
+        g2 += t < a.tcut[2];
+        big = t < a.tcut[3];
+        amb |= (t == a.tcut[0]) | (t == a.tcut[1]) | (t == a.tcut[2]) | (t == a.tcut[3]);
+      } else {
+        const double u = static_cast<double>(w4[w]);
+        g0 += u > a.cdf_head[0];
+        g1 += u > a.cdf_head[1];
+        g2 += u > a.cdf_head[2];
+        big = u > a.cdf_head[3];
+      }
+      g3 += big;
+      const unsigned bm = __ballot_sync(0xffffffffu, big);
+      if (big) queue[qn + __popc(bm & lt)] = w4[w];
+      qn += __popc(bm);
+    }
+    __syncwarp();
+    while (qn >= 32) {
+      qn -= 32;
+      const Q q = queue[qn + lane];
+      __syncwarp();
+      resolve(q, true);
+    }
+  }
+  if (qn) {
+    const bool ok = lane < qn;
+    const Q q = ok ? queue[lane] : Q(0);
+    __syncwarp();
+    resolve(q, ok);
+  }
+  // counts of 1..4 from the threshold counts
+  uint32_t c01 = g0 | (g1 << 16), c23 = g2 | (g3 << 16);  // n < 2^16
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    c01 += __shfl_xor_sync(0xffffffffu, c01, s);
+    c23 += __shfl_xor_sync(0xffffffffu, c23, s);
+  }
+  const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c23 & 0xffffu, G3 = c23 >> 16;
+  __syncwarp();
+  // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
+  uint32_t hc0 = 0, hc1 = 0;
+  const uint8_t* r0 = bins + (lane + 1) * 32;
+  const uint8_t* r1 = bins + (lane + 33) * 32;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int jj = (j + lane) & 7;  // rotate the word so the warp's loads spread over banks
+    const uint32_t w0 = reinterpret_cast<const uint32_t*>(r0)[jj];
+    const uint32_t w1 = reinterpret_cast<const uint32_t*>(r1)[jj];
+    hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
+    hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
+  }
+  hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
+  hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
+  __syncwarp();
+  if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;
+  if (lane == 1) hc0 = G0 - G1;
+  if (lane == 2) hc0 = G1 - G2;
+  if (lane == 3) hc0 = G2 - G3;
+  for (int v = 5; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
+  const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
+  if (!undecided) {
+    head[lane] = static_cast<uint16_t>(hc0);  // n <= 1024: u16 counts
+    head[lane + 32] = static_cast<uint16_t>(hc1);
+  }
+  mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
+  mx = max(mx, hc1 ? lane + 33u : (hc0 ? lane + 1u : 0u));
+  o.mn = warp_min_u32(mn);
+  o.mx = warp_max_u32(mx);
+  // log-sum: the head from its counts, the tail value by value (estimate.py:59-73 sums ln x_i)
+  ls += static_cast<double>(hc0) * __ldg(a.logs + lane + 1) + static_cast<double>(hc1) * __ldg(a.logs + lane + 33);
+  o.ls = warp_sum(ls);
+  o.m = m;
+  return !undecided;
+}
 
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(ReplicateArgs a, uint16_t* head_out,
@@ -544,163 +712,39 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   // lane-private u8 counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
   // most one queued draw per pop and there are <= n/32 + 1 <= 33 pops, so u8 cannot overflow
   uint8_t* bins = wbase;
-  double* queue = reinterpret_cast<double*>(wbase + (kKsHead + 1) * 32);
+  void* queue = wbase + (kKsHead + 1) * 32;
   load_guide(guide, a.guide, a.guide_levels);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
-  const bool two = a.guide_levels == 2;
-  const int n = static_cast<int>(a.n);
-  const int nb = (n + 3) >> 2;
-  const unsigned lt = (1u << lane) - 1u;
-  const double h0 = a.cdf_head[0], h1 = a.cdf_head[1], h2 = a.cdf_head[2], h3 = a.cdf_head[3];
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  unsigned long long philox = 0, staged = 0;
+  unsigned long long philox = 0, staged = 0, redrawn = 0;
   for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.count; i += warps) {
     const uint64_t idx = a.first + i;
     uint16_t* tail = tail_out + i * a.vals_stride;
-    uint64_t k0 = 0, k1 = 0;
-    const double* u = nullptr;
+    uint16_t* head = head_out + i * kKsHead;
+    DrawRowOut o;
+    bool done = false;
     if (a.ubuf) {
-      u = a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride;
-      staged += n;
-    } else {
-      stream_key(a.seed, a.rep, idx, k0, k1);
-      philox += n;
+      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, bins, queue, tail, head, o,
+                            lane);
+      staged += a.n;
+      redrawn += !done;
     }
-    double ls = 0.0;
-    uint32_t mn = 0xffffffffu, mx = 0, m = 0;
-    uint32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0;  // this lane's #{u > h_j}
-    int qn = 0;                               // queued draws (warp-uniform)
-    // one queued draw per lane: value by guide + search, then bin / tail
-    auto resolve = [&](double ur, bool ok) {
-      uint32_t lo, hi;
-      guide_bracket(ur, guide, two, lo, hi);
-      if (!ok) hi = lo;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a.cdf + mid) >= ur)
-          hi = mid;
-        else
-          lo = mid + 1;
-      }
-      const uint32_t v = min(lo + 1, a.L);
-      if (ok) {
-        mn = min(mn, v);
-        mx = max(mx, v);
-        if (v <= kKsHead) ++bins[v * 32 + lane];
-      }
-      const bool big = ok && v > kKsHead;
-      const unsigned bm = __ballot_sync(0xffffffffu, big);
-      if (big) {
-        tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
-        ls += __ldg(a.logs + v);
-      }
-      m += __popc(bm);
-    };
-    // staged rows: the next block's 32-byte load is issued before this block is used
-    double2 p0 = make_double2(0.0, 0.0), p1 = p0;
-    if (u && lane < nb) {
-      p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane));
-      p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * lane + 2));
+    if (!done) {
+      draw_row<false>(a, idx, nullptr, guide, bins, queue, tail, head, o, lane);
+      philox += a.n;
     }
-    for (int b0 = 0; b0 < nb; b0 += 32) {
-      const int b = b0 + lane;
-      double uu[4];
-      if (u) {
-        uu[0] = p0.x;
-        uu[1] = p0.y;
-        uu[2] = p1.x;
-        uu[3] = p1.y;
-        if (b + 32 < nb) {
-          p0 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32)));
-          p1 = __ldcs(reinterpret_cast<const double2*>(u + 4 * (b + 32) + 2));
-        } else {
-          p0 = p1 = make_double2(0.0, 0.0);
-        }
-      } else {
-        const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) uu[w] = uniform_open_closed(r.w[w]);
-      }
-      if (4 * b + 4 > n) {  // past the sample: u = 0 counts nowhere (value 1 is n - #{u > h_0})
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-          if (4 * b + w >= n) uu[w] = 0.0;
-      }
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        g0 += uu[w] > h0;
-        g1 += uu[w] > h1;
-        g2 += uu[w] > h2;
-        const bool big = uu[w] > h3;
-        g3 += big;
-        const unsigned bm = __ballot_sync(0xffffffffu, big);
-        if (big) queue[qn + __popc(bm & lt)] = uu[w];
-        qn += __popc(bm);
-      }
-      __syncwarp();
-      while (qn >= 32) {
-        qn -= 32;
-        const double ur = queue[qn + lane];
-        __syncwarp();
-        resolve(ur, true);
-      }
-    }
-    if (qn) {
-      const bool ok = lane < qn;
-      const double ur = ok ? queue[lane] : 0.0;
-      __syncwarp();
-      resolve(ur, ok);
-    }
-    // counts of 1..4 from the threshold counts
-    uint32_t c01 = g0 | (g1 << 16), c23 = g2 | (g3 << 16);  // n < 2^16
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      c01 += __shfl_xor_sync(0xffffffffu, c01, o);
-      c23 += __shfl_xor_sync(0xffffffffu, c23, o);
-    }
-    const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c23 & 0xffffu, G3 = c23 >> 16;
-    __syncwarp();
-    // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
-    uint32_t hc0 = 0, hc1 = 0;
-    const uint8_t* r0 = bins + (lane + 1) * 32;
-    const uint8_t* r1 = bins + (lane + 33) * 32;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int jj = (j + lane) & 7;  // rotate the word so the warp's loads spread over banks
-      const uint32_t w0 = reinterpret_cast<const uint32_t*>(r0)[jj];
-      const uint32_t w1 = reinterpret_cast<const uint32_t*>(r1)[jj];
-      hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
-      hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
-    }
-    hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
-    hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
-    __syncwarp();
-    if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;
-    if (lane == 1) hc0 = G0 - G1;
-    if (lane == 2) hc0 = G1 - G2;
-    if (lane == 3) hc0 = G2 - G3;
-    for (int v = 5; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
-    uint16_t* head = head_out + i * kKsHead;  // n <= 1024: u16 counts
-    head[lane] = static_cast<uint16_t>(hc0);
-    head[lane + 32] = static_cast<uint16_t>(hc1);
-    mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
-    mx = max(mx, hc1 ? lane + 33u : (hc0 ? lane + 1u : 0u));
-    mn = warp_min_u32(mn);
-    mx = warp_max_u32(mx);
-    // log-sum: the head from its counts, the tail value by value (estimate.py:59-73 sums ln x_i)
-    ls += static_cast<double>(hc0) * __ldg(a.logs + lane + 1) + static_cast<double>(hc1) * __ldg(a.logs + lane + 33);
-    ls = warp_sum(ls);
     if (lane == 0) {
-      ls_out[i] = ls;
-      min_out[i] = mn;
-      max_out[i] = mx;
-      m_out[i] = m;
+      ls_out[i] = o.ls;
+      min_out[i] = o.mn;
+      max_out[i] = o.mx;
+      m_out[i] = o.m;
     }
   }
   if (kCount && lane == 0) {
     if (philox) atomicAdd(a.counters + 1, philox);
     if (staged) atomicAdd(a.counters + 8, staged);
+    if (redrawn) atomicAdd(a.counters + kWorkFields + 1, redrawn);
   }
 }
 

@@ -72,6 +72,21 @@ struct zks_engine {
 
 namespace {
 
+// Staged words t = x >> 32 of Philox words x, u = 1 - (x >> 11) 2^-53 (stream.py:57-63):
+// u > h <=> m = x >> 11 < M(h), M(h) = #{m : 1 - m 2^-53 > h} (exact, by bisection on m).
+// Hence t < M >> 21 decides u > h, t > M >> 21 decides u <= h, and t == M >> 21 is undecided.
+uint32_t staged_cut(double h) {
+  uint64_t lo = 0, hi = uint64_t(1) << 53;  // smallest m with 1 - m 2^-53 <= h in [lo, hi]
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (1.0 - static_cast<double>(mid) * 0x1p-53 <= h)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return static_cast<uint32_t>(std::min<uint64_t>(lo >> 21, 0xffffffffu));
+}
+
 // every kernel launch goes through here: the error check and the engine's launch count
 cudaError_t launched(zks_engine* e) {
   ++e->launches;
@@ -104,11 +119,12 @@ struct zks_table {
   uint16_t* guide = nullptr;
   uint32_t len = 0;
   double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
+  uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on staged 32-bit words
 };
 
 extern "C" {
 
-int zks_version(void) { return 1; }
+int zks_version(void) { return 2; }
 
 const char* zks_last_error(void) { return g_error.c_str(); }
 
@@ -188,7 +204,10 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   zks_table* t = new zks_table();
   t->engine = e;
   t->len = static_cast<uint32_t>(len);
-  for (int j = 0; j < 4; ++j) t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
+  for (int j = 0; j < 4; ++j) {
+    t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
+    t->tcut[j] = staged_cut(t->head[j]);
+  }
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
   const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
@@ -232,7 +251,7 @@ void zks_table_destroy(zks_table* t) {
 
 namespace {
 struct Staged {
-  const double* u;
+  const uint32_t* u;
   int64_t stride;
   uint64_t first, count;
   int64_t n;
@@ -249,7 +268,7 @@ int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, dou
 int64_t zks_staging_stride(int64_t n) { return (n + 3) / 4 * 4; }
 
 int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64_t first, uint64_t count, int64_t n,
-                       double* u_dev) {
+                       uint32_t* u_dev) {
   if (!e || !u_dev) return fail(ZKS_EINVAL, "NULL argument");
   if (n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)n);
   if (count == 0) return ZKS_OK;
@@ -261,7 +280,7 @@ int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64
   return ZKS_OK;
 }
 
-int zks_run_replicates_staged(zks_engine* e, const zks_table* t, const zks_cell* c, const double* u_dev,
+int zks_run_replicates_staged(zks_engine* e, const zks_table* t, const zks_cell* c, const uint32_t* u_dev,
                               uint64_t u_first, uint64_t u_count, double* ks_dev, double* gh_dev, uint8_t* st_dev) {
   if (!u_dev) return fail(ZKS_EINVAL, "NULL argument");
   if (!c) return fail(ZKS_EINVAL, "cell is NULL");
@@ -288,7 +307,10 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   zks::ReplicateArgs a;
   a.cdf = t->cdf;
   a.guide = t->guide;
-  for (int j = 0; j < 4; ++j) a.cdf_head[j] = t->head[j];
+  for (int j = 0; j < 4; ++j) {
+    a.cdf_head[j] = t->head[j];
+    a.tcut[j] = t->tcut[j];
+  }
   a.logs = e->logs;
   a.L = L;
   a.K = c->support_k;

@@ -58,7 +58,7 @@ struct ReplicateArgs {
   int guide_levels;              // 1, or 2 for long tables (L > 4096)
   // staged uniforms (shared by the cells of a sweep with equal n and seed): u of replicate
   // index i, draw j at ubuf[(i - ubuf_first) * ubuf_stride + j]; NULL = generate (Philox)
-  const double* ubuf;
+  const uint32_t* ubuf;
   int64_t ubuf_stride;
   uint64_t ubuf_first;
   // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: u16 counts of
@@ -72,6 +72,7 @@ struct ReplicateArgs {
   const uint32_t* pre_max;
   uint64_t pre_first;
   double inv_n;  // 1 / n
+  uint32_t tcut[4];     // staged words: u > cdf_head[j] <=> t < tcut[j] (undecided at equality)
   double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
 };
 

@@ -126,7 +126,7 @@ class Engine:
         return int(self.lib.zks_staging_stride(int(n)))
 
     def stage_uniforms(self, seed: int, repetition: int, first: int, count: int, n: int, out) -> None:
-        """Uniform rows of replicate indices [first, first+count) into device float64 ``out``."""
+        """Staged 32-bit draw words of replicate indices [first, first+count) into device int32 ``out``."""
         self.bind_stream()
         _native.check(self.lib.zks_stage_uniforms(self.handle, int(seed), int(repetition), int(first), int(count),
                                                   int(n), out.data_ptr()))

@@ -293,11 +293,11 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     dev = f"cuda:{eng.device}"
     ranks = quantile_ranks(total, cfg0.quantiles)
     stride = eng.staging_stride(n)
-    chunk = max(1, min(stop - first, _STAGE_BYTES // (8 * stride)))
+    chunk = max(1, min(stop - first, _STAGE_BYTES // (4 * stride)))
     key = ("stage", eng.device)
     ubuf = _SLABS.get(key)
     if ubuf is None or ubuf.numel() < chunk * stride:
-        ubuf = torch.empty(chunk * stride, dtype=torch.float64, device=dev)
+        ubuf = torch.empty(chunk * stride, dtype=torch.int32, device=dev)  # 32-bit staged words
         _SLABS[key] = ubuf
     outs = []
     stream = eng.bind_stream()

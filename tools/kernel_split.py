@@ -8,7 +8,7 @@ from paper_1305_6738_b200.distribution import Support, sampling_cdf
 g = float(sys.argv[1]); n = int(sys.argv[2]); R = int(sys.argv[3]) if len(sys.argv) > 3 else 1000000
 eng = engine.get_engine()
 ks = torch.empty(R, dtype=torch.float64, device='cuda'); gh = torch.empty_like(ks); st = torch.empty(R, dtype=torch.uint8, device='cuda')
-u = torch.empty(R * eng.staging_stride(n), dtype=torch.float64, device='cuda')
+u = torch.empty(R * eng.staging_stride(n), dtype=torch.int32, device='cuda')
 t = eng.table(g, None, lambda: sampling_cdf(g, Support(None)))
 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 for it in range(2):

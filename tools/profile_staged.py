@@ -10,7 +10,7 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 R = int(sys.argv[3]) if len(sys.argv) > 3 else 200000
 eng = engine.get_engine()
 ks = torch.empty(R, dtype=torch.float64, device='cuda'); gh = torch.empty_like(ks); st = torch.empty(R, dtype=torch.uint8, device='cuda')
-u = torch.empty(R * eng.staging_stride(n), dtype=torch.float64, device='cuda')
+u = torch.empty(R * eng.staging_stride(n), dtype=torch.int32, device='cuda')
 t = eng.table(g, None, lambda: sampling_cdf(g, Support(None)))
 eng.stage_uniforms(1, 0, 0, R, n, u)
 for _ in range(3):

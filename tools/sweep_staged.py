@@ -11,7 +11,7 @@ R = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
 ns = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (500, 1000)
 ks = torch.empty(R, dtype=torch.float64, device='cuda'); gh = torch.empty_like(ks); st = torch.empty(R, dtype=torch.uint8, device='cuda')
 for n in ns:
-    u = torch.empty(R * eng.staging_stride(n), dtype=torch.float64, device='cuda')
+    u = torch.empty(R * eng.staging_stride(n), dtype=torch.int32, device='cuda')
     eng.stage_uniforms(1, 0, 0, R, n, u)
     line = []
     tot = 0.0
