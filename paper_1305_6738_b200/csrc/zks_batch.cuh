@@ -539,6 +539,20 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
 constexpr int kDrawWarpBytes = (kKsHead + 1) * 32 + kDrawQueue * 8;  // u8 bins [v][lane] + queue
 
+// g += (t < T), as one compare and one predicated add
+__device__ __forceinline__ void inc_if_lt(uint32_t& g, uint32_t t, uint32_t T) {
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(g) : "r"(t), "r"(T));
+}
+
+// f |= 1 if t equals any of T0..T3
+__device__ __forceinline__ void flag_if_any_eq(uint32_t& f, uint32_t t, uint32_t T0, uint32_t T1, uint32_t T2,
+                                               uint32_t T3) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\tsetp.eq.or.u32 p, %1, %3, p;\n\t"
+      "setp.eq.or.u32 p, %1, %4, p;\n\tsetp.eq.or.u32 p, %1, %5, p;\n\t@p or.b32 %0, %0, 1;\n\t}"
+      : "+r"(f)
+      : "r"(t), "r"(T0), "r"(T1), "r"(T2), "r"(T3));
+}
+
 struct DrawRowOut {
   double ls;
   uint32_t mn, mx, m;
@@ -560,8 +574,8 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   if (!kStaged) stream_key(a.seed, a.rep, idx, k0, k1);
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0, m = 0;
-  uint32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0;  // this lane's #{u > h_j}
-  bool amb = false;                         // staged: some word undecided
+  uint32_t g0 = 0, g1 = 0, g2 = 0;  // this lane's #{u > h_j}, j < 3
+  uint32_t amb = 0;                         // staged: some word undecided
   int qn = 0;                               // queued draws (warp-uniform)
   // one queued draw per lane: value by guide + search, then bin / tail
   auto resolve = [&](Q q, bool ok) {
@@ -582,7 +596,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       else
         lo = mid + 1;
     }
-    if (kStaged && ok && lo > 0u && __ldg(a.cdf + lo - 1) >= ulo) amb = true;
+    if (kStaged && ok && lo > 0u && __ldg(a.cdf + lo - 1) >= ulo) amb = 1u;
     const uint32_t v = min(lo + 1, a.L);
     if (ok) {
       mn = min(mn, v);
@@ -600,8 +614,10 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   // staged rows: the next block's 16-byte load is issued before this block is used
   uint4 p = make_uint4(0u, 0u, 0u, 0u);
   if (kStaged && lane < nb) p = __ldcs(reinterpret_cast<const uint4*>(urow) + lane);
-  for (int b0 = 0; b0 < nb; b0 += 32) {
-    const int b = b0 + lane;
+  uint32_t qtot = 0;  // words pushed (warp-uniform): #{u > h_3}
+  // one step: lane b's block of 4 draws; kMasked for the last step (words past n count nowhere:
+  // value 1 is n - #{u > h_0})
+  auto step = [&](int b, auto masked) {
     Q w4[4];
     if (kStaged) {
       w4[0] = p.x;
@@ -614,7 +630,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
 #pragma unroll
       for (int w = 0; w < 4; ++w) w4[w] = uniform_open_closed(r.w[w]);
     }
-    if (4 * b + 4 > n) {  // past the sample: counts nowhere (value 1 is n - #{u > h_0})
+    if (decltype(masked)::value) {
 #pragma unroll
       for (int w = 0; w < 4; ++w)
         if (4 * b + w >= n) w4[w] = kStaged ? Q(0xffffffffu) : Q(0);
@@ -624,11 +640,11 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       bool big;
       if (kStaged) {
         const uint32_t t = static_cast<uint32_t>(w4[w]);
-        g0 += t < a.tcut[0];
-        g1 += t < a.tcut[1];
-        g2 += t < a.tcut[2];
+        inc_if_lt(g0, t, a.tcut[0]);
+        inc_if_lt(g1, t, a.tcut[1]);
+        inc_if_lt(g2, t, a.tcut[2]);
+        flag_if_any_eq(amb, t, a.tcut[0], a.tcut[1], a.tcut[2], a.tcut[3]);
         big = t < a.tcut[3];
-        amb |= (t == a.tcut[0]) | (t == a.tcut[1]) | (t == a.tcut[2]) | (t == a.tcut[3]);
       } else {
         const double u = static_cast<double>(w4[w]);
         g0 += u > a.cdf_head[0];
@@ -636,10 +652,10 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
         g2 += u > a.cdf_head[2];
         big = u > a.cdf_head[3];
       }
-      g3 += big;
       const unsigned bm = __ballot_sync(0xffffffffu, big);
       if (big) queue[qn + __popc(bm & lt)] = w4[w];
       qn += __popc(bm);
+      qtot += __popc(bm);
     }
     __syncwarp();
     while (qn >= 32) {
@@ -648,7 +664,11 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       __syncwarp();
       resolve(q, true);
     }
-  }
+  };
+  const int full = (n >> 2) & ~31;  // blocks in steps whose 4 x 32 words are all in the sample
+  int b0 = 0;
+  for (; b0 < full; b0 += 32) step(b0 + lane, std::false_type{});
+  for (; b0 < nb; b0 += 32) step(b0 + lane, std::true_type{});
   if (qn) {
     const bool ok = lane < qn;
     const Q q = ok ? queue[lane] : Q(0);
@@ -656,13 +676,13 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     resolve(q, ok);
   }
   // counts of 1..4 from the threshold counts
-  uint32_t c01 = g0 | (g1 << 16), c23 = g2 | (g3 << 16);  // n < 2^16
+  uint32_t c01 = g0 | (g1 << 16), c2 = g2;  // n < 2^16
 #pragma unroll
   for (int s = 16; s; s >>= 1) {
     c01 += __shfl_xor_sync(0xffffffffu, c01, s);
-    c23 += __shfl_xor_sync(0xffffffffu, c23, s);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, s);
   }
-  const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c23 & 0xffffu, G3 = c23 >> 16;
+  const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c2, G3 = qtot;
   __syncwarp();
   // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
   uint32_t hc0 = 0, hc1 = 0;
@@ -683,7 +703,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   if (lane == 1) hc0 = G0 - G1;
   if (lane == 2) hc0 = G1 - G2;
   if (lane == 3) hc0 = G2 - G3;
-  for (int v = 5; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
+  for (int i = lane; i < (kKsHead - 4) * 8; i += 32) reinterpret_cast<uint32_t*>(bins + 5 * 32)[i] = 0u;
   const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
   if (!undecided) {
     head[lane] = static_cast<uint16_t>(hc0);  // n <= 1024: u16 counts
