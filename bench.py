@@ -10,8 +10,9 @@ per replicate sample -> MLE refit -> KS, then the 4 order-statistic cutoffs per 
   value        device time of the sweep with draw tables resident, L2 flushed between steps
   e2e          the public API paper_1305_6738_b200.build_table (parallel.build_table at N>1):
                host-built draw tables uploaded every step, cutoffs copied back to the host
-  roofline     replicate kernel work counted in-kernel (FP64 power terms, Philox draws) over
-               its measured launch time, against on-device micro-benchmarked pipe peaks
+  roofline     the dominant kernel (largest device time, CUDA events per launch): algorithmic
+               bytes per launch over its launch time against the measured HBM peak; plus the
+               FP64 / 64-bit-multiply pipe work of the replicate math against on-device probes
   cpu_baseline the CPU oracle (numpy restatement of the reference, bit-identical to it) on
                all host cores over a bounded sample of the same sweep
 
@@ -167,6 +168,97 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- roofline
+
+def hbm_peak_gbs() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
+    except (OSError, KeyError, ValueError):
+        return 7700.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+
+
+def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms) -> dict:
+    """Roofline of the dominant kernel of the sweep (largest summed device time in the timed
+    region, CUDA events around every launch on the engine stream).
+
+    Algorithmic bytes per kernel kind, per sweep, from the reference algorithm's data flow and
+    the in-kernel work counters:
+      stage   4 B per staged draw word written
+      draw    4 B per staged word read + 148 B per pre-drawn row (u16 head counts 128, log-sum 8,
+              min / max / tail length 12) + 2 B per tail value
+      fit     the rows and tail values read back + 17 B per replicate written (ks, gamma_hat, status)
+      batch   17 B per replicate written (n < 128: draws, fits and KS stay on chip)
+      select  8 B per KS value per radix pass (8 passes)
+    """
+    (attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made, redrawn,
+     pre_rows, pre_tails) = work
+    per_gpu = R if world == 1 else shard[1] - shard[0]
+    small_cells = sum(1 for n in NS if n < 128) * len(GAMMAS)
+    row_bytes = 128 + 8 + 12
+    alg = {
+        "stage": 4.0 * staged_made,
+        "draw": 4.0 * staged + row_bytes * pre_rows + 2.0 * pre_tails,
+        "fit": row_bytes * pre_rows + 2.0 * pre_tails + 17.0 * pre_rows,
+        "batch": 17.0 * small_cells * per_gpu,
+        "select": 8.0 * 8 * ncells * R,
+    }
+    steps = max(args.steps, 1)
+    kern = {k: {"ms_per_sweep": ms / steps, "launches_per_sweep": n / steps} for k, (ms, n) in ktimes.items() if n}
+    kernel_ms = sum(v["ms_per_sweep"] for v in kern.values())
+    for k, v in kern.items():
+        v["share_of_kernel_time"] = v["ms_per_sweep"] / kernel_ms if kernel_ms else None
+        if k in alg:
+            v["algorithmic_gb_per_sweep"] = alg[k] / 1e9
+            v["achieved_gbs"] = alg[k] / (v["ms_per_sweep"] / 1e3) / 1e9 if v["ms_per_sweep"] else None
+    dom = max(kern, key=lambda k: kern[k]["ms_per_sweep"])
+    peak, peak_src = hbm_peak_gbs()
+    d = kern[dom]
+    per_launch_bytes = alg.get(dom, 0.0) / max(d["launches_per_sweep"], 1)
+    per_launch_ms = d["ms_per_sweep"] / max(d["launches_per_sweep"], 1)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "kernel": KERNEL_NAMES.get(dom, dom), "algorithmic_bytes_per_launch": per_launch_bytes,
+            "launch_ms": per_launch_ms, "peak_source": peak_src,
+            "timing": "CUDA events around every launch on the engine stream, summed over the timed steps"}
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("kernel") == roof["kernel"]:
+            ratio = tr["dram_bytes"] / tr["algorithmic_bytes"]
+            roof["traffic"] = ratio * per_launch_bytes
+            roof["traffic_over_algorithmic"] = ratio
+            roof["traffic_source"] = tr["source"]
+    except (OSError, KeyError, ValueError, ZeroDivisionError):
+        pass
+    # the pipes that actually bound the replicate math (SURVEY.md 8(d)): FP64 power terms and
+    # 64-bit Philox multiplies, counted from the reference algorithm, against on-device probes
+    exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
+    terms = eval_terms + norm_terms + ks_terms
+    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * (2 * exp_flops + 20.0)
+    mul64 = 5.0 * (draws + staged_made)
+    kernel_s = kernel_ms / 1e3
+    roof["compute"] = {
+        "fp64": {"achieved_tflops": fp64_flops / kernel_s / 1e12, "peak_tflops": peaks["dfma_flops"] / 1e12,
+                 "t_ideal_ms_per_sweep": fp64_flops / peaks["dfma_flops"] * 1e3},
+        "int64_mul": {"achieved_tmul_s": mul64 / kernel_s / 1e12, "peak_tmul_s": peaks["mul64_per_s"] / 1e12,
+                      "t_ideal_ms_per_sweep": mul64 / peaks["mul64_per_s"] * 1e3},
+        "peak_source": "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)",
+        "work_per_sweep": {"replicates": ncells * per_gpu, "attempts": attempts, "philox_draws": draws,
+                           "staged_words_read": staged, "staged_words_made": staged_made,
+                           "staged_rows_redrawn": redrawn, "moment_evals": evals, "power_terms": terms,
+                           "ks_tail_endpoints": ks_tails, "fp64_exp_dfma_equiv": exp_flops},
+    }
+    roof["kernels"] = kern
+    roof["kernel_share_of_step"] = kernel_ms / total_ms * steps if total_ms else None
+    return roof
+
+
+KERNEL_NAMES = {"stage": "stage_uniforms_kernel", "draw": "draw_stats_kernel", "fit": "fit_ks_kernel",
+                "retry": "retry_kernel", "batch": "replicate_batch_kernel", "single": "replicate_kernel",
+                "select": "select_pass_kernel", "other": "other"}
+
+
 # ----------------------------------------------------------------------------- GPU leg
 
 def run_b200(args, world, rank, local):
@@ -195,12 +287,9 @@ def run_b200(args, world, rank, local):
         if world > 1:
             dist.barrier()
 
-    kernel_events = []
-
-    def sweep(record_kernels=False):
+    def sweep():
         plans = [mc._CellPlan(cfg) for cfg in configs]
-        mc._enqueue_plans(eng, plans, shard=shard, gather=gather,
-                          kernel_events=kernel_events if record_kernels else None)
+        mc._enqueue_plans(eng, plans, shard=shard, gather=gather)
         return plans
 
     # warm-up (also builds and uploads the 21 draw tables)
@@ -209,7 +298,7 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
 
     # work counters for the roofline: one instrumented sweep outside the timed region
-    counters = torch.zeros(11, dtype=torch.int64, device=dev)
+    counters = torch.zeros(13, dtype=torch.int64, device=dev)
     eng.set_counters(counters)
     sweep()
     torch.cuda.synchronize()
@@ -217,11 +306,13 @@ def run_b200(args, world, rank, local):
     work = [int(x) for x in counters.cpu().tolist()]
     peaks = eng.probe_peaks()
 
-    # timed region
+    # timed region; every engine kernel launch is bracketed by CUDA events on its stream
     stream = torch.cuda.current_stream()
     total_ms = 0.0
     plans = None
     launches0 = eng.launches
+    eng.set_timing(True)
+    eng.kernel_times()  # reset
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -229,65 +320,25 @@ def run_b200(args, world, rank, local):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            plans = sweep(record_kernels=True)
+            plans = sweep()
             e1.record(stream)
             torch.cuda.synchronize()
             barrier()
             total_ms += e0.elapsed_time(e1)
     clock = clocks.summary()
+    ktimes = eng.kernel_times()
+    eng.set_timing(False)
     timed_launches = eng.launches - launches0
-    kernel_ms = sum(a.elapsed_time(b) for a, b in kernel_events)
-    t = torch.tensor([total_ms, kernel_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kernel_ms = t.tolist()
+    total_ms = float(t.item())
     value = args.steps * ncells * R / (total_ms / 1e3)
     rows = {(p.config.gamma, p.config.n): tuple(c for _, c in mc._finish_cell(eng, p, shard=shard)) for p in plans}
     for row in rows.values():
         assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
 
-    # roofline of the replicate kernel (dominant kernel)
-    attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made, redrawn = work
-    exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
-    terms = eval_terms + norm_terms + ks_terms
-    # endpoint scoring: one exp + one expm1 per value (Euler-Maclaurin block)
-    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * (2 * exp_flops + 20.0)
-    mul64 = 5.0 * draws  # Philox draws inside replicate kernels: 20 mulhilo per block of 4
-    hbm_bytes = 4.0 * staged + 17.0 * attempts  # staged words read + (ks, gamma_hat, status) written
-    launches = len(kernel_events) // max(args.steps, 1)  # replicate-kernel launches per sweep
-    kernel_s = kernel_ms / 1e3 / args.steps  # per sweep
-    hbm_peak = 6532.5e9
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            hbm_peak = float(json.load(fh)["hbm_gbs"]) * 1e9
-    except (OSError, KeyError, ValueError):
-        pass
-    bounds = {
-        "fp64": (fp64_flops / peaks["dfma_flops"], fp64_flops / kernel_s / 1e12, peaks["dfma_flops"] / 1e12, "TFLOP/s"),
-        "int64-mul": (mul64 / peaks["mul64_per_s"], mul64 / kernel_s / 1e12, peaks["mul64_per_s"] / 1e12, "Tmul64/s"),
-        "hbm": (hbm_bytes / hbm_peak, hbm_bytes / kernel_s / 1e9, hbm_peak / 1e9, "GB/s"),
-    }
-    name = max(bounds, key=lambda b: bounds[b][0])
-    t_ideal, achieved, peak, unit = bounds[name]
-    roof = {"bound": name, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak}
-    roof["t_ideal_ms_per_sweep"] = {b: v[0] * 1e3 for b, v in bounds.items()}
-    roof["staging_philox_draws"] = staged_made
-    roof["traffic"] = None
-    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh)
-        roof["traffic"] = tr["dram_bytes_read_per_launch"] + tr["dram_bytes_write_per_launch"]
-        roof["traffic_source"] = tr["source"]
-    except (OSError, KeyError, ValueError):
-        pass
-    roof["peak_source"] = "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)"
-    roof["work_per_sweep"] = {"replicates": ncells * (R if world == 1 else shard[1] - shard[0]),
-                              "attempts": attempts, "draws": draws, "staged_draws": staged, "moment_evals": evals,
-                              "power_terms": terms, "ks_tail_endpoints": ks_tails,
-                              "fp64_exp_dfma_equiv": exp_flops}
-    roof["kernel_ms_per_launch"] = kernel_ms / args.steps / max(launches, 1)
-    roof["kernel_share_of_step"] = kernel_ms / total_ms
-
+    roof = roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms)
     # end to end through the public API (host tables built + uploaded each step)
     e2e = None
     if not args.no_e2e:

@@ -72,6 +72,23 @@ int zks_engine_sync(zks_engine* engine);
  * entry point).  Diagnostics: bench.py reports the timed-region delta as gpu_launches. */
 int zks_engine_launches(zks_engine* engine, unsigned long long* out);
 
+/* Per-kernel device time: with timing on, every launch is bracketed by CUDA events on the
+ * engine stream; zks_engine_kernel_times synchronises the stream, writes the summed milliseconds
+ * and launch counts per kind (arrays of ZKS_KERNEL_KINDS) since the last call, and resets. */
+enum {
+  ZKS_KERNEL_STAGE = 0,  /* stage_uniforms_kernel: staged draw words of a sweep */
+  ZKS_KERNEL_DRAW = 1,   /* draw_stats_kernel: samples -> head counts, tail values, log-sums */
+  ZKS_KERNEL_FIT = 2,    /* fit_ks_kernel: exponent fits + KS of pre-drawn rows */
+  ZKS_KERNEL_RETRY = 3,  /* retry_kernel: second attempts */
+  ZKS_KERNEL_BATCH = 4,  /* replicate_batch_kernel: n < 128, one replicate per lane */
+  ZKS_KERNEL_SINGLE = 5, /* replicate_kernel: n > 1024 or direct-sum MLE, one warp per replicate */
+  ZKS_KERNEL_SELECT = 6, /* radix selection of order statistics */
+  ZKS_KERNEL_OTHER = 7,  /* tables, user-sample fits, series, draws */
+  ZKS_KERNEL_KINDS = 8
+};
+int zks_engine_set_timing(zks_engine* engine, int on);
+int zks_engine_kernel_times(zks_engine* engine, double* ms_out, unsigned long long* launches_out);
+
 /* Upload a host-built sampling CDF (ZipfModel._sampling_cdf, distribution.py:99-105):
  * cdf_host[k-1] = P(X <= k) for k = 1..len, len = K or 65535, and build its guide table.
  * Replaces the per-process lru_cache'd table build of _generating_model (montecarlo.py:82-86). */
@@ -178,10 +195,11 @@ int zks_engine_set_mle_mode(zks_engine* engine, int mode);
 int zks_fit_eval(zks_engine* engine, int32_t support_k, const double* x_dev, int64_t count, double* mu_dev,
                  double* m2_dev, double* norm_dev);
 
-/* Accumulate the replicate kernels' work counters into counters_dev[0..11) (u64, caller
+/* Accumulate the replicate kernels' work counters into counters_dev[0..13) (u64, caller
  * zeroes): attempts, Philox draws, moment evaluations, moment terms, normaliser terms, KS
  * dense terms, KS endpoints, KS tiles, draws read from staged words, Philox draws made by
- * the staging kernel, staged replicates redrawn from Philox.  NULL switches counting off. */
+ * the staging kernel, staged replicates redrawn from Philox, rows written by the draw kernel
+ * (n >= 128), tail values in those rows.  NULL switches counting off. */
 int zks_engine_set_counters(zks_engine* engine, unsigned long long* counters_dev);
 
 /* On-device pipe peaks measured by micro-kernels: out_host[0] = FP64 DFMA FLOP/s,

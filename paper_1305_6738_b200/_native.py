@@ -13,6 +13,7 @@ from ._build import LIB
 ZKS_OK, ZKS_EINVAL, ZKS_ECUDA = 0, 1, 2
 STATUS_OK, STATUS_RETRIED, STATUS_FAILED = 0, 1, 2
 MLE_TABLE, MLE_DIRECT = 0, 1
+KERNEL_KINDS = ("stage", "draw", "fit", "retry", "batch", "single", "select", "other")  # ZKS_KERNEL_*
 ABI_VERSION = 2
 
 # every symbol include/zipfks_b200.h declares
@@ -24,6 +25,8 @@ EXPORTS = (
     "zks_engine_set_stream",
     "zks_engine_sync",
     "zks_engine_launches",
+    "zks_engine_set_timing",
+    "zks_engine_kernel_times",
     "zks_table_create",
     "zks_table_destroy",
     "zks_run_replicates",
@@ -96,6 +99,8 @@ def load() -> ctypes.CDLL:
     lib.zks_engine_set_stream.argtypes = [vp, vp]
     lib.zks_engine_sync.argtypes = [vp]
     lib.zks_engine_launches.argtypes = [vp, dp]
+    lib.zks_engine_set_timing.argtypes = [vp, ctypes.c_int]
+    lib.zks_engine_kernel_times.argtypes = [vp, dp, dp]
     lib.zks_table_create.argtypes = [vp, dp, i64, ctypes.POINTER(vp)]
     lib.zks_table_destroy.argtypes = [vp]
     lib.zks_table_destroy.restype = None

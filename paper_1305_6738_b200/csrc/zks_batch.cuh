@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  unsigned long long philox = 0, staged = 0, redrawn = 0;
+  unsigned long long philox = 0, staged = 0, redrawn = 0, rows = 0, tails = 0;
   for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.count; i += warps) {
     const uint64_t idx = a.first + i;
     uint16_t* tail = tail_out + i * a.vals_stride;
@@ -760,11 +760,15 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
       max_out[i] = o.mx;
       m_out[i] = o.m;
     }
+    ++rows;
+    tails += o.m;
   }
   if (kCount && lane == 0) {
     if (philox) atomicAdd(a.counters + 1, philox);
     if (staged) atomicAdd(a.counters + 8, staged);
     if (redrawn) atomicAdd(a.counters + kWorkFields + 1, redrawn);
+    if (rows) atomicAdd(a.counters + kWorkFields + 2, rows);
+    if (tails) atomicAdd(a.counters + kWorkFields + 3, tails);
   }
 }
 

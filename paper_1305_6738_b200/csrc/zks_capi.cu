@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
+#include <vector>
 #include <string>
 
 #include "../../include/zipfks_b200.h"
@@ -68,6 +70,10 @@ struct zks_engine {
   void* pre = nullptr;  // pre-drawn sample rows + their statistics (two-kernel path)
   size_t pre_bytes = 0;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
+  // per-kernel timing (zks_engine_set_timing): event pairs around launches on the engine stream
+  bool timing = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> timed;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 namespace {
@@ -87,6 +93,36 @@ uint32_t staged_cut(double h) {
   return static_cast<uint32_t>(std::min<uint64_t>(lo >> 21, 0xffffffffu));
 }
 
+// RAII timer of one launch: events on the engine stream before and after (timing mode only)
+struct Timed {
+  zks_engine* e;
+  int kind;
+  cudaEvent_t a = nullptr;
+  static cudaEvent_t take(zks_engine* e) {
+    cudaEvent_t ev = nullptr;
+    if (!e->event_pool.empty()) {
+      ev = e->event_pool.back();
+      e->event_pool.pop_back();
+    } else if (cudaEventCreate(&ev) != cudaSuccess) {
+      ev = nullptr;
+    }
+    return ev;
+  }
+  Timed(zks_engine* eng, int k) : e(eng), kind(k) {
+    if (e->timing && (a = take(e))) cudaEventRecord(a, e->stream);
+  }
+  ~Timed() {
+    if (!a) return;
+    cudaEvent_t b = take(e);
+    if (!b) {
+      e->event_pool.push_back(a);
+      return;
+    }
+    cudaEventRecord(b, e->stream);
+    e->timed.emplace_back(kind, a, b);
+  }
+};
+
 // every kernel launch goes through here: the error check and the engine's launch count
 cudaError_t launched(zks_engine* e) {
   ++e->launches;
@@ -103,8 +139,11 @@ int fit_table_for(zks_engine* e, int K, zks::FitTable** out) {
     T.coef = coef;
     const int threads = 128;
     const int blocks = (T.intervals * 32 + threads - 1) / threads;
-    zks::fit_table_kernel<<<blocks, threads, 0, e->stream>>>(T, coef, e->logs);
-    ZKS_CUDA(launched(e));
+    {
+      Timed tm(e, ZKS_KERNEL_OTHER);
+      zks::fit_table_kernel<<<blocks, threads, 0, e->stream>>>(T, coef, e->logs);
+      ZKS_CUDA(launched(e));
+    }
     it = e->fit_tables.emplace(K, T).first;
   }
   *out = &it->second;
@@ -171,6 +210,11 @@ void zks_engine_destroy(zks_engine* e) {
   if (e->pre) cudaFree(e->pre);
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
+  for (auto& t : e->timed) {
+    cudaEventDestroy(std::get<1>(t));
+    cudaEventDestroy(std::get<2>(t));
+  }
+  for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
   for (int i = 0; i < kStagingSlots; ++i)
     if (e->staging_done[i]) cudaEventDestroy(e->staging_done[i]);
   if (e->own) cudaStreamDestroy(e->own);
@@ -187,6 +231,34 @@ int zks_engine_sync(zks_engine* e) {
   if (!e) return fail(ZKS_EINVAL, "engine is NULL");
   ZKS_CUDA(cudaSetDevice(e->device));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_engine_set_timing(zks_engine* e, int on) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  e->timing = on != 0;
+  return ZKS_OK;
+}
+
+int zks_engine_kernel_times(zks_engine* e, double* ms_out, unsigned long long* launches_out) {
+  if (!e || !ms_out || !launches_out) return fail(ZKS_EINVAL, "NULL argument");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  for (int k = 0; k < ZKS_KERNEL_KINDS; ++k) {
+    ms_out[k] = 0.0;
+    launches_out[k] = 0;
+  }
+  cudaError_t err = cudaSuccess;
+  for (auto& t : e->timed) {
+    float ms = 0.0f;
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, std::get<1>(t), std::get<2>(t));
+    ms_out[std::get<0>(t)] += ms;
+    ++launches_out[std::get<0>(t)];
+    e->event_pool.push_back(std::get<1>(t));
+    e->event_pool.push_back(std::get<2>(t));
+  }
+  e->timed.clear();
+  ZKS_CUDA(err);
   return ZKS_OK;
 }
 
@@ -229,8 +301,11 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
     if (err == cudaSuccess) err = cudaEventRecord(e->staging_done[slot], e->stream);
   }
   if (err == cudaSuccess) {
-    zks::guide_kernel<<<(2 * zks::kGuideLevel + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
-    err = launched(e);
+    {
+      Timed tm(e, ZKS_KERNEL_OTHER);
+      zks::guide_kernel<<<(2 * zks::kGuideLevel + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
+      err = launched(e);
+    }
   }
   if (err != cudaSuccess) {
     zks_table_destroy(t);
@@ -274,9 +349,12 @@ int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64
   if (count == 0) return ZKS_OK;
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (int64_t)((count + 7) / 8)));
-  zks::stage_uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, repetition, first, count, n,
-                                                                     zks_staging_stride(n), u_dev, e->counters);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_STAGE);
+    zks::stage_uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, repetition, first, count, n,
+                                                                       zks_staging_stride(n), u_dev, e->counters);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -478,22 +556,34 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
       sub.pre_max = pmax;
       sub.pre_first = sub.first;
       const int64_t dblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)((cnt + 7) / 8)));
-      draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(sub, phead, ptail, pm, pls, pmin, pmax);
-      ZKS_CUDA(launched(e));
+      {
+        Timed tm(e, ZKS_KERNEL_DRAW);
+        draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(sub, phead, ptail, pm, pls, pmin, pmax);
+        ZKS_CUDA(launched(e));
+      }
       const int64_t fblocks =
           std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * fper, (int64_t)((cnt + 255) / 256)));
       ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
       ZKS_CUDA(cudaMemsetAsync(retry, 0, sizeof(uint32_t), e->stream));
-      fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub, retry);
-      ZKS_CUDA(launched(e));
-      again<<<(unsigned)e->sms, zks::kThreads, rsmem, e->stream>>>(sub, retry);
-      ZKS_CUDA(launched(e));
+      {
+        Timed tm(e, ZKS_KERNEL_FIT);
+        fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub, retry);
+        ZKS_CUDA(launched(e));
+      }
+      {
+        Timed tm(e, ZKS_KERNEL_RETRY);
+        again<<<(unsigned)e->sms, zks::kThreads, rsmem, e->stream>>>(sub, retry);
+        ZKS_CUDA(launched(e));
+      }
     }
     return ZKS_OK;
   }
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
-  kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, batched ? ZKS_KERNEL_BATCH : ZKS_KERNEL_SINGLE);
+    kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -514,13 +604,19 @@ int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t coun
     rl.rank[i] = static_cast<unsigned long long>(ranks_host[i]);
   }
   ZKS_CUDA(cudaSetDevice(e->device));
-  zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->sel, rl, nranks);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_SELECT);
+    zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->sel, rl, nranks);
+    ZKS_CUDA(launched(e));
+  }
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
   for (int shift = 56; shift >= 0; shift -= 8) {
-    zks::select_pass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(
-        reinterpret_cast<const unsigned long long*>(values_dev), count, shift, e->sel, nranks, out_dev);
-    ZKS_CUDA(launched(e));
+    {
+      Timed tm(e, ZKS_KERNEL_SELECT);
+      zks::select_pass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(
+          reinterpret_cast<const unsigned long long*>(values_dev), count, shift, e->sel, nranks, out_dev);
+      ZKS_CUDA(launched(e));
+    }
   }
   return ZKS_OK;
 }
@@ -546,8 +642,11 @@ int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_h
     return fail(ZKS_EINVAL, "unbounded support requires gamma >= 1.05, got %g", gamma);
   ZKS_CUDA(cudaSetDevice(e->device));
   if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
-  zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, e->sel_out);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, e->sel_out);
+    ZKS_CUDA(launched(e));
+  }
   ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
   return ZKS_OK;
@@ -571,8 +670,11 @@ int zks_fit_eval(zks_engine* e, int32_t support_k, const double* x_dev, int64_t 
   const int rc = fit_table_for(e, support_k, &T);
   if (rc) return rc;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
-  zks::fit_eval_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(*T, x_dev, count, mu_dev, m2_dev, norm_dev);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::fit_eval_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(*T, x_dev, count, mu_dev, m2_dev, norm_dev);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -595,8 +697,11 @@ int zks_stream_uniforms(zks_engine* e, uint64_t seed, uint64_t rep, uint64_t idx
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t nb = (count + 3) / 4;
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (nb + 255) / 256));
-  zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, count, out_dev);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, count, out_dev);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -606,8 +711,11 @@ int zks_draw(zks_engine* e, const zks_table* t, const double* u_dev, int64_t cou
   if (count == 0) return ZKS_OK;
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (count + 255) / 256));
-  zks::draw_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(t->cdf, t->guide, t->len, u_dev, count, out_dev);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::draw_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(t->cdf, t->guide, t->len, u_dev, count, out_dev);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -679,8 +787,11 @@ int zks_fit_samples(zks_engine* e, int32_t support_k, const int64_t* values_dev,
   ZKS_CUDA(cudaFuncSetAttribute(zks::samples_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (nsamples + zks::kWarps - 1) / zks::kWarps));
   ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
-  zks::samples_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::samples_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -690,8 +801,11 @@ int zks_series_eval(zks_engine* e, int32_t support_k, const double* gamma_dev, i
   if (count <= 0) return ZKS_OK;
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = (count * 32 + 255) / 256;
-  zks::series_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(gamma_dev, count, support_k, e->logs, out_dev);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::series_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(gamma_dev, count, support_k, e->logs, out_dev);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 
@@ -702,9 +816,12 @@ int zks_solve_exponents(zks_engine* e, int32_t support_k, const double* target_d
   if (count <= 0) return ZKS_OK;
   ZKS_CUDA(cudaSetDevice(e->device));
   const int64_t blocks = (count * 32 + 255) / 256;
-  zks::solve_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(target_dev, count, support_k, e->logs, mle_params(settings),
-                                                             bisect_only, gamma_dev, status_dev);
-  ZKS_CUDA(launched(e));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::solve_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(target_dev, count, support_k, e->logs, mle_params(settings),
+                                                               bisect_only, gamma_dev, status_dev);
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
 }
 

@@ -85,6 +85,18 @@ class Engine:
         _native.check(self.lib.zks_engine_launches(self.handle, ctypes.byref(out)))
         return out.value
 
+    def set_timing(self, on: bool) -> None:
+        """Bracket every kernel launch with CUDA events on the engine stream (diagnostics)."""
+        _native.check(self.lib.zks_engine_set_timing(self.handle, int(bool(on))))
+
+    def kernel_times(self) -> dict:
+        """{kind: (milliseconds, launches)} since the last call (synchronises; resets)."""
+        n = len(_native.KERNEL_KINDS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_ulonglong * n)()
+        _native.check(self.lib.zks_engine_kernel_times(self.handle, ms, cnt))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(_native.KERNEL_KINDS)}
+
     # -- tables --------------------------------------------------------------
     def table(self, gamma: float, support_k: int | None, cdf_builder) -> DrawTable:
         """Cached device table for the generating model (montecarlo.py:82-86 lru_cache)."""
