@@ -124,6 +124,12 @@ int zks_run_replicates_staged(zks_engine* engine, const zks_table* table, const 
 int zks_select_ranks(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,
                      int32_t nranks, double* out_host);
 
+/* Batched selection, asynchronous: for each a < narrays (<= 24), the order statistics of the
+ * counts[a] values at device values_dev[a] at ranks ranks_host[a * nranks + i] land in device
+ * out_dev[a][i], i < nranks (<= 16).  One launch for all arrays (the cells of a sweep row). */
+int zks_select_ranks_batch(zks_engine* engine, const double* const* values_dev, const int64_t* counts,
+                           int32_t narrays, const int64_t* ranks_host, int32_t nranks, double* const* out_dev);
+
 /* Same selection, asynchronous: the selected values land in out_dev[0..nranks) (device). */
 int zks_select_ranks_async(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,
                            int32_t nranks, double* out_dev);

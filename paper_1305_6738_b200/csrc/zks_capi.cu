@@ -39,6 +39,9 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
+#ifndef ZKS_SELECT_PER_SM
+#define ZKS_SELECT_PER_SM 2
+#endif
 constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
@@ -70,6 +73,7 @@ struct zks_engine {
   void* pre = nullptr;  // pre-drawn sample rows + their statistics (two-kernel path)
   size_t pre_bytes = 0;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
+  int select_blocks = 0;            // resident grid of the cooperative selection kernel
   // per-kernel timing (zks_engine_set_timing): event pairs around launches on the engine stream
   bool timing = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> timed;
@@ -591,34 +595,54 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
 
 extern "C" {
 
-int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
-                           int32_t nranks, double* out_dev) {
-  if (!e || !values_dev || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
-  if (count < 1) return fail(ZKS_EINVAL, "cannot take quantiles of an empty array");
+int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
+                           const int64_t* ranks_host, int32_t nranks, double* const* out_dev) {
+  if (!e || !values_dev || !counts || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (narrays < 1 || narrays > zks::kSelMaxArrays)
+    return fail(ZKS_EINVAL, "narrays %d outside [1, %d]", narrays, zks::kSelMaxArrays);
   if (nranks < 1 || nranks > zks::kMaxRanks) return fail(ZKS_EINVAL, "nranks %d outside [1, %d]", nranks, zks::kMaxRanks);
-  zks::RankList rl;
-  std::memset(&rl, 0, sizeof rl);
-  for (int i = 0; i < nranks; ++i) {
-    if (ranks_host[i] < 0 || ranks_host[i] >= count)
-      return fail(ZKS_EINVAL, "rank %lld out of range for %lld values", (long long)ranks_host[i], (long long)count);
-    rl.rank[i] = static_cast<unsigned long long>(ranks_host[i]);
-  }
-  ZKS_CUDA(cudaSetDevice(e->device));
-  {
-    Timed tm(e, ZKS_KERNEL_SELECT);
-    zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->sel, rl, nranks);
-    ZKS_CUDA(launched(e));
-  }
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    {
-      Timed tm(e, ZKS_KERNEL_SELECT);
-      zks::select_pass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(
-          reinterpret_cast<const unsigned long long*>(values_dev), count, shift, e->sel, nranks, out_dev);
-      ZKS_CUDA(launched(e));
+  zks::SelectBatch B;
+  std::memset(&B, 0, sizeof B);
+  B.narrays = narrays;
+  B.nr = nranks;
+  int64_t most = 0;
+  for (int a = 0; a < narrays; ++a) {
+    if (!values_dev[a] || !out_dev[a]) return fail(ZKS_EINVAL, "NULL array %d", a);
+    if (counts[a] < 1) return fail(ZKS_EINVAL, "cannot take quantiles of an empty array");
+    B.keys[a] = reinterpret_cast<const unsigned long long*>(values_dev[a]);
+    B.count[a] = counts[a];
+    B.out[a] = out_dev[a];
+    most = std::max(most, counts[a]);
+    for (int i = 0; i < nranks; ++i) {
+      const int64_t r = ranks_host[int64_t(a) * nranks + i];
+      if (r < 0 || r >= counts[a])
+        return fail(ZKS_EINVAL, "rank %lld out of range for %lld values", (long long)r, (long long)counts[a]);
+      B.rank[a][i] = static_cast<unsigned long long>(r);
     }
   }
+  ZKS_CUDA(cudaSetDevice(e->device));
+  // one cooperative launch: every block resident (grid barriers between the radix passes)
+  if (e->select_blocks == 0) {
+    int per = 0;
+    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zks::select_kernel, 256, 0));
+    e->select_blocks = std::max(1, std::min(per, ZKS_SELECT_PER_SM)) * e->sms;
+  }
+  const int blocks = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(e->select_blocks, (most * narrays + 255) / 256)));
+  {
+    Timed tm(e, ZKS_KERNEL_SELECT);
+    zks::SelectState* st = e->sel;
+    void* args[] = {&B, &st};
+    ZKS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(zks::select_kernel), dim3(blocks), dim3(256),
+                                         args, 0, e->stream));
+    ZKS_CUDA(launched(e));
+  }
   return ZKS_OK;
+}
+
+int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
+                           int32_t nranks, double* out_dev) {
+  return zks_select_ranks_batch(e, &values_dev, &count, 1, ranks_host, nranks, &out_dev);
 }
 
 int zks_select_ranks(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,

@@ -277,14 +277,16 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
-    equal n draw from identical uniforms: they are generated once per chunk of replicate
-    indices (zks_stage_uniforms) and every cell's replicate kernel reads them.  Results are
-    identical to running the cells one by one.
+    equal n draw from identical uniforms: for 128 <= n <= 1024 they are generated once per chunk
+    of replicate indices (zks_stage_uniforms) and every cell's replicate kernels read them.  The
+    cells' order statistics are selected in batched launches.  Results are identical to running
+    the cells one by one.
     """
     torch = _torch()
     cfg0 = plans[0].config
     n = cfg0.n
-    if len(plans) < 2 or not _STAGE_MIN_N <= n <= _STAGE_MAX_N:
+    staged = _STAGE_MIN_N <= n <= _STAGE_MAX_N
+    if len(plans) < 2 or (gather is not None and not staged):
         for plan in plans:
             _enqueue_cell(eng, plan, shard=shard, gather=gather, kernel_events=kernel_events)
         return
@@ -296,7 +298,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     chunk = max(1, min(stop - first, _STAGE_BYTES // (4 * stride)))
     key = ("stage", eng.device)
     ubuf = _SLABS.get(key)
-    if ubuf is None or ubuf.numel() < chunk * stride:
+    if staged and (ubuf is None or ubuf.numel() < chunk * stride):
         ubuf = torch.empty(chunk * stride, dtype=torch.int32, device=dev)  # 32-bit staged words
         _SLABS[key] = ubuf
     outs = []
@@ -310,7 +312,13 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
         outs.append(_Slab(eng, max(total, 1)))
     tables = [_table(eng, p.config) for p in plans]
     for rep in range(cfg0.repetitions):
-        for c0 in range(first, stop, chunk):
+        if not staged:  # independent streams per cell; only the selection is batched
+            for plan, table, out in zip(plans, tables, outs):
+                cfg = plan.config
+                if stop > first:
+                    eng.run_replicates(table, cfg.support.k, cfg.gamma, n, cfg.base_seed, rep, first, stop - first,
+                                       out.ks[first:], out.gh[first:], out.st[first:])
+        for c0 in range(first, stop, chunk) if staged else ():
             cnt = min(chunk, stop - c0)
             eng.stage_uniforms(cfg0.base_seed, rep, c0, cnt, n, ubuf)
             for plan, table, out in zip(plans, tables, outs):
@@ -323,12 +331,19 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
                 if kernel_events is not None:
                     k1.record(stream)
                     kernel_events.append((k0, k1))
+        jobs = []
         for plan, out in zip(plans, outs):
             if stop > first:
                 plan.worst[rep] = out.st[first:stop].max()
-            ks = out.ks[:total] if gather is None else gather(out.ks)[:total]
+            if gather is None:  # the row's cells in batched launches
+                jobs.extend((out.ks[:total], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
+                            for i in range(0, len(ranks), 16))
+                continue
+            ks = gather(out.ks)[:total]  # the gather buffer is reused: select before the next cell
             for i in range(0, len(ranks), 16):
                 eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+        for i0 in range(0, len(ranks), 16):  # equal rank counts per launch
+            eng.select_many([j for j in jobs if j[1] == ranks[i0 : i0 + 16]])
     for plan in plans:
         plan.finished.record(stream)
 
