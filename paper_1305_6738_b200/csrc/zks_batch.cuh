@@ -537,7 +537,10 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // largest u and accepted when the cdf entry below lies under its smallest u.  A replicate with
 // an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
-constexpr int kDrawWarpBytes = (kKsHead + 1) * 32 + kDrawQueue * 8;  // u8 bins [v][lane] + queue
+constexpr int kPreMaxN = 16384;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
+constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
+// per-warp smem of draw_stats_kernel: bins [v][lane] (u8, or u16 above kNarrowBinsMaxN) + queue
+__host__ __device__ constexpr int draw_warp_bytes(bool wide) { return (kKsHead + 1) * 32 * (wide ? 2 : 1) + kDrawQueue * 8; }
 
 // g += (t < T), as one compare and one predicated add
 __device__ __forceinline__ void inc_if_lt(uint32_t& g, uint32_t t, uint32_t T) {
@@ -560,9 +563,9 @@ struct DrawRowOut {
 
 // One replicate row (warp-cooperative).  kStaged: 32-bit staged words (returns false when some
 // word was undecided: the caller redraws the row with kStaged = false).
-template <bool kStaged>
+template <bool kStaged, typename BinT>
 __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, const uint32_t* __restrict__ urow,
-                                         const uint16_t* __restrict__ guide, uint8_t* bins, void* qmem,
+                                         const uint16_t* __restrict__ guide, BinT* bins, void* qmem,
                                          uint16_t* tail, uint16_t* head, DrawRowOut& o, int lane) {
   using Q = typename std::conditional<kStaged, uint32_t, double>::type;
   Q* queue = reinterpret_cast<Q*>(qmem);
@@ -686,27 +689,35 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   __syncwarp();
   // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
   uint32_t hc0 = 0, hc1 = 0;
-  const uint8_t* r0 = bins + (lane + 1) * 32;
-  const uint8_t* r1 = bins + (lane + 33) * 32;
+  const uint32_t* r0 = reinterpret_cast<const uint32_t*>(bins + (lane + 1) * 32);
+  const uint32_t* r1 = reinterpret_cast<const uint32_t*>(bins + (lane + 33) * 32);
+  constexpr int kWords = 32 * sizeof(BinT) / 4;  // words per bin row
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int jj = (j + lane) & 7;  // rotate the word so the warp's loads spread over banks
-    const uint32_t w0 = reinterpret_cast<const uint32_t*>(r0)[jj];
-    const uint32_t w1 = reinterpret_cast<const uint32_t*>(r1)[jj];
-    hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
-    hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
+  for (int j = 0; j < kWords; ++j) {
+    const int jj = (j + lane) & (kWords - 1);  // rotate the word so the warp's loads spread over banks
+    const uint32_t w0 = r0[jj], w1 = r1[jj];
+    if (sizeof(BinT) == 1) {
+      hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
+      hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
+    } else {
+      hc0 += (w0 & 0xffffu) + (w0 >> 16);
+      hc1 += (w1 & 0xffffu) + (w1 >> 16);
+    }
   }
-  hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
-  hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
+  if (sizeof(BinT) == 1) {
+    hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
+    hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
+  }
   __syncwarp();
   if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;
   if (lane == 1) hc0 = G0 - G1;
   if (lane == 2) hc0 = G1 - G2;
   if (lane == 3) hc0 = G2 - G3;
-  for (int i = lane; i < (kKsHead - 4) * 8; i += 32) reinterpret_cast<uint32_t*>(bins + 5 * 32)[i] = 0u;
+  for (int i = lane; i < (kKsHead - 4) * 8 * static_cast<int>(sizeof(BinT)); i += 32)
+    reinterpret_cast<uint32_t*>(bins + 5 * 32)[i] = 0u;
   const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
   if (!undecided) {
-    head[lane] = static_cast<uint16_t>(hc0);  // n <= 1024: u16 counts
+    head[lane] = static_cast<uint16_t>(hc0);  // n <= kPreMaxN: u16 counts
     head[lane + 32] = static_cast<uint16_t>(hc1);
   }
   mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
@@ -720,7 +731,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   return !undecided;
 }
 
-template <bool kCount>
+template <bool kCount, bool kWide>
 __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(ReplicateArgs a, uint16_t* head_out,
                                                                  uint16_t* tail_out, uint32_t* m_out, double* ls_out,
                                                                  uint32_t* min_out, uint32_t* max_out) {
@@ -728,11 +739,12 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem + guide_bytes + warp * kDrawWarpBytes;
-  // lane-private u8 counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
-  // most one queued draw per pop and there are <= n/32 + 1 <= 33 pops, so u8 cannot overflow
-  uint8_t* bins = wbase;
-  void* queue = wbase + (kKsHead + 1) * 32;
+  using BinT = typename std::conditional<kWide, uint16_t, uint8_t>::type;
+  unsigned char* wbase = smem + guide_bytes + warp * draw_warp_bytes(kWide);
+  // lane-private counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
+  // most one queued draw per pop and there are <= n/32 + 1 pops (u8 up to kNarrowBinsMaxN)
+  BinT* bins = reinterpret_cast<BinT*>(wbase);
+  void* queue = wbase + (kKsHead + 1) * 32 * sizeof(BinT);
   load_guide(guide, a.guide, a.guide_levels);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();

@@ -433,17 +433,19 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
 
   const bool counting = e->counters != nullptr;
   const bool batched = a.use_table && c->n <= kBatchMaxN;
+  const bool two_kernel = a.use_table && c->n >= zks::kLaneDrawMaxN && c->n <= zks::kPreMaxN;
   a.guide_levels = L > 4096u ? 2 : 1;
   const size_t guide_bytes = zks::round_up(a.guide_levels * zks::kGuideLevel * 2, 16);
   void (*kernel)(zks::ReplicateArgs);
   size_t smem;
   int64_t per_block;  // replicates one block takes per work item round
-  if (batched) {
+  if (batched || two_kernel) {
     // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
+    // (the histogram of the batch kernel, and of retry_kernel on the two-kernel path)
     a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
     a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
-    a.batch = std::min(32, zks::kBatchVals / a.vals_stride);
+    a.batch = std::max(1, std::min(32, zks::kBatchVals / a.vals_stride));
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
     smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + 3 * zks::kKsQueue * 4 + zks::kBatchVals * 2);
     per_block = int64_t(zks::kWarps) * a.batch;
@@ -499,7 +501,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.pre_min = nullptr;
   a.pre_max = nullptr;
   a.pre_first = 0;
-  if (batched && c->n >= zks::kLaneDrawMaxN) {
+  if (two_kernel) {
     // draw phase in its own high-occupancy kernel (head counts + tail values per replicate),
     // then fit + score, then the listed retries; chunk by chunk.  Per row: u16 head counts
     // (128 B), log-sum, min / max / m, the tail values, a retry-list slot.
@@ -520,12 +522,18 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     uint32_t* pm = pmax + chunk;
     uint16_t* ptail = reinterpret_cast<uint16_t*>(pm + chunk);
     uint32_t* retry = reinterpret_cast<uint32_t*>(ptail + chunk * a.vals_stride);  // vals_stride % 4 == 0
-    auto draw = counting ? zks::draw_stats_kernel<true> : zks::draw_stats_kernel<false>;
+    const bool wide = c->n > zks::kNarrowBinsMaxN;
+    auto draw = counting ? (wide ? zks::draw_stats_kernel<true, true> : zks::draw_stats_kernel<true, false>)
+                         : (wide ? zks::draw_stats_kernel<false, true> : zks::draw_stats_kernel<false, false>);
+    // the retry kernel's per-warp sample store grows with n: fewer warps per block for large n
+    const int rwarps = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(zks::kWarps, (size_t(227) * 1024 - guide_bytes) /
+                                             size_t(zks::retry_warp_bytes(a.hist_words, a.vals_stride)))));
     auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
     auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
-    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::kDrawWarpBytes;
+    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::draw_warp_bytes(wide);
     const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
-    const size_t rsmem = guide_bytes + size_t(zks::kWarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
+    const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
     int dper = 0, fper = 0;
     {
       int optin = 0;
@@ -576,7 +584,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
       }
       {
         Timed tm(e, ZKS_KERNEL_RETRY);
-        again<<<(unsigned)e->sms, zks::kThreads, rsmem, e->stream>>>(sub, retry);
+        again<<<(unsigned)e->sms, 32 * rwarps, rsmem, e->stream>>>(sub, retry);
         ZKS_CUDA(launched(e));
       }
     }

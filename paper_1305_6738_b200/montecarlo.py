@@ -265,7 +265,7 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
     plan.finished.record(stream)
 
 
-_STAGE_MIN_N, _STAGE_MAX_N = 128, 1024  # n range where the batch kernel reads staged uniforms
+_STAGE_MIN_N, _STAGE_MAX_N = 128, 16384  # n range of the two-kernel path (draw kernel reads staged words)
 _STAGE_BYTES = 2 << 30                   # staging buffer budget
 
 
@@ -277,7 +277,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
-    equal n draw from identical uniforms: for 128 <= n <= 1024 they are generated once per chunk
+    equal n draw from identical uniforms: for 128 <= n <= 16384 they are generated once per chunk
     of replicate indices (zks_stage_uniforms) and every cell's replicate kernels read them.  The
     cells' order statistics are selected in batched launches.  Results are identical to running
     the cells one by one.

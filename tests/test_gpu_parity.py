@@ -138,6 +138,8 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (5000, 1.0, 300, 6, 0, 100),
         (20, 0.25, 10, 1, 0, 600),
         (50, 4.0, 40, 12, 0, 600),
+        (None, 1.6, 9000, 3, 0, 24),  # two-kernel path with u16 draw bins
+        (1000, 1.0, 5000, 2, 0, 24),
     ],
 )
 def test_replicates_match_oracle(zk, mle_mode, K, gamma, n, seed, rep, count):
