@@ -159,11 +159,13 @@ __device__ __forceinline__ bool ks_lane_walk(const ReplicateArgs& a, bool on, do
   bool done = false;
   for (uint32_t k = 1; __any_sync(0xffffffffu, live && k <= end); ++k) {
     if (live && k <= end) {
-      S += exp(-g * __ldg(a.logs + k));
+      S += exp_bounded(-g * __ldg(a.logs + k));
       C += count(k);
       const double F = S * inv, E = static_cast<double>(C) * a.inv_n;
-      D = fmax(D, fabs(F - E));
-      if (D > fmax(1.0 - E, 1.0 - F) + kKsMargin) {
+      const double gap = fabs(F - E);
+      D = gap > D ? gap : D;
+      // D > max(1 - E, 1 - F) + margin, without fmax's NaN handling (all finite here)
+      if (D > (1.0 - E) + kKsMargin && D > (1.0 - F) + kKsMargin) {
         done = true;
         live = false;
       }

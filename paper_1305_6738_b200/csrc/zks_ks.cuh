@@ -116,7 +116,7 @@ __device__ __forceinline__ double em_block(const KsCtx& c, uint64_t v, double& f
   const double Lv = ln_of(c.logs, v);
   const double b = static_cast<double>(v);
   const double ib = 1.0 / b;
-  fv = exp(-c.g * Lv);
+  fv = exp_bounded(-c.g * Lv);
   // integral_a^v x^-g dx = (v^(1-g) - a^(1-g)) / (1-g); near g = 1 that difference cancels, so
   // there it is a^(1-g) * expm1((1-g) ln(v/a)) / (1-g), continuous through g = 1
   double integral;
@@ -283,7 +283,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     const bool in = k <= head_end;
     const uint32_t cnt = in ? hist[k] : 0u;
     const uint32_t C = s.Cb + warp_scan_u32(cnt, lane);
-    const double term = in ? exp(-g * __ldg(p.logs + k)) : 0.0;
+    const double term = in ? exp_bounded(-g * __ldg(p.logs + k)) : 0.0;
     const double S = s.S + warp_scan(term, lane);
     double F;
     if (c.exact) {
@@ -303,7 +303,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     s.S_head = s.S;
     s.Dw = p.from_head ? p.D0 : warp_max(s.D);  // from_head: D0 is the warp's value
     c.La = __ldg(p.logs + kKsHead + 1);
-    c.fa = exp(-g * c.La);
+    c.fa = exp_bounded(-g * c.La);
     constexpr double a = static_cast<double>(kKsHead + 1);
     c.a_pow = a * c.fa;
     const double om = 1.0 - g;
