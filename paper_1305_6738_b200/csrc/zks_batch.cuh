@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
 
 constexpr int kHeadRowWords = kKsHead / 2 + 1;        // u16 counts of 1..kKsHead + pad: conflict-free columns
 constexpr int kFitHistWords = 32 * kHeadRowWords;      // the head rows, reused as page histogram
-constexpr int kFitWarpWords = kFitHistWords + kKsQueueWords;
+constexpr int kFitStageWords = kOverCap / 2;             // one tail of <= kOverCap u16 values
+constexpr int kFitWarpWords = kFitHistWords + kKsQueueWords + kFitStageWords;
 
 // Fit + score of pre-drawn replicates (draw_stats_kernel): a warp takes 32 consecutive rows,
 // fits them lane-parallel, walks each head k <= kKsHead lane by lane from the counts, and
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
   uint32_t* heads = reinterpret_cast<uint32_t*>(smem) + warp * kFitWarpWords;
   uint32_t* hist = heads;  // page histogram once the lane walks are done
   uint32_t* queue = heads + kFitHistWords;
+  uint16_t* stage = reinterpret_cast<uint16_t*>(queue + kKsQueueWords);  // the tail being scored
   const int K = a.K;
   const double dn = static_cast<double>(a.n);
   const uint64_t nbatches = (a.count + 31) / 32;
@@ -398,7 +400,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     uint32_t vmax = 0;
     bool ok = false;
     Work lw{};
+    uint32_t my_m = 0;
     if (active) {
+      my_m = a.pre_m[row];
       vmax = a.pre_max[row];
       const double target = fit_target(a.pre_ls[row], a.pre_min[row], K, dn);
       ok = fit_exponent(M, target, lane, g, lw);
@@ -422,16 +426,43 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     const bool scored = ks_lane_walk(a, ok && active, g, norm, vmax,
                                      [&](uint32_t k) { return (hr[(k - 1) >> 1] >> (((k - 1) & 1) * 16)) & 0xffffu; },
                                      my_ks, hS, hC, hD);
-    // long tails, warp-cooperatively (the head rows are free now: pages reuse them)
-    for (unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored); need; need &= need - 1) {
-      const int r = __ffs(need) - 1;
+    // long tails, warp-cooperatively (the head rows are free now: pages reuse them).  The tail
+    // values of the next replicate are loaded into registers while the current one is scored,
+    // then staged in shared memory (tails of <= kOverCap values; longer ones read from HBM/L2).
+    unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored);
+    uint32_t pv[kOverCap / 32], pm = 0;
+    auto issue = [&](int r) {
+      pm = __shfl_sync(0xffffffffu, my_m, r);
+      const uint16_t* t = a.pre_tail + (a.first + r0 + r - a.pre_first) * a.vals_stride;
+#pragma unroll
+      for (int j = 0; j < kOverCap / 32; ++j) {
+        const uint32_t i = j * 32 + lane;
+        pv[j] = (pm <= kOverCap && i < pm) ? t[i] : 0u;
+      }
+    };
+    int r = need ? __ffs(need) - 1 : -1;
+    if (r >= 0) issue(r);
+    while (r >= 0) {
+      __syncwarp();  // the previous scan is done with the stage
+      const uint32_t m = pm;
+      if (m <= kOverCap) {
+#pragma unroll
+        for (int j = 0; j < kOverCap / 32; ++j)
+          if (j * 32 + lane < m) stage[j * 32 + lane] = static_cast<uint16_t>(pv[j]);
+      }
+      __syncwarp();
+      need &= need - 1;
+      const int nx = need ? __ffs(need) - 1 : -1;
+      if (nx >= 0) issue(nx);
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, vmax, r);
-      const uint64_t rr = a.first + r0 + r - a.pre_first;
-      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, kFitHistWords, kFitHistWords, queue,
-                                         a.pre_tail + rr * a.vals_stride, a.pre_m[rr], lane, wk);
+      const uint16_t* over =
+          m <= kOverCap ? stage : a.pre_tail + (a.first + r0 + r - a.pre_first) * a.vals_stride;
+      const KsOut ko =
+          ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, kFitHistWords, kFitHistWords, queue, over, m, lane, wk);
       if (lane == r) my_ks = ko.D;
+      r = nx;
     }
     __syncwarp();
 
