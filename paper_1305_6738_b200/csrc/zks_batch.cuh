@@ -239,6 +239,12 @@ __device__ __forceinline__ uint8_t retry_replicate(const ReplicateArgs& a, const
   return ok2 ? 1 : 2;
 }
 
+// per-warp shared memory of replicate_batch_kernel: histogram, queue, 32 samples (16-byte
+// aligned); sized to n so that small n leaves L1 room for the fit tables
+__host__ __device__ constexpr int batch_warp_bytes(int hist_words, int vals_stride) {
+  return round_up(hist_words * 4 + kKsQueueWords * 4 + 32 * vals_stride * 2, 16);
+}
+
 // Small samples (n < kLaneDrawMaxN): a warp takes B = 32 consecutive replicate indices;
 // each lane draws, fits and scores the head of its own replicate; tails that outlive the head
 // are scored warp-cooperatively from the lane's head state.
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int warp_bytes = a.hist_words * 4 + 3 * kKsQueue * 4 + kBatchVals * 2;
+  const int warp_bytes = batch_warp_bytes(a.hist_words, a.vals_stride);
   unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;
@@ -730,16 +736,12 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     const int jj = (j + lane) & (kWords - 1);  // rotate the word so the warp's loads spread over banks
     const uint32_t w0 = r0[jj], w1 = r1[jj];
     if (sizeof(BinT) == 1) {
-      hc0 += (w0 & 0x00ff00ffu) + ((w0 >> 8) & 0x00ff00ffu);  // two 16-bit lanes of byte pairs
-      hc1 += (w1 & 0x00ff00ffu) + ((w1 >> 8) & 0x00ff00ffu);
+      hc0 = __dp4a(w0, 0x01010101u, hc0);  // sum of the word's 4 bytes
+      hc1 = __dp4a(w1, 0x01010101u, hc1);
     } else {
       hc0 += (w0 & 0xffffu) + (w0 >> 16);
       hc1 += (w1 & 0xffffu) + (w1 >> 16);
     }
-  }
-  if (sizeof(BinT) == 1) {
-    hc0 = (hc0 & 0xffffu) + (hc0 >> 16);
-    hc1 = (hc1 & 0xffffu) + (hc1 >> 16);
   }
   __syncwarp();
   if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;

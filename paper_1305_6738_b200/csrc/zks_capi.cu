@@ -447,7 +447,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
     a.batch = std::max(1, std::min(32, zks::kBatchVals / a.vals_stride));
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words * 4 + 3 * zks::kKsQueue * 4 + zks::kBatchVals * 2);
+    smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride);
     per_block = int64_t(zks::kWarps) * a.batch;
   } else {
     a.batch = 1;
@@ -457,7 +457,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     per_block = zks::kWarps;
   }
   int per_sm = 0;
-  {
+  if (!two_kernel) {
     const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), smem);
     auto it = e->occupancy.find(key);
     if (it == e->occupancy.end()) {
@@ -472,7 +472,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     }
     per_sm = it->second;
   }
-  int64_t blocks = int64_t(e->sms) * per_sm;
+  int64_t blocks = int64_t(e->sms) * std::max(per_sm, 1);
   blocks = std::min<int64_t>(blocks, (int64_t)((c->count + per_block - 1) / per_block));
   a.slab = nullptr;
   a.slab_cap = 0;
