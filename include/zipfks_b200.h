@@ -126,9 +126,12 @@ int zks_select_ranks(zks_engine* engine, const double* values_dev, int64_t count
 
 /* Batched selection, asynchronous: for each a < narrays (<= 24), the order statistics of the
  * counts[a] values at device values_dev[a] at ranks ranks_host[a * nranks + i] land in device
- * out_dev[a][i], i < nranks (<= 16).  One launch for all arrays (the cells of a sweep row). */
+ * out_dev[a][i], i < nranks (<= 16).  Optionally (status_dev non-NULL, entry non-NULL) the
+ * maximum of the counts[a] status bytes at status_dev[a] lands in *worst_dev[a].  One launch
+ * for all arrays (the cells of a sweep row). */
 int zks_select_ranks_batch(zks_engine* engine, const double* const* values_dev, const int64_t* counts,
-                           int32_t narrays, const int64_t* ranks_host, int32_t nranks, double* const* out_dev);
+                           int32_t narrays, const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
+                           const uint8_t* const* status_dev, uint8_t* const* worst_dev);
 
 /* Same selection, asynchronous: the selected values land in out_dev[0..nranks) (device). */
 int zks_select_ranks_async(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,

@@ -112,7 +112,7 @@ def load() -> ctypes.CDLL:
     lib.zks_run_replicates_staged.argtypes = [vp, vp, ctypes.POINTER(ZksCell), dp, u64, u64, dp, dp, dp]
     lib.zks_select_ranks.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_async.argtypes = [vp, dp, i64, dp, i32, dp]
-    lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp]
+    lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp, dp, dp]
     lib.zks_normaliser.argtypes = [vp, ctypes.c_double, i32, dp]
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]

@@ -604,7 +604,8 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
 extern "C" {
 
 int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
-                           const int64_t* ranks_host, int32_t nranks, double* const* out_dev) {
+                           const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
+                           const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
   if (!e || !values_dev || !counts || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
   if (narrays < 1 || narrays > zks::kSelMaxArrays)
     return fail(ZKS_EINVAL, "narrays %d outside [1, %d]", narrays, zks::kSelMaxArrays);
@@ -620,6 +621,8 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
     B.keys[a] = reinterpret_cast<const unsigned long long*>(values_dev[a]);
     B.count[a] = counts[a];
     B.out[a] = out_dev[a];
+    B.status[a] = status_dev ? status_dev[a] : nullptr;
+    B.worst[a] = (status_dev && status_dev[a] && worst_dev) ? worst_dev[a] : nullptr;
     most = std::max(most, counts[a]);
     for (int i = 0; i < nranks; ++i) {
       const int64_t r = ranks_host[int64_t(a) * nranks + i];
@@ -650,7 +653,7 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
 
 int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
                            int32_t nranks, double* out_dev) {
-  return zks_select_ranks_batch(e, &values_dev, &count, 1, ranks_host, nranks, &out_dev);
+  return zks_select_ranks_batch(e, &values_dev, &count, 1, ranks_host, nranks, &out_dev, nullptr, nullptr);
 }
 
 int zks_select_ranks(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,

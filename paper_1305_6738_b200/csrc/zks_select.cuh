@@ -26,6 +26,7 @@ struct SelectState {
   unsigned int hist[kSelectPasses][kSelSlots][256];  // used slots zeroed at the start of a launch
   unsigned long long pre[kSelSlots], want[kSelSlots];
   int rep[kSelSlots];  // first rank of the same array with the same prefix (counted once)
+  unsigned int worst[kSelMaxArrays];  // max status byte per array (optional)
 };
 
 // kernel parameters (< 4 KB): the arrays, their lengths, ranks and output pointers
@@ -34,6 +35,8 @@ struct SelectBatch {
   long long count[kSelMaxArrays];
   double* out[kSelMaxArrays];
   unsigned long long rank[kSelMaxArrays][kMaxRanks];
+  const unsigned char* status[kSelMaxArrays];  // optional: replicate status bytes (count[a] of them)
+  unsigned char* worst[kSelMaxArrays];         // ... whose maximum lands here
   int narrays, nr;
 };
 
@@ -45,6 +48,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
   __shared__ int srep[kMaxRanks];
   const int nr = B.nr, slots = B.narrays * nr;
   const int lane = threadIdx.x & 31;
+  static_assert(sizeof(SelectBatch) <= 4096, "kernel parameters");
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = tid; i < int64_t(kSelectPasses) * slots * 256; i += stride)
@@ -53,7 +57,16 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
     st->pre[s] = 0ull;
     st->want[s] = B.rank[s / nr][s % nr];
   }
+  if (tid < B.narrays) st->worst[tid] = 0u;
   grid.sync();
+  // worst status per array (montecarlo.py:106-115 failures surface as SimulationError on the host)
+  for (int a = 0; a < B.narrays; ++a) {
+    if (!B.status[a]) continue;
+    unsigned w = 0;
+    for (int64_t i = tid; i < B.count[a]; i += stride) w = max(w, static_cast<unsigned>(B.status[a][i]));
+    w = __reduce_max_sync(0xffffffffu, w);
+    if (lane == 0 && w) atomicMax(&st->worst[a], w);
+  }
   const int gwarp = static_cast<int>(tid >> 5), nwarps = static_cast<int>(stride >> 5);
   for (int pass = 0; pass < kSelectPasses; ++pass) {
     const int shift = 56 - 8 * pass;
@@ -146,6 +159,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
   }
   for (int64_t s = tid; s < slots; s += stride)
     B.out[s / nr][s % nr] = __longlong_as_double(static_cast<long long>(__ldcg(&st->pre[s])));
+  if (tid < B.narrays && B.worst[tid]) *B.worst[tid] = static_cast<unsigned char>(__ldcg(&st->worst[tid]));
 }
 
 }  // namespace zks

@@ -175,22 +175,28 @@ class Engine:
         return [float(x) for x in res]
 
     def select_many(self, jobs) -> None:
-        """Asynchronous batched selection: ``jobs`` = [(values, ranks, out)] with device float64
-        ``values`` and ``out`` tensors and the same number (<= 16) of ranks each; one launch per
-        24 arrays."""
+        """Asynchronous batched selection: ``jobs`` = [(values, ranks, out[, status, worst])] with
+        device float64 ``values`` / ``out`` tensors and the same number (<= 16) of ranks each;
+        with a device uint8 ``status`` tensor (as long as ``values``), its maximum lands in the
+        one-element ``worst`` tensor.  One launch per 24 arrays."""
         jobs = list(jobs)
         for j0 in range(0, len(jobs), 24):
             part = jobs[j0 : j0 + 24]
             nr = len(part[0][1])
-            ptrs = (ctypes.c_void_p * len(part))(*[v.data_ptr() for v, _, _ in part])
-            outs = (ctypes.c_void_p * len(part))(*[o.data_ptr() for _, _, o in part])
-            counts = np.ascontiguousarray([v.numel() for v, _, _ in part], dtype=np.int64)
-            ranks = np.ascontiguousarray([list(r) for _, r, _ in part], dtype=np.int64)
+            ptrs = (ctypes.c_void_p * len(part))(*[j[0].data_ptr() for j in part])
+            outs = (ctypes.c_void_p * len(part))(*[j[2].data_ptr() for j in part])
+            sts = (ctypes.c_void_p * len(part))(*[j[3].data_ptr() if len(j) > 3 else None for j in part])
+            worst = (ctypes.c_void_p * len(part))(*[j[4].data_ptr() if len(j) > 3 else None for j in part])
+            counts = np.ascontiguousarray([j[0].numel() for j in part], dtype=np.int64)
+            ranks = np.ascontiguousarray([list(j[1]) for j in part], dtype=np.int64)
             if ranks.shape[1] != nr:
                 raise ValueError("select_many: every job needs the same number of ranks")
+            for j in part:
+                if len(j) > 3 and j[3].numel() != j[0].numel():
+                    raise ValueError("select_many: status and values differ in length")
             self.bind_stream()
             _native.check(self.lib.zks_select_ranks_batch(self.handle, ptrs, counts.ctypes.data, len(part),
-                                                          ranks.ctypes.data, nr, outs))
+                                                          ranks.ctypes.data, nr, outs, sts, worst))
 
     def normaliser(self, gamma: float, support_k: int | None) -> float:
         out = ctypes.c_double()

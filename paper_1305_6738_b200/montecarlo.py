@@ -303,9 +303,12 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
         _SLABS[key] = ubuf
     outs = []
     stream = eng.bind_stream()
-    for plan in plans:
-        plan.quantiles = torch.empty((cfg0.repetitions, len(ranks)), dtype=torch.float64, device=dev)
-        plan.worst = torch.zeros(cfg0.repetitions, dtype=torch.uint8, device=dev)
+    # one allocation (and one fill) for the whole row's quantiles and worst statuses
+    quantiles = torch.empty((len(plans), cfg0.repetitions, len(ranks)), dtype=torch.float64, device=dev)
+    worst = torch.zeros((len(plans), cfg0.repetitions), dtype=torch.uint8, device=dev)
+    for i, plan in enumerate(plans):
+        plan.quantiles = quantiles[i]
+        plan.worst = worst[i]
         plan.started = torch.cuda.Event(enable_timing=True)
         plan.finished = torch.cuda.Event(enable_timing=True)
         plan.started.record(stream)
@@ -333,12 +336,13 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
                     kernel_events.append((k0, k1))
         jobs = []
         for plan, out in zip(plans, outs):
-            if stop > first:
-                plan.worst[rep] = out.st[first:stop].max()
-            if gather is None:  # the row's cells in batched launches
+            if gather is None:  # the row's cells in batched launches; the first also takes the worst status
                 jobs.extend((out.ks[:total], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
+                            + ((out.st[:total], plan.worst[rep : rep + 1]) if i == 0 else ())
                             for i in range(0, len(ranks), 16))
                 continue
+            if stop > first:
+                plan.worst[rep] = out.st[first:stop].max()
             ks = gather(out.ks)[:total]  # the gather buffer is reused: select before the next cell
             for i in range(0, len(ranks), 16):
                 eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])

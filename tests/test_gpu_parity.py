@@ -224,6 +224,14 @@ def test_build_table_matches_run_simulation(zk):
     with pytest.raises(zk.SimulationError, match=r"gamma=-30.0, n=3"):
         zk.build_table(ns=(3,), gammas=(-30.0,), support=zk.Support.finite(20), base_seed=5, replicates=100,
                        repetitions=1)
+    # a failing cell inside a batched sweep row (worst status through the batched selection),
+    # for the small-n and the staged two-kernel rows
+    with pytest.raises(zk.SimulationError, match=r"gamma=-30.0, n=3"):
+        zk.build_table(ns=(3,), gammas=(1.0, -30.0), support=zk.Support.finite(20), base_seed=5, replicates=100,
+                       repetitions=2)
+    with pytest.raises(zk.SimulationError, match=r"gamma=-30.0, n=200"):
+        zk.build_table(ns=(200,), gammas=(1.0, -30.0), support=zk.Support.finite(20), base_seed=5, replicates=100,
+                       repetitions=1)
 
 
 def test_sweep_with_shared_uniforms_matches_cells(zk):
