@@ -74,6 +74,8 @@ struct zks_engine {
   size_t pre_bytes = 0;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
   int select_blocks = 0;            // resident grid of the cooperative selection kernel
+  void* cand = nullptr;             // selection candidates (keys matching a 16-bit prefix)
+  size_t cand_bytes = 0;
   // per-kernel timing (zks_engine_set_timing): event pairs around launches on the engine stream
   bool timing = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> timed;
@@ -212,6 +214,7 @@ void zks_engine_destroy(zks_engine* e) {
   cudaFree(e->sel);
   cudaFree(e->sel_out);
   if (e->pre) cudaFree(e->pre);
+  if (e->cand) cudaFree(e->cand);
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
   for (auto& t : e->timed) {
@@ -632,6 +635,16 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
     }
   }
   ZKS_CUDA(cudaSetDevice(e->device));
+  int64_t total = 0;
+  for (int a = 0; a < narrays; ++a) total += counts[a];
+  if (size_t(total) * 8 > e->cand_bytes) {
+    if (e->cand) ZKS_CUDA(cudaFreeAsync(e->cand, e->stream));
+    e->cand = nullptr;
+    e->cand_bytes = 0;
+    ZKS_CUDA(cudaMallocAsync(&e->cand, size_t(total) * 8, e->stream));
+    e->cand_bytes = size_t(total) * 8;
+  }
+  B.cand = static_cast<unsigned long long*>(e->cand);
   // one cooperative launch: every block resident (grid barriers between the radix passes)
   if (e->select_blocks == 0) {
     int per = 0;

@@ -3,7 +3,9 @@
 //
 // KS values are non-negative doubles, so their IEEE-754 bit patterns are order-preserving
 // uint64 keys.  Radix select, 8 passes of 8-bit digits, all requested ranks of up to
-// kSelMaxArrays arrays (the cells of a sweep row) at once, in ONE cooperative launch.  Every
+// kSelMaxArrays arrays (the cells of a sweep row) at once, in ONE cooperative launch.  After the
+// first two passes the keys matching a rank's 16-bit prefix are compacted, so passes 2-7 read
+// only those (a few % of KS values).  Every
 // pass histograms, array by array, the digit of the keys that still match each rank's prefix
 // (per block in shared memory, equal runs counted in registers), merges the block histograms
 // into the pass's global histogram, and after a grid-wide barrier one warp per (array, rank)
@@ -27,6 +29,7 @@ struct SelectState {
   unsigned long long pre[kSelSlots], want[kSelSlots];
   int rep[kSelSlots];  // first rank of the same array with the same prefix (counted once)
   unsigned int worst[kSelMaxArrays];  // max status byte per array (optional)
+  unsigned long long cand_n[kSelMaxArrays];  // keys matching a rank's 16-bit prefix (after pass 1)
 };
 
 // kernel parameters (< 4 KB): the arrays, their lengths, ranks and output pointers
@@ -37,6 +40,7 @@ struct SelectBatch {
   unsigned long long rank[kSelMaxArrays][kMaxRanks];
   const unsigned char* status[kSelMaxArrays];  // optional: replicate status bytes (count[a] of them)
   unsigned char* worst[kSelMaxArrays];         // ... whose maximum lands here
+  unsigned long long* cand;  // >= sum(count) keys: the candidates of passes 2..7, array after array
   int narrays, nr;
 };
 
@@ -57,7 +61,10 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
     st->pre[s] = 0ull;
     st->want[s] = B.rank[s / nr][s % nr];
   }
-  if (tid < B.narrays) st->worst[tid] = 0u;
+  if (tid < B.narrays) {
+    st->worst[tid] = 0u;
+    st->cand_n[tid] = 0ull;
+  }
   grid.sync();
   // worst status per array (montecarlo.py:106-115 failures surface as SimulationError on the host)
   for (int a = 0; a < B.narrays; ++a) {
@@ -88,8 +95,11 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
       __syncthreads();
       // a thread's run of equal (rank, digit) hits is counted in registers and flushed to the
       // block histogram when it changes: the top digits of KS keys repeat (shared exponents)
-      const unsigned long long* keys = B.keys[a];
-      const int64_t count = B.count[a];
+      // passes 0-1 read every key; later passes only the keys that matched a 16-bit prefix
+      int64_t off = 0;
+      for (int q = 0; q < a; ++q) off += B.count[q];
+      const unsigned long long* keys = pass < 2 ? B.keys[a] : B.cand + off;
+      const int64_t count = pass < 2 ? B.count[a] : static_cast<int64_t>(__ldcg(&st->cand_n[a]));
       int run_r = -1;
       unsigned run_d = 0, run_n = 0;
       for (int64_t i = tid; i < count; i += stride) {
@@ -156,6 +166,34 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
       }
     }
     grid.sync();
+    if (pass == 1) {
+      // compaction: the keys that still match a rank's 16-bit prefix (a few % of them for KS
+      // values) are all the later passes need to read
+      int64_t off = 0;
+      for (int a = 0; a < B.narrays; ++a) {
+        if (threadIdx.x < nr) spre[threadIdx.x] = __ldcg(&st->pre[a * nr + threadIdx.x]);
+        __syncthreads();
+        const unsigned long long* keys = B.keys[a];
+        unsigned long long* cand = B.cand + off;
+        for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < B.count[a]; base += stride) {
+          const int64_t i = base + threadIdx.x;  // whole warps iterate together (ballot below)
+          const unsigned long long key = i < B.count[a] ? __ldcg(keys + i) : ~0ull;
+          const unsigned long long top = key & (~0ull << 48);
+          bool hit = false;
+          for (int r = 0; r < nr; ++r) hit |= i < B.count[a] && top == spre[r];
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (m) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(&st->cand_n[a], static_cast<unsigned long long>(__popc(m)));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (hit) cand[at + __popc(m & ((1u << lane) - 1u))] = key;
+          }
+        }
+        off += B.count[a];
+        __syncthreads();
+      }
+      grid.sync();
+    }
   }
   for (int64_t s = tid; s < slots; s += stride)
     B.out[s / nr][s % nr] = __longlong_as_double(static_cast<long long>(__ldcg(&st->pre[s])));
