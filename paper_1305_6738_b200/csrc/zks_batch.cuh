@@ -19,7 +19,7 @@
 namespace zks {
 
 #ifndef ZKS_BATCH_MINB
-#define ZKS_BATCH_MINB 2
+#define ZKS_BATCH_MINB 3
 #endif
 #ifndef ZKS_DRAW_MINB
 #define ZKS_DRAW_MINB 4
