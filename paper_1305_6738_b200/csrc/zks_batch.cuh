@@ -38,6 +38,20 @@ struct DrawStats {
   uint32_t vmin, vmax;
 };
 
+// g += (t < T), as one compare and one predicated add
+__device__ __forceinline__ void inc_if_lt(uint32_t& g, uint32_t t, uint32_t T) {
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(g) : "r"(t), "r"(T));
+}
+
+// f |= 1 if t equals any of T0..T3
+__device__ __forceinline__ void flag_if_any_eq(uint32_t& f, uint32_t t, uint32_t T0, uint32_t T1, uint32_t T2,
+                                               uint32_t T3) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\tsetp.eq.or.u32 p, %1, %3, p;\n\t"
+      "setp.eq.or.u32 p, %1, %4, p;\n\tsetp.eq.or.u32 p, %1, %5, p;\n\t@p or.b32 %0, %0, 1;\n\t}"
+      : "+r"(f)
+      : "r"(t), "r"(T0), "r"(T1), "r"(T2), "r"(T3));
+}
+
 // Draw the n values of stream key (k0, k1) into v[0..n) (warp-cooperative); warp-reduced stats.
 __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
                                                  const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
@@ -98,6 +112,62 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
   s.vmin = mn;
   s.vmax = mx;
   return s;
+}
+
+// The same draws by one lane from its staged row of 32-bit words t = x >> 32 (sweeps): values
+// 1..4 by the exact cut tests t < a.tcut[j] (u > cdf[j]), larger ones by the guide + cdf search
+// on the word's largest u, accepted when the cdf entry below lies under its smallest u.  Returns
+// false when some word leaves its value undecided (the caller redraws from Philox).
+__device__ __forceinline__ bool draw_sample_lane_staged(const ReplicateArgs& a, const uint32_t* __restrict__ row,
+                                                        const uint16_t* __restrict__ guide, uint16_t* v,
+                                                        DrawStats& st) {
+  const int n = static_cast<int>(a.n);
+  const int nb = (n + 3) >> 2;
+  double ls = 0.0;
+  uint32_t mn = 0xffffffffu, mx = 0, amb = 0;
+  for (int b = 0; b < nb; ++b) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(row) + b);
+    const uint32_t t4[4] = {q.x, q.y, q.z, q.w};
+    bool vb[4], big[4];
+    double uu[4];
+    uint32_t x[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t t = t4[w];
+      uint32_t val = 1;
+      inc_if_lt(val, t, a.tcut[0]);
+      inc_if_lt(val, t, a.tcut[1]);
+      inc_if_lt(val, t, a.tcut[2]);
+      inc_if_lt(val, t, a.tcut[3]);
+      vb[w] = 4 * b + w < n;
+      if (vb[w]) flag_if_any_eq(amb, t, a.tcut[0], a.tcut[1], a.tcut[2], a.tcut[3]);
+      big[w] = vb[w] && val == 5u;
+      x[w] = val;
+      uu[w] = 1.0 - static_cast<double>(t) * 0x1p-32;  // the word's largest u
+    }
+    uint32_t s[4];
+    draw_block_u(uu, big, guide, a, s);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      if (big[w]) {
+        const double ulo = uu[w] - (0x1p-32 - 0x1p-53);  // its smallest u
+        if (s[w] >= 2u && __ldg(a.cdf + s[w] - 2) >= ulo) amb = 1u;
+        x[w] = s[w];
+      }
+      if (vb[w]) {
+        ls += __ldg(a.logs + x[w]);
+        mn = min(mn, x[w]);
+        mx = max(mx, x[w]);
+      } else {
+        x[w] = 0u;
+      }
+    }
+    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
+  }
+  st.log_sum = ls;
+  st.vmin = mn;
+  st.vmax = mx;
+  return amb == 0u;
 }
 
 __device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int K, double dn) {
@@ -283,7 +353,10 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     // 1-2. stream key and sample of this lane's replicate
     uint16_t* mv = vals + lane * a.vals_stride;
     DrawStats st{0.0, 0u, 0u};
-    if (active) {
+    bool drawn = false;
+    if (active && a.ubuf)  // sweeps: the row's staged words, shared by every gamma of the row
+      drawn = draw_sample_lane_staged(a, a.ubuf + (a.first + r0 + lane - a.ubuf_first) * a.ubuf_stride, guide, mv, st);
+    if (active && !drawn) {
       uint64_t k0, k1;
       stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
       st = draw_sample_lane(a, k0, k1, guide, mv);
@@ -291,7 +364,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     __syncwarp();
     if (kCount) {
       wk.attempts += nrep;
-      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
+      const unsigned long long d = a.n, nd = __popc(__ballot_sync(0xffffffffu, active && !drawn));
+      wk.draws += nd * d;
+      if (a.ubuf) wk.staged += static_cast<unsigned long long>(nrep) * d;
     }
 
     // 3. exponent fits, one replicate per lane
@@ -580,20 +655,6 @@ constexpr int kPreMaxN = 16384;     // largest n of the two-kernel path (u16 cou
 constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
 // per-warp smem of draw_stats_kernel: bins [v][lane] (u8, or u16 above kNarrowBinsMaxN) + queue
 __host__ __device__ constexpr int draw_warp_bytes(bool wide) { return (kKsHead + 1) * 32 * (wide ? 2 : 1) + kDrawQueue * 8; }
-
-// g += (t < T), as one compare and one predicated add
-__device__ __forceinline__ void inc_if_lt(uint32_t& g, uint32_t t, uint32_t T) {
-  asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(g) : "r"(t), "r"(T));
-}
-
-// f |= 1 if t equals any of T0..T3
-__device__ __forceinline__ void flag_if_any_eq(uint32_t& f, uint32_t t, uint32_t T0, uint32_t T1, uint32_t T2,
-                                               uint32_t T3) {
-  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\tsetp.eq.or.u32 p, %1, %3, p;\n\t"
-      "setp.eq.or.u32 p, %1, %4, p;\n\tsetp.eq.or.u32 p, %1, %5, p;\n\t@p or.b32 %0, %0, 1;\n\t}"
-      : "+r"(f)
-      : "r"(t), "r"(T0), "r"(T1), "r"(T2), "r"(T3));
-}
 
 struct DrawRowOut {
   double ls;

@@ -265,7 +265,9 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
     plan.finished.record(stream)
 
 
-_STAGE_MIN_N, _STAGE_MAX_N = 128, 16384  # n range of the two-kernel path (draw kernel reads staged words)
+# n range whose sweep rows share staged draw words.  Below 128 the lane-per-replicate kernel
+# regenerates its streams: strided per-lane reads of staged rows measured slower than Philox there.
+_STAGE_MIN_N, _STAGE_MAX_N = 128, 16384
 _STAGE_BYTES = 2 << 30                   # staging buffer budget
 
 

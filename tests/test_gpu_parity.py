@@ -267,3 +267,40 @@ def test_sharded_ranges_are_bitwise_identical(zk):
     parts = [run_cell(None, 2.0, 100, 3, 0, a, b - a) for a, b in ((0, 1000), (1000, 3001), (3001, 4096))]
     np.testing.assert_array_equal(ks, np.concatenate([p[0] for p in parts]))
     np.testing.assert_array_equal(gh, np.concatenate([p[1] for p in parts]))
+
+
+@pytest.mark.parametrize("n", [20, 300])
+@pytest.mark.parametrize("j", [0, 2, 9])
+def test_undecided_staged_words_redraw_from_philox(zk, n, j):
+    # a sampling table with cdf[j] strictly inside one staged word's u interval
+    # [1 - (t+1) 2^-32 + 2^-53, 1 - t 2^-32]: that word's value is undecided by its 32 bits
+    # (cut test for j < 4, straddled search for j >= 4), so its replicate must be redrawn from
+    # Philox -- the staged run equals the unstaged one bit for bit (batch kernel at n = 20,
+    # draw kernel at n = 300)
+    import torch
+
+    from paper_1305_6738_b200 import engine
+
+    eng = engine.get_engine()
+    R, K = 64, 20
+    stride = eng.staging_stride(n)
+    u = torch.empty(R * stride, dtype=torch.int32, device="cuda")
+    eng.stage_uniforms(11, 0, 0, R, n, u)
+    t = int(u[5 * stride + 3].item()) & 0xFFFFFFFF  # a word of replicate 5
+    c = 1.0 - (t + 0.5) * 2.0**-32
+    cdf = np.concatenate([np.linspace(c * 0.1, c * 0.9, j), [c], np.linspace(c + (1 - c) * 0.1, 1.0, K - j - 1)])
+    assert np.all(np.diff(cdf) > 0) and cdf.size == K
+    table = engine.DrawTable(eng, cdf)
+    dev = "cuda"
+    outs = []
+    for staged in (False, True):
+        ks = torch.empty(R, dtype=torch.float64, device=dev)
+        gh = torch.empty_like(ks)
+        st = torch.empty(R, dtype=torch.uint8, device=dev)
+        if staged:
+            eng.run_replicates_staged(table, K, 1.0, n, 11, 0, 0, R, u, 0, R, ks, gh, st)
+        else:
+            eng.run_replicates(table, K, 1.0, n, 11, 0, 0, R, ks, gh, st)
+        outs.append((ks.cpu().numpy(), gh.cpu().numpy(), st.cpu().numpy()))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
