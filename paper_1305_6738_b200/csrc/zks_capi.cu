@@ -46,7 +46,7 @@ constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory ca
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
 constexpr int64_t kBatchMaxN = 1024;                  // n up to which replicate_batch_kernel runs
-constexpr uint64_t kPreBytes = uint64_t(1) << 30;     // pre-drawn rows per chunk (bytes)
+constexpr uint64_t kPreBytes = uint64_t(4) << 30;     // pre-drawn rows per chunk (bytes)
 constexpr uint32_t kBatchHist = 512;                  // its per-warp histogram bins
 
 }  // namespace

@@ -268,7 +268,7 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
 # n range whose sweep rows share staged draw words.  Below 128 the lane-per-replicate kernel
 # regenerates its streams: strided per-lane reads of staged rows measured slower than Philox there.
 _STAGE_MIN_N, _STAGE_MAX_N = 128, 16384
-_STAGE_BYTES = 2 << 30                   # staging buffer budget
+_STAGE_BYTES = 8 << 30                   # staging buffer budget (one chunk per 10^6-replicate row up to n = 2000)
 
 
 def _stage_key(cfg: SimulationConfig):
