@@ -779,12 +779,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     resolve(q, ok);
   }
   // counts of 1..4 from the threshold counts
-  uint32_t c01 = g0 | (g1 << 16), c2 = g2;  // n < 2^16
-#pragma unroll
-  for (int s = 16; s; s >>= 1) {
-    c01 += __shfl_xor_sync(0xffffffffu, c01, s);
-    c2 += __shfl_xor_sync(0xffffffffu, c2, s);
-  }
+  const uint32_t c01 = warp_sum_u32(g0 | (g1 << 16)), c2 = warp_sum_u32(g2);  // n < 2^16
   const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c2, G3 = qtot;
   __syncwarp();
   // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33

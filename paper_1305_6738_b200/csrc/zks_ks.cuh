@@ -30,21 +30,10 @@ constexpr int kKsQueueWords = 3 * kKsQueue;
 constexpr uint32_t kOverCap = 128;     // values above the histogram ordered in registers (<= kKsQueueWords)
 constexpr double kKsMargin = 1e-11;  // early-exit safety margin (>> fp64 rounding of the sums)
 
-__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
+// warp reductions of 32-bit integers: one REDUX instruction each (sm_80+)
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
 
 struct KsParams {
   int64_t n;
@@ -197,7 +186,7 @@ __device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int&
       }
       q -= 32;
       __syncwarp();
-      s.Dw = warp_max(s.D);
+      s.Dw = warp_max_nonneg(s.D);
     }
     // exit test, only once the empirical part of the bound allows it (D changes only at
     // flushes); F-based tests back off geometrically in k (heavy tails approach 1 slowly)
@@ -206,7 +195,7 @@ __device__ __forceinline__ void ks_sparse_tiles(KsState& s, const KsCtx& c, int&
       ks_flush<kArg>(s, c, q, lane, wk);
       q = 0;
       __syncwarp();
-      s.Dw = warp_max(s.D);
+      s.Dw = warp_max_nonneg(s.D);
       double fk;
       const double F_pos = (s.S_head + em_block(c, k_hi, fk)) * c.inv;
       ++wk.ks_tails;
@@ -296,12 +285,12 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     s.S = __shfl_sync(0xffffffffu, S, 31);
     s.Cb = __shfl_sync(0xffffffffu, C, 31);
     wk.ks_terms += min(32u, head_end - k0 + 1);
-    const double Dw = warp_max(s.D);
+    const double Dw = warp_max_nonneg(s.D);
     if (Dw > fmax(1.0 - emp(c, s.Cb), 1.0 - s.S * c.inv) + kKsMargin) s.done = true;
   }
   if (!s.done && kmax > kKsHead) {
     s.S_head = s.S;
-    s.Dw = p.from_head ? p.D0 : warp_max(s.D);  // from_head: D0 is the warp's value
+    s.Dw = p.from_head ? p.D0 : warp_max_nonneg(s.D);  // from_head: D0 is the warp's value
     c.La = __ldg(p.logs + kKsHead + 1);
     c.fa = exp_bounded(-g * c.La);
     constexpr double a = static_cast<double>(kKsHead + 1);
@@ -324,7 +313,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
         ks_flush<kArg>(s, c, q, lane, wk);  // the emptied queue stages the values
         q = 0;
         __syncwarp();
-        s.Dw = warp_max(s.D);
+        s.Dw = warp_max_nonneg(s.D);
       }
       const unsigned lt = (1u << lane) - 1u;
       uint32_t m = 0;
@@ -406,7 +395,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
             }
             ne -= 32;
             __syncwarp();
-            s.Dw = warp_max(s.D);
+            s.Dw = warp_max_nonneg(s.D);
             // observations <= the last scored value, and F there, bound every later gap
             if (s.Dw > fmax(1.0 - emp(c, fl.C_last), 1.0 - fl.F_last) + kKsMargin) s.done = true;
           }
@@ -445,7 +434,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
   }
   // warp result: max gap, smallest k among equal maxima
   if (!kArg) {
-    out.D = warp_max(s.D);
+    out.D = warp_max_nonneg(s.D);
     return out;
   }
   double D = s.D;
