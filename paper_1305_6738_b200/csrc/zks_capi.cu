@@ -57,7 +57,6 @@ struct zks_engine {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   double* logs = nullptr;
-  unsigned long long* work = nullptr;
   uint16_t* slab = nullptr;
   size_t slab_bytes = 0;
   zks::SelectState* sel = nullptr;
@@ -70,8 +69,14 @@ struct zks_engine {
   int mle_mode = ZKS_MLE_TABLE;
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
-  void* pre = nullptr;  // pre-drawn sample rows + their statistics (two-kernel path)
-  size_t pre_bytes = 0;
+  // per-stream scratch: the replicate kernels' work counter and the pre-drawn rows (two-kernel
+  // path), so cells enqueued on different streams run concurrently without sharing either
+  struct Scratch {
+    unsigned long long* work = nullptr;
+    void* pre = nullptr;
+    size_t pre_bytes = 0;
+  };
+  std::map<cudaStream_t, Scratch> scratch;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
   int select_blocks = 0;            // resident grid of the cooperative selection kernel
   void* cand = nullptr;             // selection candidates (keys matching a 16-bit prefix)
@@ -128,6 +133,19 @@ struct Timed {
     e->timed.emplace_back(kind, a, b);
   }
 };
+
+// the calling stream's scratch (created on first use)
+cudaError_t scratch_for(zks_engine* e, zks_engine::Scratch** out) {
+  auto it = e->scratch.find(e->stream);
+  if (it == e->scratch.end()) {
+    zks_engine::Scratch sc;
+    const cudaError_t err = cudaMalloc(&sc.work, sizeof(unsigned long long));
+    if (err != cudaSuccess) return err;
+    it = e->scratch.emplace(e->stream, sc).first;
+  }
+  *out = &it->second;
+  return cudaSuccess;
+}
 
 // every kernel launch goes through here: the error check and the engine's launch count
 cudaError_t launched(zks_engine* e) {
@@ -190,7 +208,6 @@ int zks_engine_create(int device, const double* logs_host, int64_t logs_len, zks
   cudaError_t err = cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaMalloc(&e->logs, kLogsLen * sizeof(double));
   if (err == cudaSuccess) err = cudaMemcpy(e->logs, logs_host, kLogsLen * sizeof(double), cudaMemcpyHostToDevice);
-  if (err == cudaSuccess) err = cudaMalloc(&e->work, sizeof(unsigned long long));
   if (err == cudaSuccess) err = cudaMalloc(&e->sel, sizeof(zks::SelectState));
   if (err == cudaSuccess) err = cudaMallocHost(&e->staging, kStagingSlots * kStagingLen * sizeof(double));
   for (int i = 0; i < kStagingSlots && err == cudaSuccess; ++i)
@@ -209,11 +226,13 @@ void zks_engine_destroy(zks_engine* e) {
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
   cudaFree(e->logs);
-  cudaFree(e->work);
   cudaFree(e->slab);
   cudaFree(e->sel);
   cudaFree(e->sel_out);
-  if (e->pre) cudaFree(e->pre);
+  for (auto& kv : e->scratch) {
+    cudaFree(kv.second.work);
+    if (kv.second.pre) cudaFree(kv.second.pre);
+  }
   if (e->cand) cudaFree(e->cand);
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
@@ -411,7 +430,9 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.ks_out = ks_dev;
   a.gh_out = gh_dev;
   a.st_out = st_dev;
-  a.work = e->work;
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  a.work = sc->work;
   a.counters = e->counters;
   a.ubuf = nullptr;
   a.ubuf_stride = 0;
@@ -511,14 +532,14 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(a.vals_stride) * 2 + 4;
     const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, kPreBytes / row_bytes));
     const size_t need = size_t(chunk) * row_bytes + 16;
-    if (need > e->pre_bytes) {
-      if (e->pre) ZKS_CUDA(cudaFreeAsync(e->pre, e->stream));
-      e->pre = nullptr;
-      e->pre_bytes = 0;
-      ZKS_CUDA(cudaMallocAsync(&e->pre, need, e->stream));
-      e->pre_bytes = need;
+    if (need > sc->pre_bytes) {
+      if (sc->pre) ZKS_CUDA(cudaFreeAsync(sc->pre, e->stream));
+      sc->pre = nullptr;
+      sc->pre_bytes = 0;
+      ZKS_CUDA(cudaMallocAsync(&sc->pre, need, e->stream));
+      sc->pre_bytes = need;
     }
-    uint16_t* phead = reinterpret_cast<uint16_t*>(e->pre);
+    uint16_t* phead = reinterpret_cast<uint16_t*>(sc->pre);
     double* pls = reinterpret_cast<double*>(phead + chunk * zks::kKsHead);
     uint32_t* pmin = reinterpret_cast<uint32_t*>(pls + chunk);
     uint32_t* pmax = pmin + chunk;
@@ -578,7 +599,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
       }
       const int64_t fblocks =
           std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * fper, (int64_t)((cnt + 255) / 256)));
-      ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+      ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
       ZKS_CUDA(cudaMemsetAsync(retry, 0, sizeof(uint32_t), e->stream));
       {
         Timed tm(e, ZKS_KERNEL_FIT);
@@ -593,7 +614,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     }
     return ZKS_OK;
   }
-  ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+  ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
   {
     Timed tm(e, batched ? ZKS_KERNEL_BATCH : ZKS_KERNEL_SINGLE);
     kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
@@ -823,7 +844,9 @@ int zks_fit_samples(zks_engine* e, int32_t support_k, const int64_t* values_dev,
   a.argmax_out = argmax_dev;
   a.status_out = status_dev;
   a.hist_words = zks::round_up(zks::kSamplesHist + 1, 4);
-  a.work = e->work;
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  a.work = sc->work;
   // the fit tables cover [-20, 20] (finite) and [1.05, 20] (unbounded): wider brackets sum directly
   a.use_table = e->mle_mode == ZKS_MLE_TABLE && (support_k == 0 || (P.lo >= -20.0 && P.hi <= 20.0));
   if (a.use_table) {
@@ -834,7 +857,7 @@ int zks_fit_samples(zks_engine* e, int32_t support_k, const int64_t* values_dev,
   const size_t smem = size_t(zks::kWarps) * (a.hist_words + zks::kKsQueueWords) * 4;
   ZKS_CUDA(cudaFuncSetAttribute(zks::samples_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (nsamples + zks::kWarps - 1) / zks::kWarps));
-  ZKS_CUDA(cudaMemsetAsync(e->work, 0, sizeof(unsigned long long), e->stream));
+  ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
   {
     Timed tm(e, ZKS_KERNEL_OTHER);
     zks::samples_kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
