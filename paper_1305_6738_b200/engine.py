@@ -98,6 +98,10 @@ class Engine:
         return {k: (ms[i], cnt[i]) for i, k in enumerate(_native.KERNEL_KINDS)}
 
     # -- tables --------------------------------------------------------------
+    def has_table(self, gamma: float, support_k: int | None) -> bool:
+        with self._lock:
+            return (float(gamma), support_k) in self._tables
+
     def table(self, gamma: float, support_k: int | None, cdf_builder) -> DrawTable:
         """Cached device table for the generating model (montecarlo.py:82-86 lru_cache)."""
         key = (float(gamma), support_k)

@@ -226,6 +226,7 @@ class _CellPlan:
     worst: object = None       # device [reps] max status
     started: object = None
     finished: object = None
+    host: object = None        # (quantiles, worst) copied to the host by _fetch_plans
 
 
 def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, gather=None,
@@ -354,8 +355,28 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
         plan.finished.record(stream)
 
 
+def _prefetch_tables(eng, configs) -> None:
+    """Build the host sampling CDFs a sweep still lacks on a thread pool (numpy releases the
+    GIL), then upload them: the first cells do not wait for every table to be built serially."""
+    missing = {}
+    for cfg in configs:
+        key = (float(cfg.gamma), cfg.support.k)
+        if key not in missing and not eng.has_table(*key):
+            missing[key] = cfg
+    if len(missing) < 2:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfgs = list(missing.values())
+    with ThreadPoolExecutor(max_workers=min(len(cfgs), os.cpu_count() or 1, 16)) as ex:
+        cdfs = list(ex.map(lambda c: sampling_cdf(c.gamma, c.support), cfgs))
+    for cfg, cdf in zip(cfgs, cdfs):
+        eng.table(cfg.gamma, cfg.support.k, lambda cdf=cdf: cdf)
+
+
 def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
     """Queue many cells, grouping those that can share uniform streams (_enqueue_group)."""
+    _prefetch_tables(eng, [p.config for p in plans])
     groups: dict = {}
     for plan in plans:
         groups.setdefault(_stage_key(plan.config), []).append(plan)
@@ -363,9 +384,24 @@ def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
         _enqueue_group(eng, group, shard=shard, gather=gather, kernel_events=kernel_events)
 
 
+def _fetch_plans(plans: list[_CellPlan]) -> None:
+    """One device-to-host copy of every plan's worst statuses and quantiles (instead of two
+    synchronising copies per cell); _finish_cell then reads the host copies."""
+    torch = _torch()
+    if not plans:
+        return
+    flat = torch.cat([torch.cat([p.quantiles.reshape(-1), p.worst.to(torch.float64)]) for p in plans]).cpu().numpy()
+    at = 0
+    for p in plans:
+        nq, nw = p.quantiles.numel(), p.worst.numel()
+        p.host = (flat[at : at + nq].reshape(p.quantiles.shape), flat[at + nq : at + nq + nw].astype(np.uint8))
+        at += nq + nw
+
+
 def _finish_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None) -> list[tuple[float, float]]:
     cfg = plan.config
-    worst = plan.worst.cpu().numpy()
+    host = getattr(plan, "host", None)
+    worst = host[1] if host is not None else plan.worst.cpu().numpy()
     if worst.max(initial=0) >= _native.STATUS_FAILED:
         # re-run the first failing repetition to name the first failing replicate
         rep = int(np.flatnonzero(worst >= _native.STATUS_FAILED)[0])
@@ -373,7 +409,7 @@ def _finish_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None) -> 
         slab = _slab(eng, cfg.replicates)
         _enqueue(eng, cfg, rep, first, stop - first, slab, offset=first)
         _raise_first_failure(cfg, rep, first, slab.st[first:stop].cpu().numpy(), slab.gh[first:stop].cpu().numpy())
-    per_rep = plan.quantiles.cpu().numpy()
+    per_rep = host[0] if host is not None else plan.quantiles.cpu().numpy()
     per_level = np.zeros(per_rep.shape[1])
     for rep in range(cfg.repetitions):  # montecarlo.py:203-211: add in repetition order
         per_level += per_rep[rep]
@@ -467,6 +503,7 @@ def build_table(
             plans.append(_CellPlan(cfg))
     eng = _engine()
     _enqueue_plans(eng, plans)
+    _fetch_plans(plans)
     cells: dict[tuple[float, int], tuple[float, ...]] = {}
     for plan in plans:
         cfg = plan.config

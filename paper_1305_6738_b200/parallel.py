@@ -26,6 +26,7 @@ from .montecarlo import (
     _CellPlan,
     _engine,
     _enqueue_plans,
+    _fetch_plans,
     _finish_cell,
     _slab,
     _validate_levels,
@@ -110,6 +111,7 @@ def build_table(
     dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
     for plan, w in zip(plans, worst.tolist()):
         plan.worst.fill_(w if w < _native.STATUS_FAILED else 0)
+    _fetch_plans(plans)
     cells = {}
     for plan, w in zip(plans, worst.tolist()):
         cfg = plan.config
