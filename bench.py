@@ -365,7 +365,7 @@ def run_b200(args, world, rank, local):
         assert table.cells == rows, "public API and device sweep disagree"
         e2e = {"value": args.steps * ncells * R / secs, "unit": "replicates/s",
                "h2d_bytes_per_step": len(GAMMAS) * 65535 * 8,
-               "d2h_bytes_per_step": ncells * (4 * 8 + 1) + (4 * ncells if world > 1 else 0),
+               "d2h_bytes_per_step": ncells * (4 + 1) * 8 + (4 * ncells if world > 1 else 0),
                "api": "paper_1305_6738_b200.build_table" if world == 1 else "paper_1305_6738_b200.parallel.build_table"}
 
     cpu = None
