@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // largest u and accepted when the cdf entry below lies under its smallest u.  A replicate with
 // an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
-constexpr int kPreMaxN = 16384;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
+constexpr int kPreMaxN = 65535;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
 constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
 // per-warp smem of draw_stats_kernel: bins [v][lane] (u8, or u16 above kNarrowBinsMaxN) + queue
 __host__ __device__ constexpr int draw_warp_bytes(bool wide) { return (kKsHead + 1) * 32 * (wide ? 2 : 1) + kDrawQueue * 8; }

@@ -140,6 +140,7 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (50, 4.0, 40, 12, 0, 600),
         (None, 1.6, 9000, 3, 0, 24),  # two-kernel path with u16 draw bins
         (1000, 1.0, 5000, 2, 0, 24),
+        (None, 1.9, 40000, 4, 0, 8),  # two-kernel path near its u16 limit
     ],
 )
 def test_replicates_match_oracle(zk, mle_mode, K, gamma, n, seed, rep, count):

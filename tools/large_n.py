@@ -9,7 +9,7 @@ eng = engine.get_engine()
 cells = [(1000, 1.0, 500, 200000), (1000, 1.0, 1000, 200000), (1000, 1.0, 2000, 100000), (1000, 1.0, 5000, 50000),
          (1000, 1.0, 10000, 20000), (1000, 0.5, 10000, 20000), (1000, 2.0, 10000, 20000),
          (None, 2.0, 1000, 200000), (None, 2.0, 2000, 100000), (None, 2.0, 10000, 20000),
-         (None, 2.0, 100000, 4000), (None, 2.0, 1000000, 400)]
+         (None, 2.0, 30000, 10000), (None, 2.0, 65535, 4000), (1000, 1.0, 50000, 4000), (None, 2.0, 100000, 4000), (None, 2.0, 1000000, 400)]
 for K, g, n, R in cells:
     ks = torch.empty(R, dtype=torch.float64, device='cuda'); gh = torch.empty_like(ks); st = torch.empty(R, dtype=torch.uint8, device='cuda')
     t = eng.table(g, K, lambda: sampling_cdf(g, Support(K)))
