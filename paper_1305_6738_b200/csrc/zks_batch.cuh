@@ -286,6 +286,21 @@ __device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r
   return ks_scan<uint16_t, false>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
 }
 
+// The same from dense counts of the values kKsHead+1..K (counts[v - kKsHead - 1], global memory)
+__device__ __forceinline__ KsOut ks_tail_dense(const ReplicateArgs& a, int r, double g, double norm, uint32_t kmax,
+                                               double S, uint32_t C, double D, const uint32_t* counts,
+                                               uint32_t* queue, int lane, Work& wk) {
+  KsParams p = ks_params(a);
+  p.H = static_cast<uint32_t>(kKsHead + a.dense_words);  // kmax <= K <= H: no values above
+  p.from_head = true;
+  p.S0 = __shfl_sync(0xffffffffu, S, r);
+  p.C0 = __shfl_sync(0xffffffffu, C, r);
+  p.D0 = __shfl_sync(0xffffffffu, D, r);
+  // ks_scan reads counts[k] for k > kKsHead
+  return ks_scan<uint16_t, false>(p, g, norm, kmax, const_cast<uint32_t*>(counts) - (kKsHead + 1), nullptr, 0u, queue,
+                                  lane, wk);
+}
+
 // One replicate's second attempt on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative:
 // draw into v, fit, score.  Returns the status (1 retried, 2 failed twice).
 template <bool kCount>
@@ -511,6 +526,18 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     // values of the next replicate are loaded into registers while the current one is scored,
     // then staged in shared memory (tails of <= kOverCap values; longer ones read from HBM/L2).
     unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored);
+    if (a.dense_words) {  // dense finite support: tiles over the counts of kKsHead+1..kmax
+      for (; need; need &= need - 1) {
+        const int r = __ffs(need) - 1;
+        const double gr = __shfl_sync(0xffffffffu, g, r);
+        const double nr = __shfl_sync(0xffffffffu, norm, r);
+        const uint32_t kmax = __shfl_sync(0xffffffffu, vmax, r);
+        const uint32_t* counts = reinterpret_cast<const uint32_t*>(
+            a.pre_tail + (a.first + r0 + r - a.pre_first) * a.vals_stride);
+        const KsOut ko = ks_tail_dense(a, r, gr, nr, kmax, hS, hC, hD, counts, queue, lane, wk);
+        if (lane == r) my_ks = ko.D;
+      }
+    }
     uint32_t pv[kOverCap / 32], pm = 0;
     auto issue = [&](int r) {
       pm = __shfl_sync(0xffffffffu, my_m, r);
@@ -652,6 +679,7 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
 constexpr int kPreMaxN = 65535;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
+constexpr int kDenseMaxK = 1024;       // finite supports kept as dense counts above the head
 constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
 // per-warp smem of draw_stats_kernel: bins [v][lane] (u8, or u16 above kNarrowBinsMaxN) + queue
 __host__ __device__ constexpr int draw_warp_bytes(bool wide) { return (kKsHead + 1) * 32 * (wide ? 2 : 1) + kDrawQueue * 8; }
@@ -665,7 +693,7 @@ struct DrawRowOut {
 // word was undecided: the caller redraws the row with kStaged = false).
 template <bool kStaged, typename BinT>
 __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, const uint32_t* __restrict__ urow,
-                                         const uint16_t* __restrict__ guide, BinT* bins, void* qmem,
+                                         const uint16_t* __restrict__ guide, BinT* bins, void* qmem, uint32_t* dense,
                                          uint16_t* tail, uint16_t* head, DrawRowOut& o, int lane) {
   using Q = typename std::conditional<kStaged, uint32_t, double>::type;
   Q* queue = reinterpret_cast<Q*>(qmem);
@@ -709,7 +737,10 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     const bool big = ok && v > kKsHead;
     const unsigned bm = __ballot_sync(0xffffffffu, big);
     if (big) {
-      tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+      if (dense)
+        atomicAdd(dense + (v - kKsHead - 1), 1u);
+      else
+        tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
       ls += __ldg(a.logs + v);
     }
     m += __popc(bm);
@@ -807,6 +838,15 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   for (int i = lane; i < (kKsHead - 4) * 8 * static_cast<int>(sizeof(BinT)); i += 32)
     reinterpret_cast<uint32_t*>(bins + 5 * 32)[i] = 0u;
   const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
+  if (dense) {  // counts of kKsHead+1..K into the row's tail slot (u32), the warp histogram reset
+    __syncwarp();
+    uint32_t* out = reinterpret_cast<uint32_t*>(tail);
+    for (int i = lane; i < a.dense_words; i += 32) {
+      if (!undecided) out[i] = dense[i];
+      dense[i] = 0u;
+    }
+    __syncwarp();
+  }
   if (!undecided) {
     head[lane] = static_cast<uint16_t>(hc0);  // n <= kPreMaxN: u16 counts
     head[lane + 32] = static_cast<uint16_t>(hc1);
@@ -831,11 +871,13 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using BinT = typename std::conditional<kWide, uint16_t, uint8_t>::type;
-  unsigned char* wbase = smem + guide_bytes + warp * draw_warp_bytes(kWide);
+  unsigned char* wbase = smem + guide_bytes + warp * (draw_warp_bytes(kWide) + a.dense_words * 4);
   // lane-private counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
   // most one queued draw per pop and there are <= n/32 + 1 pops (u8 up to kNarrowBinsMaxN)
   BinT* bins = reinterpret_cast<BinT*>(wbase);
   void* queue = wbase + (kKsHead + 1) * 32 * sizeof(BinT);
+  uint32_t* dense = a.dense_words ? reinterpret_cast<uint32_t*>(wbase + draw_warp_bytes(kWide)) : nullptr;
+  for (int i = lane; i < a.dense_words; i += 32) dense[i] = 0u;
   load_guide(guide, a.guide, a.guide_levels);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
@@ -848,13 +890,13 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
     DrawRowOut o;
     bool done = false;
     if (a.ubuf) {
-      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, bins, queue, tail, head, o,
-                            lane);
+      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, bins, queue, dense, tail,
+                            head, o, lane);
       staged += a.n;
       redrawn += !done;
     }
     if (!done) {
-      draw_row<false>(a, idx, nullptr, guide, bins, queue, tail, head, o, lane);
+      draw_row<false>(a, idx, nullptr, guide, bins, queue, dense, tail, head, o, lane);
       philox += a.n;
     }
     if (lane == 0) {

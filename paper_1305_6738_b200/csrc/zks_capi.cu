@@ -525,7 +525,13 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.pre_min = nullptr;
   a.pre_max = nullptr;
   a.pre_first = 0;
+  a.dense_words = 0;
   if (two_kernel) {
+    // finite supports above the head and up to kDenseMaxK: dense counts instead of value lists
+    if (c->support_k > static_cast<int>(zks::kKsHead) && c->support_k <= zks::kDenseMaxK) {
+      a.dense_words = c->support_k - static_cast<int>(zks::kKsHead);
+      a.vals_stride = std::max(a.vals_stride, zks::round_up(2 * a.dense_words, 4));
+    }
     // draw phase in its own high-occupancy kernel (head counts + tail values per replicate),
     // then fit + score, then the listed retries; chunk by chunk.  Per row: u16 head counts
     // (128 B), log-sum, min / max / m, the tail values, a retry-list slot.
@@ -555,7 +561,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
                                              size_t(zks::retry_warp_bytes(a.hist_words, a.vals_stride)))));
     auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
     auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
-    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * zks::draw_warp_bytes(wide);
+    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(a.dense_words) * 4);
     const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
     const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
     int dper = 0, fper = 0;

@@ -71,6 +71,9 @@ struct ReplicateArgs {
   const uint32_t* pre_min;
   const uint32_t* pre_max;
   uint64_t pre_first;
+  // dense finite supports (kKsHead < K <= kDenseMaxK): the values above kKsHead are kept as u32
+  // counts of kKsHead+1..K in the row's tail slot instead of a value list (0 = value lists)
+  int dense_words;
   double inv_n;  // 1 / n
   uint32_t tcut[4];     // staged words: u > cdf_head[j] <=> t < tcut[j] (undecided at equality)
   double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
