@@ -305,3 +305,36 @@ def test_undecided_staged_words_redraw_from_philox(zk, n, j):
         outs.append((ks.cpu().numpy(), gh.cpu().numpy(), st.cpu().numpy()))
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+def test_cells_on_two_streams_match_sequential(zk):
+    # the engine keeps its scratch (work counters, pre-drawn rows) per CUDA stream: cells enqueued
+    # on two streams at once give the same results as one after the other
+    import torch
+
+    from paper_1305_6738_b200 import engine
+    from paper_1305_6738_b200.distribution import Support, sampling_cdf
+
+    eng = engine.get_engine()
+    cells = [(None, 2.2, 300), (None, 1.8, 600), (1000, 1.0, 50), (None, 2.6, 400)]
+    R = 3000
+
+    def run(streams):
+        outs = []
+        for i, (K, g, n) in enumerate(cells):
+            table = eng.table(g, K, lambda: sampling_cdf(g, Support(K)))
+            with torch.cuda.stream(streams[i % len(streams)]):
+                ks = torch.empty(R, dtype=torch.float64, device="cuda")
+                gh = torch.empty_like(ks)
+                st = torch.empty(R, dtype=torch.uint8, device="cuda")
+                eng.run_replicates(table, K, g, n, 5, 0, 0, R, ks, gh, st)
+                outs.append((ks, gh, st))
+        torch.cuda.synchronize()
+        eng.bind_stream()
+        return [tuple(x.cpu().numpy() for x in o) for o in outs]
+
+    seq = run([torch.cuda.current_stream()])
+    par = run([torch.cuda.Stream(), torch.cuda.Stream()])
+    for a, b in zip(seq, par):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
