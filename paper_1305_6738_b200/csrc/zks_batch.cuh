@@ -27,10 +27,6 @@ namespace zks {
 #ifndef ZKS_FIT_MINB
 #define ZKS_FIT_MINB 3
 #endif
-#ifndef ZKS_BATCH_VALS
-#define ZKS_BATCH_VALS 4096
-#endif
-constexpr int kBatchVals = ZKS_BATCH_VALS;  // u16 sample slots per warp
 constexpr int kLaneDrawMaxN = 128;  // below this n a lane draws a whole replicate
 
 struct DrawStats {
@@ -55,7 +51,7 @@ __device__ __forceinline__ void flag_if_any_eq(uint32_t& f, uint32_t t, uint32_t
 // Draw the n values of stream key (k0, k1) into v[0..n) (warp-cooperative); warp-reduced stats.
 __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
                                                  const uint16_t* __restrict__ guide, uint16_t* v, int lane) {
-  const int n = static_cast<int>(a.n);  // batch kernel: n <= kBatchVals
+  const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0;

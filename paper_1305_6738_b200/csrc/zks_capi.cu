@@ -469,7 +469,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
     a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
-    a.batch = std::max(1, std::min(32, zks::kBatchVals / a.vals_stride));
+    a.batch = 32;  // one replicate per lane (n < kLaneDrawMaxN)
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
     smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride);
     per_block = int64_t(zks::kWarps) * a.batch;
