@@ -231,22 +231,36 @@ def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms) -> di
             roof["traffic_source"] = tr["source"]
     except (OSError, KeyError, ValueError, ZeroDivisionError):
         pass
-    # the pipes that actually bound the replicate math: FP64 power terms and
-    # 64-bit Philox multiplies, counted from the reference algorithm, against on-device probes
+    # SURVEY.md 8(d)'s compute roofline of the REFERENCE algorithm on the same inputs: W_INT =
+    # 5 mulhilo per draw (Philox4x64-10, n draws per replicate), T = the power terms it sums
+    # (Newton moment evaluations x their m-rule / K terms, the fitted normaliser, min(kmax, 4096)
+    # KS terms; counted in-kernel at the same iterates), each one exp + 3 FMA-class ops;
+    # T_ideal = max(W_INT / P_INT, T c_exp / P_FP64) with the pipe peaks probed on this device.
+    # ratio = T_ideal / measured sweep time (> 1: the fit tables and Euler-Maclaurin tails skip
+    # work the reference algorithm does).
     exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
     terms = eval_terms + norm_terms + ks_terms
-    fp64_flops = terms * (exp_flops + 6.0) + ks_tails * (2 * exp_flops + 20.0)
-    mul64 = 5.0 * (draws + staged_made)
+    fp64_flops = terms * (exp_flops + 6.0)
+    ref_draws = sum(n for n in NS) * len(GAMMAS) * per_gpu
+    mul64 = 5.0 * ref_draws
+    t_fp64 = fp64_flops / peaks["dfma_flops"]
+    t_int = mul64 / peaks["mul64_per_s"]
+    sweep_s = total_ms / steps / 1e3
     kernel_s = kernel_ms / 1e3
     roof["compute"] = {
-        "fp64": {"achieved_tflops": fp64_flops / kernel_s / 1e12, "peak_tflops": peaks["dfma_flops"] / 1e12,
-                 "t_ideal_ms_per_sweep": fp64_flops / peaks["dfma_flops"] * 1e3},
-        "int64_mul": {"achieved_tmul_s": mul64 / kernel_s / 1e12, "peak_tmul_s": peaks["mul64_per_s"] / 1e12,
-                      "t_ideal_ms_per_sweep": mul64 / peaks["mul64_per_s"] * 1e3},
+        "reference_algorithm": {"t_ideal_ms_per_sweep": max(t_fp64, t_int) * 1e3, "bound": "fp64" if t_fp64 > t_int
+                                else "int64_mul", "ratio_to_measured": max(t_fp64, t_int) / sweep_s,
+                                "power_terms": terms, "philox_mulhilo": mul64},
+        "fp64": {"reference_tflop_equiv_per_s": fp64_flops / sweep_s / 1e12, "peak_tflops": peaks["dfma_flops"] / 1e12,
+                 "t_ideal_ms_per_sweep": t_fp64 * 1e3},
+        "int64_mul": {"reference_tmul_per_s": mul64 / sweep_s / 1e12, "peak_tmul_s": peaks["mul64_per_s"] / 1e12,
+                      "t_ideal_ms_per_sweep": t_int * 1e3,
+                      "made_on_device_per_sweep": 5.0 * (draws + staged_made)},
         "peak_source": "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)",
         "work_per_sweep": {"replicates": ncells * per_gpu, "attempts": attempts, "philox_draws": draws,
                            "staged_words_read": staged, "staged_words_made": staged_made,
-                           "staged_rows_redrawn": redrawn, "moment_evals": evals, "power_terms": terms,
+                           "staged_rows_redrawn": redrawn, "moment_evals": evals,
+                           "reference_power_terms": {"moments": eval_terms, "normaliser": norm_terms, "ks": ks_terms},
                            "ks_tail_endpoints": ks_tails, "fp64_exp_dfma_equiv": exp_flops},
     }
     roof["kernels"] = kern

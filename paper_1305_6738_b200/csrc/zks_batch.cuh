@@ -29,6 +29,22 @@ namespace zks {
 #endif
 constexpr int kLaneDrawMaxN = 128;  // below this n a lane draws a whole replicate
 
+// warp totals of the lane-parallel fits' work counters into the warp's Work
+__device__ __forceinline__ void add_lane_work(Work& wk, const Work& lw) {
+  const unsigned long long f[4] = {lw.evals, lw.eval_terms, lw.norm_terms, lw.ks_terms};
+  unsigned long long t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    t[i] = f[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t[i] += __shfl_xor_sync(0xffffffffu, t[i], o);
+  }
+  wk.evals += t[0];
+  wk.eval_terms += t[1];
+  wk.norm_terms += t[2];
+  wk.ks_terms += t[3];
+}
+
 struct DrawStats {
   double log_sum;
   uint32_t vmin, vmax;
@@ -389,13 +405,12 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
       ok = fit_exponent(M, target, lane, g, lw);
       if (ok) norm = fit_norm(a.fit, g);
       if (!ok) g = target;
+      if (kCount && ok) {  // the reference's normaliser and KS terms (min(kmax, 4096), gof.py:49-105)
+        lw.norm_terms += ref_norm_terms(a.fit, g);
+        lw.ks_terms += min(st.vmax, static_cast<uint32_t>(kSeam));
+      }
     }
-    if (kCount) {
-      unsigned long long e = lw.evals;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-      wk.evals += e;
-    }
+    if (kCount) add_lane_work(wk, lw);
 
     // 4. KS: the head lane by lane, long tails warp-cooperatively
     double my_ks = __longlong_as_double(0x7ff8000000000000ll);
@@ -500,12 +515,13 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
       ok = fit_exponent(M, target, lane, g, lw);
       if (ok) norm = fit_norm(a.fit, g);
       if (!ok) g = target;
+      if (kCount && ok) {
+        lw.norm_terms += ref_norm_terms(a.fit, g);
+        lw.ks_terms += min(vmax, static_cast<uint32_t>(kSeam));
+      }
     }
     if (kCount) {
-      unsigned long long e = lw.evals;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-      wk.evals += e;
+      add_lane_work(wk, lw);
       wk.attempts += nrep;
     }
     __syncwarp();

@@ -100,6 +100,24 @@ __device__ __forceinline__ double fit_norm(const FitTable& T, double x) {
   return v;
 }
 
+// Terms the reference sums for one model-moment evaluation at x (K, or the m rule of the
+// segment: series.py:102-123) and for the normaliser (series.py:126-138): the reference
+// algorithm's work, counted for the roofline (bench.py) when work counters are on.
+__device__ __forceinline__ unsigned ref_moment_terms(const FitTable& T, double x) {
+  if (T.K > 0) return static_cast<unsigned>(T.K);
+  int s = 0;
+  for (int i = 1; i < T.nseg; ++i)
+    if (x >= T.seg[i].x0) s = i;
+  return static_cast<unsigned>(T.seg[s].m_mom);
+}
+__device__ __forceinline__ unsigned ref_norm_terms(const FitTable& T, double x) {
+  if (T.K > 0) return static_cast<unsigned>(T.K);
+  int s = 0;
+  for (int i = 1; i < T.nseg; ++i)
+    if (x >= T.seg[i].x0) s = i;
+  return static_cast<unsigned>(T.seg[s].m_norm);
+}
+
 // ---------------------------------------------------------------------------- building
 
 // Neumaier-compensated accumulator

@@ -248,6 +248,7 @@ __device__ __forceinline__ bool model_mean_slope(const ModelFns& M, double x, in
                                                  Work& wk) {
   if (M.table) {
     ++wk.evals;
+    wk.eval_terms += ref_moment_terms(M.T, x);
     fit_mean_slope(M.T, x, mean, slope);
     return true;
   }
@@ -261,6 +262,7 @@ __device__ __forceinline__ bool model_mean_slope(const ModelFns& M, double x, in
 __device__ __forceinline__ double model_mean(const ModelFns& M, double x, int lane, bool& ok, Work& wk) {
   if (M.table) {
     ++wk.evals;
+    wk.eval_terms += ref_moment_terms(M.T, x);
     ok = true;
     return fit_mean(M.T, x);
   }
