@@ -690,6 +690,26 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // largest u and accepted when the cdf entry below lies under its smallest u.  A replicate with
 // an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
+constexpr int kCutTabBits = 10;  // the cut table: one entry per 2^22-wide range of staged words
+
+// The cut table of a sampling table: entry i covers the words t in [i 2^22, (i+1) 2^22).  With
+// the exact cuts T_j (u > cdf[j] <=> t < T_j, t = T_j undecided), a range holding no cut decides
+// the value 1 + #{j : T_j > t} of all its words: the entry is the count increment 1 << 8(v-1)
+// for v <= 4, and 0 (queue for the exact search) for v = 5 or a range holding a cut.
+__device__ __forceinline__ void build_cut_table(uint32_t* tab, const uint32_t tcut[4]) {
+  for (int i = threadIdx.x; i < (1 << kCutTabBits); i += blockDim.x) {
+    const uint32_t lo = static_cast<uint32_t>(i) << (32 - kCutTabBits);
+    const uint32_t hi = lo + ((1u << (32 - kCutTabBits)) - 1u);
+    int c = 0;
+    bool cut = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      c += tcut[j] > hi;
+      cut |= tcut[j] >= lo && tcut[j] <= hi;
+    }
+    tab[i] = (cut || c == 4) ? 0u : (1u << (8 * c));
+  }
+}
 constexpr int kPreMaxN = 65535;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
 constexpr int kDenseMaxK = 1024;       // finite supports kept as dense counts above the head
 constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
@@ -705,8 +725,9 @@ struct DrawRowOut {
 // word was undecided: the caller redraws the row with kStaged = false).
 template <bool kStaged, typename BinT>
 __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, const uint32_t* __restrict__ urow,
-                                         const uint16_t* __restrict__ guide, BinT* bins, void* qmem, uint32_t* dense,
-                                         uint16_t* tail, uint16_t* head, DrawRowOut& o, int lane) {
+                                         const uint16_t* __restrict__ guide, const uint32_t* __restrict__ ctab,
+                                         BinT* bins, void* qmem, uint32_t* dense, uint16_t* tail, uint16_t* head,
+                                         DrawRowOut& o, int lane) {
   using Q = typename std::conditional<kStaged, uint32_t, double>::type;
   Q* queue = reinterpret_cast<Q*>(qmem);
   const bool two = a.guide_levels == 2;
@@ -717,7 +738,8 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   if (!kStaged) stream_key(a.seed, a.rep, idx, k0, k1);
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0, m = 0;
-  uint32_t g0 = 0, g1 = 0, g2 = 0;  // this lane's #{u > h_j}, j < 3
+  uint32_t acc = 0;          // this lane's counts of the values 1..4, 8-bit fields (flushed below)
+  uint32_t acc02 = 0, acc13 = 0;  // ... accumulated in 16-bit fields
   uint32_t amb = 0;                         // staged: some word undecided
   int qn = 0;                               // queued draws (warp-uniform)
   // one queued draw per lane: value by guide + search, then bin / tail
@@ -760,48 +782,40 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   // staged rows: the next block's 16-byte load is issued before this block is used
   uint4 p = make_uint4(0u, 0u, 0u, 0u);
   if (kStaged && lane < nb) p = __ldcs(reinterpret_cast<const uint4*>(urow) + lane);
-  uint32_t qtot = 0;  // words pushed (warp-uniform): #{u > h_3}
-  // one step: lane b's block of 4 draws; kMasked for the last step (words past n count nowhere:
-  // value 1 is n - #{u > h_0})
+  // one step: lane b's block of 4 draws.  A word's top 10 bits index ctab: the count increment
+  // of its value 1..4 (1 << 8(v-1)), or 0 = queue it (value above 4, or a cut inside the bin);
+  // kMasked for the last step (words past n count nowhere)
   auto step = [&](int b, auto masked) {
+    uint32_t t4[4];
     Q w4[4];
     if (kStaged) {
-      w4[0] = p.x;
-      w4[1] = p.y;
-      w4[2] = p.z;
-      w4[3] = p.w;
+      t4[0] = p.x;
+      t4[1] = p.y;
+      t4[2] = p.z;
+      t4[3] = p.w;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) w4[w] = t4[w];
       p = b + 32 < nb ? __ldcs(reinterpret_cast<const uint4*>(urow) + b + 32) : make_uint4(0u, 0u, 0u, 0u);
     } else {
       const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
 #pragma unroll
-      for (int w = 0; w < 4; ++w) w4[w] = uniform_open_closed(r.w[w]);
-    }
-    if (decltype(masked)::value) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-        if (4 * b + w >= n) w4[w] = kStaged ? Q(0xffffffffu) : Q(0);
+      for (int w = 0; w < 4; ++w) {
+        t4[w] = static_cast<uint32_t>(r.w[w] >> 32);
+        w4[w] = uniform_open_closed(r.w[w]);
+      }
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      bool big;
-      if (kStaged) {
-        const uint32_t t = static_cast<uint32_t>(w4[w]);
-        inc_if_lt(g0, t, a.tcut[0]);
-        inc_if_lt(g1, t, a.tcut[1]);
-        inc_if_lt(g2, t, a.tcut[2]);
-        flag_if_any_eq(amb, t, a.tcut[0], a.tcut[1], a.tcut[2], a.tcut[3]);
-        big = t < a.tcut[3];
-      } else {
-        const double u = static_cast<double>(w4[w]);
-        g0 += u > a.cdf_head[0];
-        g1 += u > a.cdf_head[1];
-        g2 += u > a.cdf_head[2];
-        big = u > a.cdf_head[3];
+      uint32_t e = ctab[t4[w] >> (32 - kCutTabBits)];
+      bool big = e == 0u;
+      if (decltype(masked)::value && 4 * b + w >= n) {
+        e = 0u;
+        big = false;
       }
+      acc += e;
       const unsigned bm = __ballot_sync(0xffffffffu, big);
       if (big) queue[qn + __popc(bm & lt)] = w4[w];
       qn += __popc(bm);
-      qtot += __popc(bm);
     }
     __syncwarp();
     while (qn >= 32) {
@@ -811,19 +825,30 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       resolve(q, true);
     }
   };
+  auto flush = [&]() {  // 8-bit fields hold <= 63 steps x 4 words
+    acc02 += acc & 0x00ff00ffu;
+    acc13 += (acc >> 8) & 0x00ff00ffu;
+    acc = 0u;
+  };
   const int full = (n >> 2) & ~31;  // blocks in steps whose 4 x 32 words are all in the sample
   int b0 = 0;
-  for (; b0 < full; b0 += 32) step(b0 + lane, std::false_type{});
+  for (int chunk = 0; b0 < full; b0 += 32) {
+    step(b0 + lane, std::false_type{});
+    if (++chunk == 63) {
+      flush();
+      chunk = 0;
+    }
+  }
   for (; b0 < nb; b0 += 32) step(b0 + lane, std::true_type{});
+  flush();
   if (qn) {
     const bool ok = lane < qn;
     const Q q = ok ? queue[lane] : Q(0);
     __syncwarp();
     resolve(q, ok);
   }
-  // counts of 1..4 from the threshold counts
-  const uint32_t c01 = warp_sum_u32(g0 | (g1 << 16)), c2 = warp_sum_u32(g2);  // n < 2^16
-  const uint32_t G0 = c01 & 0xffffu, G1 = c01 >> 16, G2 = c2, G3 = qtot;
+  // counts of 1..4 counted by the cut table (the queued ones are in the bins)
+  const uint32_t c02 = warp_sum_u32(acc02), c13 = warp_sum_u32(acc13);  // n < 2^16
   __syncwarp();
   // head[k - 1] = count of value k: lane l sums the 32 lane columns of k = l + 1 and l + 33
   uint32_t hc0 = 0, hc1 = 0;
@@ -843,12 +868,9 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     }
   }
   __syncwarp();
-  if (lane == 0) hc0 = static_cast<uint32_t>(n) - G0;
-  if (lane == 1) hc0 = G0 - G1;
-  if (lane == 2) hc0 = G1 - G2;
-  if (lane == 3) hc0 = G2 - G3;
-  for (int i = lane; i < (kKsHead - 4) * 8 * static_cast<int>(sizeof(BinT)); i += 32)
-    reinterpret_cast<uint32_t*>(bins + 5 * 32)[i] = 0u;
+  if (lane < 4) hc0 += ((lane & 1) ? c13 : c02) >> (16 * (lane >> 1)) & 0xffffu;
+  for (int i = lane; i < kKsHead * 8 * static_cast<int>(sizeof(BinT)); i += 32)
+    reinterpret_cast<uint32_t*>(bins + 32)[i] = 0u;
   const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
   if (dense) {  // counts of kKsHead+1..K into the row's tail slot (u32), the warp histogram reset
     __syncwarp();
@@ -883,7 +905,8 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using BinT = typename std::conditional<kWide, uint16_t, uint8_t>::type;
-  unsigned char* wbase = smem + guide_bytes + warp * (draw_warp_bytes(kWide) + a.dense_words * 4);
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + guide_bytes);
+  unsigned char* wbase = smem + guide_bytes + (4 << kCutTabBits) + warp * (draw_warp_bytes(kWide) + a.dense_words * 4);
   // lane-private counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
   // most one queued draw per pop and there are <= n/32 + 1 pops (u8 up to kNarrowBinsMaxN)
   BinT* bins = reinterpret_cast<BinT*>(wbase);
@@ -891,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   uint32_t* dense = a.dense_words ? reinterpret_cast<uint32_t*>(wbase + draw_warp_bytes(kWide)) : nullptr;
   for (int i = lane; i < a.dense_words; i += 32) dense[i] = 0u;
   load_guide(guide, a.guide, a.guide_levels);
+  build_cut_table(ctab, a.tcut);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -902,13 +926,13 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
     DrawRowOut o;
     bool done = false;
     if (a.ubuf) {
-      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, bins, queue, dense, tail,
-                            head, o, lane);
+      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, ctab, bins, queue, dense,
+                            tail, head, o, lane);
       staged += a.n;
       redrawn += !done;
     }
     if (!done) {
-      draw_row<false>(a, idx, nullptr, guide, bins, queue, dense, tail, head, o, lane);
+      draw_row<false>(a, idx, nullptr, guide, ctab, bins, queue, dense, tail, head, o, lane);
       philox += a.n;
     }
     if (lane == 0) {

@@ -561,7 +561,8 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
                                              size_t(zks::retry_warp_bytes(a.hist_words, a.vals_stride)))));
     auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
     auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
-    const size_t dsmem = guide_bytes + size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(a.dense_words) * 4);
+    const size_t dsmem = guide_bytes + (size_t(4) << zks::kCutTabBits) +
+                         size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(a.dense_words) * 4);
     const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
     const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
     int dper = 0, fper = 0;
