@@ -752,7 +752,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       ur = q;
     }
     uint32_t lo, hi;
-    guide_bracket(ur, guide, two, lo, hi);
+    guide_bracket_fine(ur, guide, a.guide_fine, two, lo, hi);
     if (!ok) hi = lo;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
                                                                  uint32_t* min_out, uint32_t* max_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
-  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
+  const int guide_bytes = round_up(kGuideLevel * 2, 16);  // level 1 only (level 2: the fine one, global)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using BinT = typename std::conditional<kWide, uint16_t, uint8_t>::type;
   uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + guide_bytes);
@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   void* queue = wbase + (kKsHead + 1) * 32 * sizeof(BinT);
   uint32_t* dense = a.dense_words ? reinterpret_cast<uint32_t*>(wbase + draw_warp_bytes(kWide)) : nullptr;
   for (int i = lane; i < a.dense_words; i += 32) dense[i] = 0u;
-  load_guide(guide, a.guide, a.guide_levels);
+  load_guide(guide, a.guide, 1);
   build_cut_table(ctab, a.tcut);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();

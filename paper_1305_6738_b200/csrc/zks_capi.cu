@@ -309,7 +309,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
   const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
-  cudaError_t err = cudaMallocAsync(&mem, cdf_slots * sizeof(double) + 2 * zks::kGuideLevel * sizeof(uint16_t), e->stream);
+  cudaError_t err = cudaMallocAsync(&mem, cdf_slots * sizeof(double) + zks::kGuideEntries * sizeof(uint16_t), e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
     t->guide = reinterpret_cast<uint16_t*>(t->cdf + cdf_slots);
@@ -329,7 +329,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   if (err == cudaSuccess) {
     {
       Timed tm(e, ZKS_KERNEL_OTHER);
-      zks::guide_kernel<<<(2 * zks::kGuideLevel + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
+      zks::guide_kernel<<<(zks::kGuideEntries + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
       err = launched(e);
     }
   }
@@ -411,6 +411,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   zks::ReplicateArgs a;
   a.cdf = t->cdf;
   a.guide = t->guide;
+  a.guide_fine = t->guide + 2 * zks::kGuideLevel;
   for (int j = 0; j < 4; ++j) {
     a.cdf_head[j] = t->head[j];
     a.tcut[j] = t->tcut[j];
@@ -561,7 +562,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
                                              size_t(zks::retry_warp_bytes(a.hist_words, a.vals_stride)))));
     auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
     auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
-    const size_t dsmem = guide_bytes + (size_t(4) << zks::kCutTabBits) +
+    const size_t dsmem = zks::round_up(zks::kGuideLevel * 2, 16) + (size_t(4) << zks::kCutTabBits) +
                          size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(a.dense_words) * 4);
     const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
     const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);

@@ -30,12 +30,17 @@ constexpr int kGuide = 1 << kGuideLog2;
 constexpr int kGuideLevel = kGuide + 2;     // entries per guide level
 // second level: the top 2^-5 of u in 4096 bins of 2^-17 (heavy tails: k ranges per bin stay short)
 constexpr double kGuide2Start = 0.96875;    // 1 - 2^-5
-constexpr double kGuide2Scale = 131072.0;   // 2^17
+constexpr double kGuide2Scale = 131072.0;   // 2^17: level 2 (shared memory), the top 2^-5 in G bins
+constexpr int kGuideFineBins = 1 << 16;     // fine level 2 (global memory): the top 2^-5 in 2^16 bins
+constexpr int kGuideFineLevel = kGuideFineBins + 2;
+constexpr double kGuideFineScale = 2097152.0;  // 2^21
+constexpr int kGuideEntries = 2 * kGuideLevel + kGuideFineLevel;  // level 1, level 2, fine level 2
 constexpr double kLn2 = 0.69314718055994530942;  // math.log(2.0)
 
 struct ReplicateArgs {
   const double* cdf;
-  const uint16_t* guide;  // guide_levels x kGuideLevel entries
+  const uint16_t* guide;      // levels 1 and 2 (2 x kGuideLevel entries; copied to shared memory)
+  const uint16_t* guide_fine;  // fine level 2 (kGuideFineLevel entries, read from global memory / L2)
   const double* logs;
   uint32_t L;      // draw-table length: K or 65535
   int32_t K;       // finite support bound, 0 = unbounded
@@ -84,6 +89,18 @@ __device__ __forceinline__ void guide_bracket(double u, const uint16_t* guide, b
   const bool up = two && u >= kGuide2Start;
   const int j = up ? static_cast<int>((u - kGuide2Start) * kGuide2Scale) : static_cast<int>(u * static_cast<double>(kGuide));
   const uint16_t* g = guide + (up ? kGuideLevel : 0) + j;
+  lo = g[0];
+  hi = g[1];
+}
+
+// the same with the fine level 2 (65536 bins, global memory): a bracket of ~1 entry for heavy
+// tails, where the shared level 2 leaves several search steps -- for the queued resolution of
+// draw_stats_kernel, whose lanes all search at once
+__device__ __forceinline__ void guide_bracket_fine(double u, const uint16_t* guide, const uint16_t* __restrict__ fine,
+                                                   bool two, uint32_t& lo, uint32_t& hi) {
+  const bool up = two && u >= kGuide2Start;
+  const int j = up ? static_cast<int>((u - kGuide2Start) * kGuideFineScale) : static_cast<int>(u * static_cast<double>(kGuide));
+  const uint16_t* g = up ? fine + j : guide + j;
   lo = g[0];
   hi = g[1];
 }
@@ -422,18 +439,20 @@ __global__ void normaliser_kernel(double g, int K, const double* __restrict__ lo
   if (threadIdx.x == 0) *out = v;
 }
 
-// level 0: guide[j] = lower_bound(cdf, j / G), j = 0..G; level 1: lower_bound(cdf, 1 - 2^-5 + j 2^-17);
-// each level ends with L
+// level 1: guide[j] = lower_bound(cdf, j / G), j = 0..G; level 2: lower_bound(cdf,
+// 1 - 2^-5 + j 2^-17), j = 0..G; fine level 2: lower_bound(cdf, 1 - 2^-5 + j 2^-21),
+// j = 0..kGuideFineBins; each level ends with L
 __global__ void guide_kernel(const double* __restrict__ cdf, uint32_t L, uint16_t* guide) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * kGuideLevel) return;
-  const int level = t / kGuideLevel, j = t % kGuideLevel;
-  if (j == kGuide + 1) {
+  if (t >= kGuideEntries) return;
+  const int level = t < kGuideLevel ? 0 : t < 2 * kGuideLevel ? 1 : 2;
+  const int j = t - level * kGuideLevel;
+  if (j == (level == 2 ? kGuideFineBins : kGuide) + 1) {
     guide[t] = static_cast<uint16_t>(L);
     return;
   }
-  const double u = level ? kGuide2Start + static_cast<double>(j) / kGuide2Scale
-                         : static_cast<double>(j) / static_cast<double>(kGuide);
+  const double u = level == 0 ? static_cast<double>(j) / static_cast<double>(kGuide)
+                              : kGuide2Start + static_cast<double>(j) / (level == 1 ? kGuide2Scale : kGuideFineScale);
   uint32_t lo = 0, hi = L;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
