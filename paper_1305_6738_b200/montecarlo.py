@@ -109,7 +109,15 @@ def _engine():
     return get_engine()
 
 
+_PENDING: dict = {}  # (device, gamma, K) -> future of a host sampling CDF being built (_prefetch_tables)
+_POOL = None
+
+
 def _table(eng, config: SimulationConfig):
+    fut = _PENDING.pop((eng.device, float(config.gamma), config.support.k), None)
+    if fut is not None:
+        cdf = fut.result()
+        return eng.table(config.gamma, config.support.k, lambda: cdf)
     return eng.table(config.gamma, config.support.k, lambda: sampling_cdf(config.gamma, config.support))
 
 
@@ -356,22 +364,23 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
 
 
 def _prefetch_tables(eng, configs) -> None:
-    """Build the host sampling CDFs a sweep still lacks on a thread pool (numpy releases the
-    GIL), then upload them: the first cells do not wait for every table to be built serially."""
+    """Start building the host sampling CDFs a sweep still lacks on a thread pool (numpy releases
+    the GIL); _table() takes each one when its first cell is enqueued, so device work starts
+    after the first table instead of after all of them."""
+    global _POOL
     missing = {}
     for cfg in configs:
         key = (float(cfg.gamma), cfg.support.k)
-        if key not in missing and not eng.has_table(*key):
+        if key not in missing and not eng.has_table(*key) and (eng.device, *key) not in _PENDING:
             missing[key] = cfg
     if len(missing) < 2:
         return
-    from concurrent.futures import ThreadPoolExecutor
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
 
-    cfgs = list(missing.values())
-    with ThreadPoolExecutor(max_workers=min(len(cfgs), os.cpu_count() or 1, 16)) as ex:
-        cdfs = list(ex.map(lambda c: sampling_cdf(c.gamma, c.support), cfgs))
-    for cfg, cdf in zip(cfgs, cdfs):
-        eng.table(cfg.gamma, cfg.support.k, lambda cdf=cdf: cdf)
+        _POOL = ThreadPoolExecutor(max_workers=min(os.cpu_count() or 1, 16))
+    for key, cfg in missing.items():
+        _PENDING[(eng.device, *key)] = _POOL.submit(sampling_cdf, cfg.gamma, cfg.support)
 
 
 def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
