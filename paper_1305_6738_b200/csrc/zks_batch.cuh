@@ -681,14 +681,16 @@ __global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint
 // of the values 1..kKsHead and the list of values above it -- so fit_ks_kernel never touches the
 // n draws again.  Draws from Philox, or from a staged sweep buffer of 32-bit words (a.ubuf).
 //
-// Values 1..4 are counted without a search: with h = cdf[0..3] in the kernel parameters,
-// #{u > h_j} over the sample gives the counts by differences (lower_bound semantics; h_j = +inf
-// from L-1 on clamps to L, distribution.py:200-201).  On staged words the test is u > h_j <=>
-// t < a.tcut[j] (exact unless t == tcut[j]).  Draws above h_3 -- 5 % of them at gamma = 2.5,
-// 36 % at 1.5 -- are pushed onto a warp queue and resolved 32 at a time by the guide + cdf
-// search with every lane busy, so divergence costs nothing; a staged word is searched with its
-// largest u and accepted when the cdf entry below lies under its smallest u.  A replicate with
-// an undecided staged word is redrawn from Philox (exact), about one in 70 at n = 1000.
+// Values 1..4 are counted without a search: with h = cdf[0..3] and the exact cuts T_j of the
+// 32-bit words (u > h_j <=> t < T_j, t = x >> 32 for staged and Philox words alike; h_j = +inf
+// from L-1 on clamps to L, distribution.py:200-201), a per-block table indexed by a word's top
+// 10 bits holds the count increment of the value every word of that 2^22-wide range takes, or
+// 0 when the range holds a cut or lies above h_3.  Those words -- 5 % of them at gamma = 2.5,
+// 36 % at 1.5, plus the rare ranges with a cut -- are pushed onto a warp queue and resolved 32 at
+// a time by the guide + cdf search with every lane busy, so divergence costs nothing; a staged
+// word is searched with its largest u and accepted when the cdf entry below lies under its
+// smallest u.  A replicate with an undecided staged word is redrawn from Philox (exact), about
+// one in 200 at n = 1000.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
 constexpr int kCutTabBits = 10;  // the cut table: one entry per 2^22-wide range of staged words
 
