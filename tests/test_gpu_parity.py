@@ -141,6 +141,8 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (None, 1.6, 9000, 3, 0, 24),  # two-kernel path with u16 draw bins
         (1000, 1.0, 5000, 2, 0, 24),
         (None, 1.9, 40000, 4, 0, 8),  # two-kernel path near its u16 limit
+        (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
+        (5, 2.0, 300, 7, 1, 64),
     ],
 )
 def test_replicates_match_oracle(zk, mle_mode, K, gamma, n, seed, rep, count):
