@@ -297,7 +297,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     cfg0 = plans[0].config
     n = cfg0.n
     staged = _STAGE_MIN_N <= n <= _STAGE_MAX_N
-    if len(plans) < 2 or (gather is not None and not staged):
+    if len(plans) < 2:
         for plan in plans:
             _enqueue_cell(eng, plan, shard=shard, gather=gather, kernel_events=kernel_events)
         return
@@ -352,11 +352,12 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
                             + ((out.st[:total], plan.worst[rep : rep + 1]) if i == 0 else ())
                             for i in range(0, len(ranks), 16))
                 continue
+            # multi-GPU: this rank's statuses only (the worst is all-reduced later); the gathered
+            # index-ordered KS array of every cell stays alive for the row's batched selection
             if stop > first:
                 plan.worst[rep] = out.st[first:stop].max()
-            ks = gather(out.ks)[:total]  # the gather buffer is reused: select before the next cell
-            for i in range(0, len(ranks), 16):
-                eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+            ks = gather(out.ks, fresh=True)[:total]
+            jobs.extend((ks, ranks[i : i + 16], plan.quantiles[rep, i : i + 16]) for i in range(0, len(ranks), 16))
         for i0 in range(0, len(ranks), 16):  # equal rank counts per launch
             eng.select_many([j for j in jobs if j[1] == ranks[i0 : i0 + 16]])
     for plan in plans:

@@ -54,11 +54,15 @@ class ShardGather:
         self.chunk = -(-total // world)
         self.out = None
 
-    def __call__(self, local_full):
+    def __call__(self, local_full, fresh: bool = False):
+        """All-gathered copy of ``local_full``; into a reused buffer, or a new one (``fresh``) when
+        several gathered arrays must stay alive (a sweep row's batched selection)."""
         import torch
         import torch.distributed as dist
 
         need = self.chunk * self.world
+        if fresh:
+            self.out = None
         if self.out is None or self.out.numel() < need or self.out.device != local_full.device:
             self.out = torch.empty(need, dtype=local_full.dtype, device=local_full.device)
         start = self.rank * self.chunk

@@ -8,6 +8,8 @@ Tiers (BASELINE.json north_star):
      within MC error.
 All calls go through the C ABI (libzks_b200.so).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -340,3 +342,28 @@ def test_cells_on_two_streams_match_sequential(zk):
     for a, b in zip(seq, par):
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+def test_parallel_build_table_single_rank_matches(zk):
+    # the multi-GPU path (shards, NCCL all-gather of every cell's KS array, batched selection
+    # of the gathered arrays, all-reduced worst status) on a one-rank NCCL group equals the
+    # single-GPU table bit for bit
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_6738_b200 import parallel
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        kw = dict(ns=(20, 300), gammas=(1.7, 2.4), support=zk.Support.unbounded(), base_seed=9, replicates=2000,
+                  repetitions=2)
+        assert parallel.build_table(**kw).cells == zk.build_table(**kw).cells
+    finally:
+        dist.destroy_process_group()
