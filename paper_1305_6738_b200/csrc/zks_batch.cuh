@@ -928,6 +928,12 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
     DrawRowOut o;
     bool done = false;
     if (a.ubuf) {
+      // the warp's next row into L2 while this one is drawn (its loads then wait on L2, not HBM)
+      if (i + warps < a.count) {
+        const char* next = reinterpret_cast<const char*>(a.ubuf + (idx + warps - a.ubuf_first) * a.ubuf_stride);
+        for (int64_t off = 128 * lane; off < a.n * 4; off += 128 * 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(next + off));
+      }
       done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, ctab, bins, queue, dense,
                             tail, head, o, lane);
       staged += a.n;
