@@ -3,8 +3,8 @@
 
 Workload ("config2"): K = inf, gamma = 1.5..3.5 step 0.1 (21 values) x n in {10, 20, 50, 100,
 500, 1000} = 126 cells, base_seed = 1, one repetition, R = 10^6 replicates per cell and GPU
-(weak scaling: at N GPUs each cell has N*10^6 replicates, sharded by index, KS all-gathered
-over NCCL, exact quantiles selected on every rank).  One step = the whole 126-cell sweep:
+(weak scaling: at N GPUs each cell has N*10^6 replicates, sharded by index; the exact
+quantiles are selected across the shards with NCCL all-reduces of radix digit histograms).  One step = the whole 126-cell sweep:
 per replicate sample -> MLE refit -> KS, then the 4 order-statistic cutoffs per cell.
 
   value        device time of the sweep with draw tables resident, L2 flushed between steps
@@ -292,7 +292,7 @@ def run_b200(args, world, rank, local):
                for g in GAMMAS for n in NS]
     ncells = len(configs)
     shard = parallel.shard_bounds(R, world, rank) if world > 1 else None
-    gather = parallel.ShardGather(R, world, rank) if world > 1 else None
+    reduce = parallel.histogram_reducer() if world > 1 else None
     mc._slab(eng, parallel.padded_size(R, world))
     dev = torch.device("cuda", local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -303,7 +303,7 @@ def run_b200(args, world, rank, local):
 
     def sweep():
         plans = [mc._CellPlan(cfg) for cfg in configs]
-        mc._enqueue_plans(eng, plans, shard=shard, gather=gather)
+        mc._enqueue_plans(eng, plans, shard=shard, reduce=reduce)
         return plans
 
     # warm-up (also builds and uploads the 21 draw tables)

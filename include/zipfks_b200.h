@@ -133,6 +133,21 @@ int zks_select_ranks_batch(zks_engine* engine, const double* const* values_dev, 
                            int32_t narrays, const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
                            const uint8_t* const* status_dev, uint8_t* const* worst_dev);
 
+/* The batched selection in steps, for arrays sharded over GPUs: each GPU passes its shards
+ * values_dev[a] (counts[a] keys) of the full arrays (global_counts[a] keys; ranks refer to
+ * those).  zks_select_dist_begin resets the state; then for pass = 0..7:
+ * zks_select_dist_count ADDS this GPU's digit counts to hist_dev (uint32, [narrays * nranks][256],
+ * zeroed by the caller), the caller sums hist_dev over the GPUs (e.g. an NCCL all-reduce), and
+ * zks_select_dist_pick chooses the digits from the sum; zks_select_dist_end writes out_dev[a][i]
+ * (identical on every GPU) and this GPU's worst status.  Key work is proportional to the shard.
+ * Asynchronous; one selection at a time per engine. */
+int zks_select_dist_begin(zks_engine* engine, const double* const* values_dev, const int64_t* counts,
+                          const int64_t* global_counts, int32_t narrays, const int64_t* ranks_host, int32_t nranks,
+                          double* const* out_dev, const uint8_t* const* status_dev, uint8_t* const* worst_dev);
+int zks_select_dist_count(zks_engine* engine, int32_t pass, uint32_t* hist_dev);
+int zks_select_dist_pick(zks_engine* engine, int32_t pass, const uint32_t* hist_dev);
+int zks_select_dist_end(zks_engine* engine);
+
 /* Same selection, asynchronous: the selected values land in out_dev[0..nranks) (device). */
 int zks_select_ranks_async(zks_engine* engine, const double* values_dev, int64_t count, const int64_t* ranks_host,
                            int32_t nranks, double* out_dev);

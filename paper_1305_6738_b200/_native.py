@@ -36,6 +36,10 @@ EXPORTS = (
     "zks_select_ranks",
     "zks_select_ranks_async",
     "zks_select_ranks_batch",
+    "zks_select_dist_begin",
+    "zks_select_dist_count",
+    "zks_select_dist_pick",
+    "zks_select_dist_end",
     "zks_normaliser",
     "zks_stream_uniforms",
     "zks_draw",
@@ -113,6 +117,10 @@ def load() -> ctypes.CDLL:
     lib.zks_select_ranks.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_async.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp, dp, dp]
+    lib.zks_select_dist_begin.argtypes = [vp, dp, dp, dp, i32, dp, i32, dp, dp, dp]
+    lib.zks_select_dist_count.argtypes = [vp, i32, dp]
+    lib.zks_select_dist_pick.argtypes = [vp, i32, dp]
+    lib.zks_select_dist_end.argtypes = [vp]
     lib.zks_normaliser.argtypes = [vp, ctypes.c_double, i32, dp]
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]

@@ -81,6 +81,9 @@ struct zks_engine {
   int select_blocks = 0;            // resident grid of the cooperative selection kernel
   void* cand = nullptr;             // selection candidates (keys matching a 16-bit prefix)
   size_t cand_bytes = 0;
+  zks::SelectBatch dist{};          // the distributed selection in progress (zks_select_dist_*)
+  bool dist_active = false;
+  int dist_blocks = 1;
   // per-kernel timing (zks_engine_set_timing): event pairs around launches on the engine stream
   bool timing = false;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> timed;
@@ -631,35 +634,32 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   return ZKS_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
-                           const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
-                           const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
+// the batch of a selection call (validation, candidate buffer); `global_counts` (optional) are
+// the full arrays' lengths the ranks refer to when this GPU holds shards
+int select_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
+                 const int64_t* ranks_host, int32_t nranks, double* const* out_dev, const uint8_t* const* status_dev,
+                 uint8_t* const* worst_dev, const int64_t* global_counts, zks::SelectBatch* out) {
   if (!e || !values_dev || !counts || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
   if (narrays < 1 || narrays > zks::kSelMaxArrays)
     return fail(ZKS_EINVAL, "narrays %d outside [1, %d]", narrays, zks::kSelMaxArrays);
   if (nranks < 1 || nranks > zks::kMaxRanks) return fail(ZKS_EINVAL, "nranks %d outside [1, %d]", nranks, zks::kMaxRanks);
-  zks::SelectBatch B;
+  zks::SelectBatch& B = *out;
   std::memset(&B, 0, sizeof B);
   B.narrays = narrays;
   B.nr = nranks;
-  int64_t most = 0;
   for (int a = 0; a < narrays; ++a) {
-    if (!values_dev[a] || !out_dev[a]) return fail(ZKS_EINVAL, "NULL array %d", a);
-    if (counts[a] < 1) return fail(ZKS_EINVAL, "cannot take quantiles of an empty array");
+    const int64_t full = global_counts ? global_counts[a] : counts[a];
+    if (!out_dev[a] || (counts[a] > 0 && !values_dev[a])) return fail(ZKS_EINVAL, "NULL array %d", a);
+    if (full < 1 || counts[a] < 0 || counts[a] > full) return fail(ZKS_EINVAL, "cannot take quantiles of an empty array");
     B.keys[a] = reinterpret_cast<const unsigned long long*>(values_dev[a]);
     B.count[a] = counts[a];
     B.out[a] = out_dev[a];
     B.status[a] = status_dev ? status_dev[a] : nullptr;
     B.worst[a] = (status_dev && status_dev[a] && worst_dev) ? worst_dev[a] : nullptr;
-    most = std::max(most, counts[a]);
     for (int i = 0; i < nranks; ++i) {
       const int64_t r = ranks_host[int64_t(a) * nranks + i];
-      if (r < 0 || r >= counts[a])
-        return fail(ZKS_EINVAL, "rank %lld out of range for %lld values", (long long)r, (long long)counts[a]);
+      if (r < 0 || r >= full)
+        return fail(ZKS_EINVAL, "rank %lld out of range for %lld values", (long long)r, (long long)full);
       B.rank[a][i] = static_cast<unsigned long long>(r);
     }
   }
@@ -670,10 +670,26 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
     if (e->cand) ZKS_CUDA(cudaFreeAsync(e->cand, e->stream));
     e->cand = nullptr;
     e->cand_bytes = 0;
-    ZKS_CUDA(cudaMallocAsync(&e->cand, size_t(total) * 8, e->stream));
-    e->cand_bytes = size_t(total) * 8;
+    ZKS_CUDA(cudaMallocAsync(&e->cand, std::max<size_t>(size_t(total) * 8, 8), e->stream));
+    e->cand_bytes = std::max<size_t>(size_t(total) * 8, 8);
   }
   B.cand = static_cast<unsigned long long*>(e->cand);
+  return ZKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
+                           const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
+                           const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
+  zks::SelectBatch B;
+  const int rc = select_batch(e, values_dev, counts, narrays, ranks_host, nranks, out_dev, status_dev, worst_dev,
+                              nullptr, &B);
+  if (rc) return rc;
+  int64_t most = 0;
+  for (int a = 0; a < narrays; ++a) most = std::max<int64_t>(most, counts[a]);
   // one cooperative launch: every block resident (grid barriers between the radix passes)
   if (e->select_blocks == 0) {
     int per = 0;
@@ -696,6 +712,64 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
 int zks_select_ranks_async(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,
                            int32_t nranks, double* out_dev) {
   return zks_select_ranks_batch(e, &values_dev, &count, 1, ranks_host, nranks, &out_dev, nullptr, nullptr);
+}
+
+int zks_select_dist_begin(zks_engine* e, const double* const* values_dev, const int64_t* counts,
+                          const int64_t* global_counts, int32_t narrays, const int64_t* ranks_host, int32_t nranks,
+                          double* const* out_dev, const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
+  if (!global_counts) return fail(ZKS_EINVAL, "NULL argument");
+  zks::SelectBatch B;
+  const int rc = select_batch(e, values_dev, counts, narrays, ranks_host, nranks, out_dev, status_dev, worst_dev,
+                              global_counts, &B);
+  if (rc) return rc;
+  e->dist = B;
+  e->dist_active = true;
+  int64_t most = 0;
+  for (int a = 0; a < narrays; ++a) most = std::max<int64_t>(most, counts[a]);
+  e->dist_blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (most * narrays + 255) / 256)));
+  Timed tm(e, ZKS_KERNEL_SELECT);
+  zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->sel);
+  ZKS_CUDA(launched(e));
+  return ZKS_OK;
+}
+
+int zks_select_dist_count(zks_engine* e, int32_t pass, uint32_t* hist_dev) {
+  if (!e || !hist_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (!e->dist_active || pass < 0 || pass >= zks::kSelectPasses) return fail(ZKS_EINVAL, "no selection pass %d", pass);
+  ZKS_CUDA(cudaSetDevice(e->device));
+  Timed tm(e, ZKS_KERNEL_SELECT);
+  zks::select_count_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->sel, pass, hist_dev);
+  ZKS_CUDA(launched(e));
+  return ZKS_OK;
+}
+
+int zks_select_dist_pick(zks_engine* e, int32_t pass, const uint32_t* hist_dev) {
+  if (!e || !hist_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (!e->dist_active || pass < 0 || pass >= zks::kSelectPasses) return fail(ZKS_EINVAL, "no selection pass %d", pass);
+  ZKS_CUDA(cudaSetDevice(e->device));
+  {
+    Timed tm(e, ZKS_KERNEL_SELECT);
+    const int slots = e->dist.narrays * e->dist.nr;
+    zks::select_pick_kernel<<<(unsigned)((slots + 7) / 8), 256, 0, e->stream>>>(e->dist, e->sel, pass, hist_dev);
+    ZKS_CUDA(launched(e));
+  }
+  if (pass == 1) {
+    Timed tm(e, ZKS_KERNEL_SELECT);
+    zks::select_compact_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->sel);
+    ZKS_CUDA(launched(e));
+  }
+  return ZKS_OK;
+}
+
+int zks_select_dist_end(zks_engine* e) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  if (!e->dist_active) return fail(ZKS_EINVAL, "no selection in progress");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  e->dist_active = false;
+  Timed tm(e, ZKS_KERNEL_SELECT);
+  zks::select_out_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->sel);
+  ZKS_CUDA(launched(e));
+  return ZKS_OK;
 }
 
 int zks_select_ranks(zks_engine* e, const double* values_dev, int64_t count, const int64_t* ranks_host,

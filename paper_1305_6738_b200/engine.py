@@ -202,6 +202,38 @@ class Engine:
             _native.check(self.lib.zks_select_ranks_batch(self.handle, ptrs, counts.ctypes.data, len(part),
                                                           ranks.ctypes.data, nr, outs, sts, worst))
 
+    def select_dist(self, jobs, total: int, reduce) -> None:
+        """Batched selection over arrays sharded across processes: ``jobs`` as in select_many
+        with this process's shard of each array (``total`` values in all, which the ranks refer
+        to); ``reduce(t)`` must sum the device int32 tensor ``t`` over the processes in place
+        (e.g. torch.distributed.all_reduce).  Per pass: local digit counts, reduce, pick."""
+        torch = _torch()
+        jobs = list(jobs)
+        for j0 in range(0, len(jobs), 24):
+            part = jobs[j0 : j0 + 24]
+            nr = len(part[0][1])
+            ptrs = (ctypes.c_void_p * len(part))(*[j[0].data_ptr() if j[0].numel() else None for j in part])
+            outs = (ctypes.c_void_p * len(part))(*[j[2].data_ptr() for j in part])
+            sts = (ctypes.c_void_p * len(part))(*[j[3].data_ptr() if len(j) > 3 and j[3].numel() else None
+                                                  for j in part])
+            worst = (ctypes.c_void_p * len(part))(*[j[4].data_ptr() if len(j) > 3 else None for j in part])
+            counts = np.ascontiguousarray([j[0].numel() for j in part], dtype=np.int64)
+            totals = np.full(len(part), int(total), dtype=np.int64)
+            ranks = np.ascontiguousarray([list(j[1]) for j in part], dtype=np.int64)
+            if ranks.shape[1] != nr:
+                raise ValueError("select_dist: every job needs the same number of ranks")
+            self.bind_stream()
+            _native.check(self.lib.zks_select_dist_begin(self.handle, ptrs, counts.ctypes.data, totals.ctypes.data,
+                                                         len(part), ranks.ctypes.data, nr, outs, sts, worst))
+            hist = torch.empty(len(part) * nr * 256, dtype=torch.int32, device=part[0][2].device)
+            for p in range(8):
+                hist.zero_()
+                _native.check(self.lib.zks_select_dist_count(self.handle, p, hist.data_ptr()))
+                reduce(hist)
+                self.bind_stream()
+                _native.check(self.lib.zks_select_dist_pick(self.handle, p, hist.data_ptr()))
+            _native.check(self.lib.zks_select_dist_end(self.handle))
+
     def normaliser(self, gamma: float, support_k: int | None) -> float:
         out = ctypes.c_double()
         self.bind_stream()

@@ -237,13 +237,13 @@ class _CellPlan:
     host: object = None        # (quantiles, worst) copied to the host by _fetch_plans
 
 
-def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, gather=None,
+def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, reduce=None,
                   kernel_events: list | None = None) -> None:
-    """Queue every repetition of one cell: replicates -> (gather) -> selection, all async.
+    """Queue every repetition of one cell: replicates -> selection, all async.
 
-    ``shard`` = (first, stop) restricts this process to replicate indices [first, stop);
-    ``gather(slab_ks)`` must then return a device tensor whose first ``replicates`` entries are
-    the KS values of every index in order (the multi-GPU all-gather, parallel.py).
+    ``shard`` = (first, stop) restricts this process to replicate indices [first, stop); the
+    order statistics are then selected over every process's shard with ``reduce`` summing the
+    selection's digit histograms over the processes (NCCL all-reduce, parallel.py).
     """
     torch = _torch()
     cfg = plan.config
@@ -268,9 +268,12 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, ga
                 k1.record(stream)
                 kernel_events.append((k0, k1))
             plan.worst[rep] = slab.st[first:stop].max()
-        ks = slab.ks[:total] if gather is None else gather(slab.ks)[:total]
-        for i in range(0, len(ranks), 16):
-            eng.select_ranks(ks, ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+        if reduce is None:
+            for i in range(0, len(ranks), 16):
+                eng.select_ranks(slab.ks[:total], ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
+        else:
+            eng.select_dist([(slab.ks[first:stop], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
+                             for i in range(0, len(ranks), 16)], total, reduce)
     plan.finished.record(stream)
 
 
@@ -284,7 +287,7 @@ def _stage_key(cfg: SimulationConfig):
     return (cfg.support.k, cfg.n, cfg.base_seed, cfg.replicates, cfg.repetitions, cfg.quantiles)
 
 
-def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
+def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None) -> None:
     """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
@@ -299,7 +302,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
     staged = _STAGE_MIN_N <= n <= _STAGE_MAX_N
     if len(plans) < 2:
         for plan in plans:
-            _enqueue_cell(eng, plan, shard=shard, gather=gather, kernel_events=kernel_events)
+            _enqueue_cell(eng, plan, shard=shard, reduce=reduce, kernel_events=kernel_events)
         return
     total = cfg0.replicates
     first, stop = shard if shard is not None else (0, total)
@@ -345,21 +348,20 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_
                 if kernel_events is not None:
                     k1.record(stream)
                     kernel_events.append((k0, k1))
+        # the row's cells in batched selections; the first rank chunk also takes the worst status
+        # (multi-GPU: over this rank's shard, digit histograms summed by `reduce`; the worst
+        # status is this rank's, all-reduced by the caller)
         jobs = []
         for plan, out in zip(plans, outs):
-            if gather is None:  # the row's cells in batched launches; the first also takes the worst status
-                jobs.extend((out.ks[:total], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
-                            + ((out.st[:total], plan.worst[rep : rep + 1]) if i == 0 else ())
-                            for i in range(0, len(ranks), 16))
-                continue
-            # multi-GPU: this rank's statuses only (the worst is all-reduced later); the gathered
-            # index-ordered KS array of every cell stays alive for the row's batched selection
-            if stop > first:
-                plan.worst[rep] = out.st[first:stop].max()
-            ks = gather(out.ks, fresh=True)[:total]
-            jobs.extend((ks, ranks[i : i + 16], plan.quantiles[rep, i : i + 16]) for i in range(0, len(ranks), 16))
+            jobs.extend((out.ks[first:stop], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
+                        + ((out.st[first:stop], plan.worst[rep : rep + 1]) if i == 0 else ())
+                        for i in range(0, len(ranks), 16))
         for i0 in range(0, len(ranks), 16):  # equal rank counts per launch
-            eng.select_many([j for j in jobs if j[1] == ranks[i0 : i0 + 16]])
+            part = [j for j in jobs if j[1] == ranks[i0 : i0 + 16]]
+            if reduce is None:
+                eng.select_many(part)
+            else:
+                eng.select_dist(part, total, reduce)
     for plan in plans:
         plan.finished.record(stream)
 
@@ -384,14 +386,14 @@ def _prefetch_tables(eng, configs) -> None:
         _PENDING[(eng.device, *key)] = _POOL.submit(sampling_cdf, cfg.gamma, cfg.support)
 
 
-def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, gather=None, kernel_events=None) -> None:
+def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None) -> None:
     """Queue many cells, grouping those that can share uniform streams (_enqueue_group)."""
     _prefetch_tables(eng, [p.config for p in plans])
     groups: dict = {}
     for plan in plans:
         groups.setdefault(_stage_key(plan.config), []).append(plan)
     for group in groups.values():
-        _enqueue_group(eng, group, shard=shard, gather=gather, kernel_events=kernel_events)
+        _enqueue_group(eng, group, shard=shard, reduce=reduce, kernel_events=kernel_events)
 
 
 def _fetch_plans(plans: list[_CellPlan]) -> None:

@@ -1,14 +1,16 @@
-"""Multi-GPU cutoff tables: one process per GPU, replicate ranges sharded, KS all-gathered.
+"""Multi-GPU cutoff tables: one process per GPU, replicate ranges sharded, a distributed select.
 
 The reference parallelises one repetition over a process pool of 512-replicate spans
 (montecarlo.py:151-191) and is worker-count invariant because streams are keyed
 ``(base_seed, repetition, index)``.  Here each rank of a ``torch.distributed`` group (NCCL
 over NVLink on a B200 box) computes a contiguous shard of replicate indices of every
-(cell, repetition) into its slice of a device buffer, an all-gather assembles the full
-index-ordered KS array on every rank, and every rank runs the same exact selection, so the
-table is bit-identical for any number of GPUs.  The only data-path collective is that
-all-gather (8 B per replicate); a cell's worst status is all-reduced so every rank raises
-the same SimulationError.
+(cell, repetition) into its slice of a device buffer, and the order statistics are selected
+across the shards without moving the KS values: per radix pass every rank histograms the
+digits of its own keys, an NCCL all-reduce sums the histograms (4 x 256 counts per cell and
+pass), and every rank picks the same digits -- so the table is bit-identical for any number of
+GPUs and each rank's selection work stays proportional to its shard.  A cell's worst status is
+all-reduced so every rank raises the same SimulationError.  ``ShardGather`` (an all-gather of
+the shards in index order) remains for callers that want the full KS arrays.
 """
 from __future__ import annotations
 
@@ -75,6 +77,17 @@ class ShardGather:
         return self.out[: self.total]
 
 
+def histogram_reducer(group=None):
+    """Sum of a device tensor over the ranks of ``group`` in place (NCCL all-reduce): the
+    distributed selection's per-pass digit histograms."""
+    import torch.distributed as dist
+
+    def reduce(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return reduce
+
+
 def build_table(
     ns: Iterable[int],
     gammas: Iterable[float],
@@ -108,9 +121,8 @@ def build_table(
                                    repetitions=repetitions, quantiles=levels)
             plans.append(_CellPlan(cfg))
     shard = shard_bounds(replicates, world, rank)
-    gather = ShardGather(replicates, world, rank, group)
     _slab(eng, padded_size(replicates, world))
-    _enqueue_plans(eng, plans, shard=shard, gather=gather)
+    _enqueue_plans(eng, plans, shard=shard, reduce=histogram_reducer(group))
     worst = torch.stack([p.worst.max() for p in plans]).to(torch.int32)
     dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
     for plan, w in zip(plans, worst.tolist()):

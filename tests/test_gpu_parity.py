@@ -367,3 +367,52 @@ def test_parallel_build_table_single_rank_matches(zk):
         assert parallel.build_table(**kw).cells == zk.build_table(**kw).cells
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", [(500, 7500), (0, 8000), (2999, 5001), (4000, 4000)])
+def test_distributed_select_over_shards_matches_whole_array(zk, split):
+    # the distributed selection's arithmetic without NCCL: two engines on one GPU each hold a
+    # shard; their per-pass digit counts land in ONE histogram (the all-reduce's sum), both pick
+    # from it -- every order statistic equals the single-array selection, on both engines
+    import ctypes
+
+    import torch
+
+    from paper_1305_6738_b200 import _native, engine
+
+    rng = np.random.default_rng(split[0] + 7)
+    n = sum(split)
+    vals = torch.tensor(np.concatenate([rng.random(n // 2) * 0.08, rng.random(n - n // 2) * 0.3]) ** 1.5,
+                        dtype=torch.float64, device="cuda")
+    vals[::97] = vals[3]  # ties
+    ranks = [0, 1, n // 3, int(0.9 * n), int(0.99 * n), n - 1]
+    want = torch.empty(len(ranks), dtype=torch.float64, device="cuda")
+    main = engine.get_engine()
+    main.select_ranks(vals, ranks, out=want)
+    engines = [main, engine.Engine(0)]
+    shards = [vals[: split[0]], vals[split[0] :]]
+    outs = [torch.empty(len(ranks), dtype=torch.float64, device="cuda") for _ in engines]
+    lib = main.lib
+    r = np.ascontiguousarray([ranks], dtype=np.int64)
+    for eng, sh, out in zip(engines, shards, outs):
+        eng.bind_stream()
+        ptr = (ctypes.c_void_p * 1)(sh.data_ptr() if sh.numel() else None)
+        optr = (ctypes.c_void_p * 1)(out.data_ptr())
+        nil = (ctypes.c_void_p * 1)(None)
+        cnt = np.array([sh.numel()], dtype=np.int64)
+        tot = np.array([n], dtype=np.int64)
+        _native.check(lib.zks_select_dist_begin(eng.handle, ptr, cnt.ctypes.data, tot.ctypes.data, 1, r.ctypes.data,
+                                                len(ranks), optr, nil, nil))
+    hist = torch.empty(len(ranks) * 256, dtype=torch.int32, device="cuda")
+    for p in range(8):
+        hist.zero_()
+        for eng in engines:
+            _native.check(lib.zks_select_dist_count(eng.handle, p, hist.data_ptr()))
+        for eng in engines:
+            _native.check(lib.zks_select_dist_pick(eng.handle, p, hist.data_ptr()))
+    for eng in engines:
+        _native.check(lib.zks_select_dist_end(eng.handle))
+    torch.cuda.synchronize()
+    for out in outs:
+        assert out.cpu().tolist() == want.cpu().tolist()
+    engines[1].close()
