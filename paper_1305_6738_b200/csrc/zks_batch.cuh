@@ -95,9 +95,11 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   return s;
 }
 
-// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle).
+// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle); the
+// values <= kKsHead are also counted into the lane's column of the u8 histogram lh ([v][lane]).
 __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
-                                                      const uint16_t* __restrict__ guide, uint16_t* v) {
+                                                      const uint16_t* __restrict__ guide, uint16_t* v, uint8_t* lh) {
+  const int lane = threadIdx.x & 31;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   double ls = 0.0;
@@ -115,6 +117,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
         ls += __ldg(a.logs + x[w]);
         mn = min(mn, x[w]);
         mx = max(mx, x[w]);
+        if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
       }
     }
     *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
@@ -131,8 +134,9 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
 // on the word's largest u, accepted when the cdf entry below lies under its smallest u.  Returns
 // false when some word leaves its value undecided (the caller redraws from Philox).
 __device__ __forceinline__ bool draw_sample_lane_staged(const ReplicateArgs& a, const uint32_t* __restrict__ row,
-                                                        const uint16_t* __restrict__ guide, uint16_t* v,
+                                                        const uint16_t* __restrict__ guide, uint16_t* v, uint8_t* lh,
                                                         DrawStats& st) {
+  const int lane = threadIdx.x & 31;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   double ls = 0.0;
@@ -170,6 +174,7 @@ __device__ __forceinline__ bool draw_sample_lane_staged(const ReplicateArgs& a, 
         ls += __ldg(a.logs + x[w]);
         mn = min(mn, x[w]);
         mx = max(mx, x[w]);
+        if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
       } else {
         x[w] = 0u;
       }
@@ -264,19 +269,11 @@ __device__ __forceinline__ bool ks_lane_walk(const ReplicateArgs& a, bool on, do
 
 constexpr int kLaneHistWords = (kKsHead + 1) * 32 / 4;  // u8 counts [value 0..64][lane]
 
-// Small samples: lane r's values <= kKsHead into a private u8 histogram (value-major, so a
-// warp's lanes touch neighbouring bytes), then the lane walk.
+// Small samples: the lane walk over lane r's private u8 histogram of its values <= kKsHead
+// (value-major, so a warp's lanes touch neighbouring bytes; filled while drawing).
 __device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, double g, double norm, uint32_t kmax,
-                                             uint8_t* lh, const uint16_t* v, double& ks, double& S, uint32_t& C,
-                                             double& D) {
+                                             const uint8_t* lh, double& ks, double& S, uint32_t& C, double& D) {
   const int lane = threadIdx.x & 31;
-  const int n = static_cast<int>(a.n);
-  if (on) {
-    for (int j = 0; j < n; ++j) {
-      const uint32_t x = v[j];
-      if (x <= kKsHead) ++lh[x * 32 + lane];
-    }
-  }
   return ks_lane_walk(a, on, g, norm, kmax, [&](uint32_t k) { return static_cast<uint32_t>(lh[k * 32 + lane]); }, ks,
                       S, C, D);
 }
@@ -381,12 +378,17 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     uint16_t* mv = vals + lane * a.vals_stride;
     DrawStats st{0.0, 0u, 0u};
     bool drawn = false;
-    if (active && a.ubuf)  // sweeps: the row's staged words, shared by every gamma of the row
-      drawn = draw_sample_lane_staged(a, a.ubuf + (a.first + r0 + lane - a.ubuf_first) * a.ubuf_stride, guide, mv, st);
+    uint8_t* lh = reinterpret_cast<uint8_t*>(hist);  // lane histograms, zero between batches
+    if (active && a.ubuf) {  // sweeps: the row's staged words, shared by every gamma of the row
+      drawn = draw_sample_lane_staged(a, a.ubuf + (a.first + r0 + lane - a.ubuf_first) * a.ubuf_stride, guide, mv, lh,
+                                      st);
+      if (!drawn)
+        for (int v = 0; v <= static_cast<int>(kKsHead); ++v) lh[v * 32 + lane] = 0;
+    }
     if (active && !drawn) {
       uint64_t k0, k1;
       stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
-      st = draw_sample_lane(a, k0, k1, guide, mv);
+      st = draw_sample_lane(a, k0, k1, guide, mv, lh);
     }
     __syncwarp();
     if (kCount) {
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     double my_ks = __longlong_as_double(0x7ff8000000000000ll);
     double hS, hD;
     uint32_t hC;
-    const bool scored = ks_lane_head(a, ok && active, g, norm, st.vmax, reinterpret_cast<uint8_t*>(hist), mv, my_ks,
+    const bool scored = ks_lane_head(a, ok && active, g, norm, st.vmax, lh, my_ks,
                                      hS, hC, hD);
     clear_hist(hist, kLaneHistWords, lane);
     for (unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored); need; need &= need - 1) {
