@@ -240,7 +240,7 @@ def test_build_table_matches_run_simulation(zk):
 
 
 def test_sweep_with_shared_uniforms_matches_cells(zk):
-    # build_table stages one uniform stream per (n, repetition) for all gammas (n in [128, 1024]);
+    # build_table stages one uniform stream per (n, repetition) for all gammas (128 <= n <= 16384);
     # every cell must equal its own run_simulation bit for bit
     table = zk.build_table(ns=(200, 700), gammas=(1.6, 2.2, 3.0), support=zk.Support.unbounded(), base_seed=3,
                            replicates=3000, repetitions=2)
@@ -345,7 +345,7 @@ def test_cells_on_two_streams_match_sequential(zk):
 
 
 def test_parallel_build_table_single_rank_matches(zk):
-    # the multi-GPU path (shards, NCCL all-gather of every cell's KS array, batched selection
+    # the multi-GPU path (shards, the distributed radix select with its histogram all-reduces,
     # of the gathered arrays, all-reduced worst status) on a one-rank NCCL group equals the
     # single-GPU table bit for bit
     import socket
