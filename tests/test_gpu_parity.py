@@ -346,8 +346,7 @@ def test_cells_on_two_streams_match_sequential(zk):
 
 def test_parallel_build_table_single_rank_matches(zk):
     # the multi-GPU path (shards, the distributed radix select with its histogram all-reduces,
-    # of the gathered arrays, all-reduced worst status) on a one-rank NCCL group equals the
-    # single-GPU table bit for bit
+    # all-reduced worst status) on a one-rank NCCL group equals the single-GPU table bit for bit
     import socket
 
     import torch
