@@ -53,3 +53,23 @@ def test_invalid_arguments_fail_loudly_without_a_device(lib):
     rc = lib.zks_engine_create(0, None, 0, ctypes.byref(ctypes.c_void_p()))
     assert rc == _native.ZKS_EINVAL
     assert b"log table" in lib.zks_last_error()
+
+
+def test_plain_c_consumer_links_and_runs(lib, tmp_path):
+    # the header is plain C and the library links into a C program (the FFI a non-Python
+    # host would use); only calls that need no device
+    src = tmp_path / "consumer.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "zipfks_b200.h"\n'
+        "int main(void) {\n"
+        "  zks_engine* e = 0;\n"
+        "  double logs[2] = {0.0, 0.0};\n"
+        "  int rc = zks_engine_create(0, logs, 2, &e);  /* rejected: logs_len < 65537 */\n"
+        '  printf("%d %d %s\\n", zks_version(), rc != 0, zks_last_error());\n'
+        "  return 0;\n}\n")
+    exe = tmp_path / "consumer"
+    libdir = os.path.dirname(_build.LIB)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L", libdir, "-l:" + os.path.basename(_build.LIB), "-Wl,-rpath," + libdir], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split(maxsplit=2)
+    assert int(out[0]) == _native.ABI_VERSION and out[1] == "1" and "65537" in out[2]
