@@ -143,6 +143,7 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (None, 1.6, 9000, 3, 0, 24),  # two-kernel path with u16 draw bins
         (1000, 1.0, 5000, 2, 0, 24),
         (None, 1.9, 40000, 4, 0, 8),  # two-kernel path near its u16 limit
+        (None, 2.3, 131, 8, 0, 96),  # n not a multiple of 4: the draw kernel's masked last step
         (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
         (5, 2.0, 300, 7, 1, 64),
     ],
@@ -242,8 +243,8 @@ def test_build_table_matches_run_simulation(zk):
 def test_sweep_with_shared_uniforms_matches_cells(zk):
     # build_table stages one uniform stream per (n, repetition) for all gammas (128 <= n <= 16384);
     # every cell must equal its own run_simulation bit for bit
-    table = zk.build_table(ns=(200, 700), gammas=(1.6, 2.2, 3.0), support=zk.Support.unbounded(), base_seed=3,
-                           replicates=3000, repetitions=2)
+    table = zk.build_table(ns=(131, 200, 701), gammas=(1.6, 2.2, 3.0), support=zk.Support.unbounded(), base_seed=3,
+                           replicates=3000, repetitions=2)  # 131, 701: masked last blocks
     for (g, n), row in table.cells.items():
         cfg = zk.SimulationConfig(n=n, support=zk.Support.unbounded(), gamma=g, base_seed=3, replicates=3000,
                                   repetitions=2)
