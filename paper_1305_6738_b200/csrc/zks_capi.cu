@@ -45,7 +45,9 @@ constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
 constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
-constexpr int64_t kBatchMaxN = 1024;                  // n up to which replicate_batch_kernel runs
+constexpr int64_t kBatchMaxN = 1024;                  // n up to which the lane-batch layout applies
+                                                      // (replicate_batch_kernel below kLaneDrawMaxN,
+                                                      // retry_kernel's layout on the two-kernel path)
 constexpr uint64_t kPreBytes = uint64_t(4) << 30;     // pre-drawn rows per chunk (bytes)
 constexpr uint32_t kBatchHist = 512;                  // its per-warp histogram bins
 

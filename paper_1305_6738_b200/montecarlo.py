@@ -208,16 +208,18 @@ def order_quantiles(stats, levels: Sequence[float]) -> list[float]:
     the values must be non-negative, as KS statistics are).
     """
     torch = _torch()
-    eng = _engine()
-    if isinstance(stats, torch.Tensor) and stats.is_cuda:
-        values = stats.to(torch.float64).contiguous()
-    else:
-        arr = np.ascontiguousarray(np.asarray(stats, dtype=np.float64))
-        values = torch.from_numpy(arr).to(f"cuda:{eng.device}")
-    count = values.numel()
+    on_device = isinstance(stats, torch.Tensor) and stats.is_cuda
+    arr = None if on_device else np.ascontiguousarray(np.asarray(stats, dtype=np.float64))
+    count = stats.numel() if on_device else arr.size
+    # argument errors first, as the reference raises them (montecarlo.py:128-135)
     if count == 0:
         raise ValueError("cannot take quantiles of an empty array")
     ranks = quantile_ranks(count, levels)
+    eng = _engine()
+    if on_device:
+        values = stats.to(torch.float64).contiguous()
+    else:
+        values = torch.from_numpy(arr).to(f"cuda:{eng.device}")
     if bool((values < 0).any()) or bool(torch.isnan(values).any()):
         raise ValueError("order_quantiles on the device needs non-negative, non-NaN values")
     values = values + 0.0  # canonicalise -0.0 to +0.0 (order-preserving bit patterns)
