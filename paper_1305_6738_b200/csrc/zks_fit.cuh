@@ -1,4 +1,4 @@
-// Exponent-fit tables: piecewise polynomial (Chebyshev-fitted, evaluated by Horner) images of
+// Exponent-fit tables: piecewise polynomial (Chebyshev-fitted, evaluated by split Horner) images of
 // the reference's model-moment functions, built once per support on the device.
 //
 // The reference evaluates, at every Newton / bisection iterate x (estimate.py:76-83, 94-146),
@@ -66,38 +66,52 @@ __device__ __forceinline__ int fit_locate(const FitTable& T, double x, double& t
 // Interval layout (kFitStride doubles, 16-byte aligned): (mu_j, m2_j) pairs for j = 0..kFitDeg,
 // then norm_0..norm_kFitDeg -- one 16-byte load per Horner step of the Newton pair.
 
+// The degree-11 polynomials are evaluated as two independent Horner halves,
+// sum_{j<6} c_j t^j + t^6 sum_{j<6} c_{j+6} t^j: half the dependent fp64 chain of one Horner pass.
+constexpr int kFitHalf = kFitCoef / 2;
+
 // mean and slope of ln X at x (estimate.py:76-83)
 __device__ __forceinline__ void fit_mean_slope(const FitTable& T, double x, double& mean, double& slope) {
   double t;
   const double2* c = reinterpret_cast<const double2*>(T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride);
-  const double2 top = __ldg(c + kFitDeg);
-  double mu = top.x, m2 = top.y;
+  const double2 top = __ldg(c + kFitDeg), mid = __ldg(c + kFitHalf - 1);
+  double mu_h = top.x, m2_h = top.y, mu_l = mid.x, m2_l = mid.y;
 #pragma unroll
-  for (int j = kFitDeg - 1; j >= 0; --j) {
-    const double2 cj = __ldg(c + j);
-    mu = fma(mu, t, cj.x);
-    m2 = fma(m2, t, cj.y);
+  for (int j = kFitHalf - 2; j >= 0; --j) {
+    const double2 ch = __ldg(c + kFitHalf + j), cl = __ldg(c + j);
+    mu_h = fma(mu_h, t, ch.x);
+    m2_h = fma(m2_h, t, ch.y);
+    mu_l = fma(mu_l, t, cl.x);
+    m2_l = fma(m2_l, t, cl.y);
   }
+  const double t3 = t * t * t, t6 = t3 * t3;
+  const double mu = fma(mu_h, t6, mu_l), m2 = fma(m2_h, t6, m2_l);
   mean = mu;
   slope = m2 - mu * mu;
+}
+
+// one polynomial with coefficients c[j * step], j = 0..kFitDeg
+__device__ __forceinline__ double fit_poly(const double* c, int step, double t) {
+  double h = __ldg(c + kFitDeg * step), l = __ldg(c + (kFitHalf - 1) * step);
+#pragma unroll
+  for (int j = kFitHalf - 2; j >= 0; --j) {
+    h = fma(h, t, __ldg(c + (kFitHalf + j) * step));
+    l = fma(l, t, __ldg(c + j * step));
+  }
+  const double t3 = t * t * t;
+  return fma(h, t3 * t3, l);
 }
 
 __device__ __forceinline__ double fit_mean(const FitTable& T, double x) {
   double t;
   const double* c = T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride;
-  double mu = __ldg(c + 2 * kFitDeg);
-#pragma unroll
-  for (int j = kFitDeg - 1; j >= 0; --j) mu = fma(mu, t, __ldg(c + 2 * j));
-  return mu;
+  return fit_poly(c, 2, t);
 }
 
 __device__ __forceinline__ double fit_norm(const FitTable& T, double x) {
   double t;
   const double* c = T.coef + static_cast<int64_t>(fit_locate(T, x, t)) * kFitStride + 2 * kFitCoef;
-  double v = __ldg(c + kFitDeg);
-#pragma unroll
-  for (int j = kFitDeg - 1; j >= 0; --j) v = fma(v, t, __ldg(c + j));
-  return v;
+  return fit_poly(c, 1, t);
 }
 
 // Terms the reference sums for one model-moment evaluation at x (K, or the m rule of the
