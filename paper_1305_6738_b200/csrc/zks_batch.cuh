@@ -267,6 +267,10 @@ __device__ __forceinline__ bool ks_lane_walk(const ReplicateArgs& a, bool on, do
   return on && done;
 }
 
+#ifndef ZKS_LANE_TAIL_MAX
+#define ZKS_LANE_TAIL_MAX 48
+#endif
+constexpr uint32_t kLaneTailMax = ZKS_LANE_TAIL_MAX;  // longest tail ks_tail_lane takes (values above kKsHead)
 constexpr int kLaneHistWords = (kKsHead + 1) * 32 / 4;  // u8 counts [value 0..64][lane]
 
 // Small samples: the lane walk over lane r's private u8 histogram of its values <= kKsHead
@@ -293,6 +297,48 @@ __device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r
   p.C0 = __shfl_sync(0xffffffffu, C, r);
   p.D0 = __shfl_sync(0xffffffffu, D, r);
   return ks_scan<uint16_t, false>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
+}
+
+// Tail of this lane's own replicate (kmax > kKsHead, n < kLaneDrawMaxN), lane-parallel: the
+// values above the head are compacted to the front of the lane's stored sample v, sorted by
+// insertion, and every distinct value x is scored at k = x - 1 and k = x from
+// S(kKsHead) + em_block(x) -- ks_flush's per-endpoint arithmetic, so the statistic is the warp
+// path's bit for bit (its early exit never changes the maximum).  Overwrites v.
+__device__ __forceinline__ double ks_tail_lane(const ReplicateArgs& a, double g, double norm, double S, uint32_t C,
+                                               double D, uint16_t* v, uint32_t& endpoints) {
+  KsCtx c;
+  c.g = g;
+  c.inv = 1.0 / norm;
+  c.dn = static_cast<double>(a.n);
+  c.inv_n = a.inv_n > 0.0 ? a.inv_n : 1.0 / c.dn;
+  c.exact = false;
+  c.logs = a.logs;
+  ks_tail_ctx(c, g);
+  const int n = static_cast<int>(a.n);
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const uint16_t x = v[i];
+    if (x > kKsHead) v[m++] = x;
+  }
+  for (int i = 1; i < m; ++i) {
+    const uint16_t x = v[i];
+    int j = i;
+    for (; j > 0 && v[j - 1] > x; --j) v[j] = v[j - 1];
+    v[j] = x;
+  }
+  for (int i = 0; i < m;) {
+    const uint32_t x = v[i];
+    int j = i + 1;
+    while (j < m && v[j] == x) ++j;
+    double fx;
+    const double Sx = S + em_block(c, x, fx);
+    D = fmax(D, fabs((Sx - fx) * c.inv - emp(c, C)));
+    C += static_cast<uint32_t>(j - i);
+    D = fmax(D, fabs(Sx * c.inv - emp(c, C)));
+    ++endpoints;
+    i = j;
+  }
+  return D;
 }
 
 // The same from dense counts of the values kKsHead+1..K (counts[v - kKsHead - 1], global memory)
@@ -341,7 +387,8 @@ __host__ __device__ constexpr int batch_warp_bytes(int hist_words, int vals_stri
 
 // Small samples (n < kLaneDrawMaxN): a warp takes B = 32 consecutive replicate indices;
 // each lane draws, fits and scores the head of its own replicate; tails that outlive the head
-// are scored warp-cooperatively from the lane's head state.
+// are scored from the lane's head state, lane by lane when short (ks_tail_lane), else
+// warp-cooperatively.
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -414,14 +461,21 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     }
     if (kCount) add_lane_work(wk, lw);
 
-    // 4. KS: the head lane by lane, long tails warp-cooperatively
+    // 4. KS: the head lane by lane, then the tails
     double my_ks = __longlong_as_double(0x7ff8000000000000ll);
     double hS, hD;
     uint32_t hC;
     const bool scored = ks_lane_head(a, ok && active, g, norm, st.vmax, lh, my_ks,
                                      hS, hC, hD);
     clear_hist(hist, kLaneHistWords, lane);
-    for (unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored); need; need &= need - 1) {
+    // short tails lane by lane (insertion sort: quadratic in the tail length), long ones by the warp
+    const bool tail = active && ok && !scored;
+    const bool short_tail = tail && static_cast<uint32_t>(a.n) - hC <= kLaneTailMax;
+    uint32_t ends = 0;
+    if (short_tail) my_ks = ks_tail_lane(a, g, norm, hS, hC, hD, mv, ends);
+    if (kCount) wk.ks_tails += warp_sum_u32(ends);
+    __syncwarp();
+    for (unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail); need; need &= need - 1) {
       const int r = __ffs(need) - 1;
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);

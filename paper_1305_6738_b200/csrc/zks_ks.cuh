@@ -118,6 +118,20 @@ __device__ __forceinline__ double em_block(const KsCtx& c, uint64_t v, double& f
   return integral + 0.5 * (c.fa + fv) + d1 * (1.0 / 12.0) - d3 * (1.0 / 720.0);
 }
 
+// em_block's constants for the tail above the head at exponent g (c.logs set)
+__device__ __forceinline__ void ks_tail_ctx(KsCtx& c, double g) {
+  c.La = __ldg(c.logs + kKsHead + 1);
+  c.fa = exp_bounded(-g * c.La);
+  constexpr double a = static_cast<double>(kKsHead + 1);
+  c.a_pow = a * c.fa;
+  const double om = 1.0 - g;
+  c.direct = fabs(om) >= 0.125;
+  c.inv_om = om == 0.0 ? 0.0 : 1.0 / om;
+  c.g3 = g * (g + 1.0) * (g + 2.0);
+  c.fa1 = c.fa * (1.0 / a);
+  c.fa3 = c.fa * (1.0 / (a * a * a));
+}
+
 struct FlushTail {
   double F_last;    // fitted cdf at the last scored value
   uint32_t C_last;  // observations <= the last scored value
@@ -291,16 +305,7 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
   if (!s.done && kmax > kKsHead) {
     s.S_head = s.S;
     s.Dw = p.from_head ? p.D0 : warp_max_nonneg(s.D);  // from_head: D0 is the warp's value
-    c.La = __ldg(p.logs + kKsHead + 1);
-    c.fa = exp_bounded(-g * c.La);
-    constexpr double a = static_cast<double>(kKsHead + 1);
-    c.a_pow = a * c.fa;
-    const double om = 1.0 - g;
-    c.direct = fabs(om) >= 0.125;
-    c.inv_om = om == 0.0 ? 0.0 : 1.0 / om;
-    c.g3 = g * (g + 1.0) * (g + 2.0);
-    c.fa1 = c.fa * (1.0 / a);
-    c.fa3 = c.fa * (1.0 / (a * a * a));
+    ks_tail_ctx(c, g);
 
     // above the head: endpoints of the observed values
     int q = 0;

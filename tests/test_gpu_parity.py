@@ -144,6 +144,9 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (1000, 1.0, 5000, 2, 0, 24),
         (None, 1.9, 40000, 4, 0, 8),  # two-kernel path near its u16 limit
         (None, 2.3, 131, 8, 0, 96),  # n not a multiple of 4: the draw kernel's masked last step
+        (1000, 0.5, 100, 5, 0, 128),  # n < 128 with tails of ~75 values above the head: warp-scored
+        (1000, 0.9, 90, 6, 1, 128),  # tails around kLaneTailMax: lane- and warp-scored in one warp
+        (None, 1.05, 120, 3, 0, 96),  # the heaviest unbounded tail at n < 128
         (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
         (5, 2.0, 300, 7, 1, 64),
     ],
