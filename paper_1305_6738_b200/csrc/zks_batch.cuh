@@ -299,13 +299,12 @@ __device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r
   return ks_scan<uint16_t, false>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
 }
 
-// Tail of this lane's own replicate (kmax > kKsHead, n < kLaneDrawMaxN), lane-parallel: the
-// values above the head are compacted to the front of the lane's stored sample v, sorted by
-// insertion, and every distinct value x is scored at k = x - 1 and k = x from
-// S(kKsHead) + em_block(x) -- ks_flush's per-endpoint arithmetic, so the statistic is the warp
-// path's bit for bit (its early exit never changes the maximum).  Overwrites v.
+// Tail of this lane's own replicate (kmax > kKsHead), lane-parallel: its m values above the head
+// v[0..m) are sorted by insertion and every distinct value x is scored at k = x - 1 and k = x
+// from S(kKsHead) + em_block(x) -- ks_flush's per-endpoint arithmetic, so the statistic is the
+// warp path's bit for bit (whose early exit never changes the maximum).  Sorts v in place.
 __device__ __forceinline__ double ks_tail_lane(const ReplicateArgs& a, double g, double norm, double S, uint32_t C,
-                                               double D, uint16_t* v, uint32_t& endpoints) {
+                                               double D, uint16_t* v, int m, uint32_t& endpoints) {
   KsCtx c;
   c.g = g;
   c.inv = 1.0 / norm;
@@ -314,12 +313,6 @@ __device__ __forceinline__ double ks_tail_lane(const ReplicateArgs& a, double g,
   c.exact = false;
   c.logs = a.logs;
   ks_tail_ctx(c, g);
-  const int n = static_cast<int>(a.n);
-  int m = 0;
-  for (int i = 0; i < n; ++i) {
-    const uint16_t x = v[i];
-    if (x > kKsHead) v[m++] = x;
-  }
   for (int i = 1; i < m; ++i) {
     const uint16_t x = v[i];
     int j = i;
@@ -339,6 +332,19 @@ __device__ __forceinline__ double ks_tail_lane(const ReplicateArgs& a, double g,
     i = j;
   }
   return D;
+}
+
+// The same for a whole stored sample v[0..n) (n < kLaneDrawMaxN): its values above the head
+// are first compacted to the front of v (overwritten).
+__device__ __forceinline__ double ks_tail_lane_sample(const ReplicateArgs& a, double g, double norm, double S,
+                                                      uint32_t C, double D, uint16_t* v, uint32_t& endpoints) {
+  const int n = static_cast<int>(a.n);
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const uint16_t x = v[i];
+    if (x > kKsHead) v[m++] = x;
+  }
+  return ks_tail_lane(a, g, norm, S, C, D, v, m, endpoints);
 }
 
 // The same from dense counts of the values kKsHead+1..K (counts[v - kKsHead - 1], global memory)
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     const bool tail = active && ok && !scored;
     const bool short_tail = tail && static_cast<uint32_t>(a.n) - hC <= kLaneTailMax;
     uint32_t ends = 0;
-    if (short_tail) my_ks = ks_tail_lane(a, g, norm, hS, hC, hD, mv, ends);
+    if (short_tail) my_ks = ks_tail_lane_sample(a, g, norm, hS, hC, hD, mv, ends);
     if (kCount) wk.ks_tails += warp_sum_u32(ends);
     __syncwarp();
     for (unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail); need; need &= need - 1) {
@@ -517,6 +523,13 @@ constexpr int kHeadRowWords = kKsHead / 2 + 1;        // u16 counts of 1..kKsHea
 constexpr int kFitHistWords = 32 * kHeadRowWords;      // the head rows, reused as page histogram
 constexpr int kFitStageWords = kOverCap / 2;             // one tail of <= kOverCap u16 values
 constexpr int kFitWarpWords = kFitHistWords + kKsQueueWords + kFitStageWords;
+#ifndef ZKS_FIT_LANE_TAIL_MAX
+#define ZKS_FIT_LANE_TAIL_MAX 48
+#endif
+// longest tail list fit_ks_kernel scores lane by lane (0 = none): the insertion sort's serial
+// latency outgrows the warp path's per-replicate cost at about this length
+constexpr uint32_t kFitLaneTailMax = ZKS_FIT_LANE_TAIL_MAX;
+static_assert(2 * kHeadRowWords >= static_cast<int>(kFitLaneTailMax), "a short tail is sorted in one head row");
 
 // Fit + score of pre-drawn replicates (draw_stats_kernel): a warp takes 32 consecutive rows,
 // fits them lane-parallel, walks each head k <= kKsHead lane by lane from the counts, and
@@ -593,7 +606,19 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     // long tails, warp-cooperatively (the head rows are free now: pages reuse them).  The tail
     // values of the next replicate are loaded into registers while the current one is scored,
     // then staged in shared memory (tails of <= kOverCap values; longer ones read from HBM/L2).
-    unsigned need = __ballot_sync(0xffffffffu, active && ok && !scored);
+    const bool tail = active && ok && !scored;
+    // short tail lists lane by lane, sorted in the lane's own head row (free after its walk)
+    const bool short_tail = tail && !a.dense_words && my_m <= kFitLaneTailMax;
+    uint32_t ends = 0;
+    if (short_tail) {
+      uint16_t* buf = reinterpret_cast<uint16_t*>(heads + lane * kHeadRowWords);
+      const uint16_t* t = a.pre_tail + row * a.vals_stride;
+      for (uint32_t i = 0; i < my_m; ++i) buf[i] = t[i];
+      my_ks = ks_tail_lane(a, g, norm, hS, hC, hD, buf, static_cast<int>(my_m), ends);
+    }
+    if (kCount) wk.ks_tails += warp_sum_u32(ends);
+    __syncwarp();
+    unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail);
     if (a.dense_words) {  // dense finite support: tiles over the counts of kKsHead+1..kmax
       for (; need; need &= need - 1) {
         const int r = __ffs(need) - 1;

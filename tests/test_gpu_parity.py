@@ -147,6 +147,7 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (1000, 0.5, 100, 5, 0, 128),  # n < 128 with tails of ~75 values above the head: warp-scored
         (1000, 0.9, 90, 6, 1, 128),  # tails around kLaneTailMax: lane- and warp-scored in one warp
         (None, 1.05, 120, 3, 0, 96),  # the heaviest unbounded tail at n < 128
+        (None, 1.6, 800, 2, 0, 96),  # two-kernel path, tail lists around kFitLaneTailMax (lane + warp)
         (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
         (5, 2.0, 300, 7, 1, 64),
     ],
