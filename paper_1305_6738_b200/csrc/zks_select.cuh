@@ -9,6 +9,7 @@
 // picks the digit holding the rank.  After the first two passes the keys matching a rank's
 // 16-bit prefix are compacted, so passes 2-7 read only those (a few % of KS values).
 //
+// The arrays are processed concurrently (ArrayPart: each block works on one array at a time).
 // Two drivers of the same steps:
 //   * select_kernel: ONE cooperative launch, grid barriers between the steps (one GPU);
 //   * select_{init,count,pick,out}_kernel: one launch per step, so that between count and pick
@@ -24,6 +25,10 @@ namespace zks {
 
 constexpr int kMaxRanks = 16;
 constexpr int kSelMaxArrays = 24;
+#ifndef ZKS_SEL_UNROLL
+#define ZKS_SEL_UNROLL 8
+#endif
+constexpr int kSelUnroll = ZKS_SEL_UNROLL;  // key loads in flight per thread
 constexpr int kSelectPasses = 8;
 constexpr int kSelSlots = kSelMaxArrays * kMaxRanks;
 
@@ -53,6 +58,36 @@ struct SelectShared {
   int srep[kMaxRanks];
 };
 
+// Arrays are worked on concurrently: with G >= A blocks, array a takes the blocks b = a (mod A);
+// with fewer blocks, block b takes the arrays a = b (mod G).  One block-wide histogram cycle per
+// (block, array) instead of every block stepping through every array in turn.
+struct ArrayPart {
+  int a0, da;      // this block's first array and the step to its next one
+  int lb, nb;      // this block's index among its array's blocks, and their number
+  __device__ __forceinline__ ArrayPart(int narrays) {
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    if (G >= narrays) {
+      a0 = b % narrays;
+      da = G;  // one array per block
+      lb = b / narrays;
+      nb = (G - a0 + narrays - 1) / narrays;
+    } else {
+      a0 = b;
+      da = G;
+      lb = 0;
+      nb = 1;
+    }
+  }
+  __device__ __forceinline__ int64_t tid() const { return int64_t(lb) * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int64_t stride() const { return int64_t(nb) * blockDim.x; }
+};
+
+__device__ __forceinline__ int64_t array_offset(const SelectBatch& B, int a) {
+  int64_t off = 0;
+  for (int i = 0; i < a; ++i) off += B.count[i];
+  return off;
+}
+
 // step 0: prefixes, remaining ranks, candidate counts, worst statuses (grid-stride over `tid`)
 __device__ __forceinline__ void sel_init(const SelectBatch& B, SelectState* st, int64_t tid, int64_t stride) {
   const int nr = B.nr, slots = B.narrays * nr;
@@ -67,11 +102,25 @@ __device__ __forceinline__ void sel_init(const SelectBatch& B, SelectState* st, 
 }
 
 // worst status per array (montecarlo.py:106-115 failures surface as SimulationError on the host)
-__device__ __forceinline__ void sel_worst(const SelectBatch& B, SelectState* st, int64_t tid, int64_t stride) {
-  for (int a = 0; a < B.narrays; ++a) {
+__device__ __forceinline__ void sel_worst(const SelectBatch& B, SelectState* st) {
+  const ArrayPart P(B.narrays);
+  for (int a = P.a0; a < B.narrays; a += P.da) {
     if (!B.status[a]) continue;
+    const unsigned char* s8 = B.status[a];
+    const int64_t n = B.count[a];
     unsigned w = 0;
-    for (int64_t i = tid; i < B.count[a]; i += stride) w = max(w, static_cast<unsigned>(B.status[a][i]));
+    // 16-byte loads from the first aligned byte on, single bytes around them
+    const int64_t lead = static_cast<int64_t>((16 - (reinterpret_cast<uintptr_t>(s8) & 15)) & 15);
+    const int64_t head = lead < n ? lead : n;
+    const int64_t n16 = (n - head) >> 4;
+    const uint4* v = reinterpret_cast<const uint4*>(s8 + head);
+    for (int64_t i = P.tid(); i < n16; i += P.stride()) {
+      const uint4 q = __ldcs(v + i);
+      w = __vmaxu4(w, __vmaxu4(__vmaxu4(q.x, q.y), __vmaxu4(q.z, q.w)));  // byte-wise maxima
+    }
+    w = max(max(w & 0xffu, (w >> 8) & 0xffu), max((w >> 16) & 0xffu, w >> 24));
+    for (int64_t i = P.tid(); i < head; i += P.stride()) w = max(w, static_cast<unsigned>(s8[i]));
+    for (int64_t i = head + (n16 << 4) + P.tid(); i < n; i += P.stride()) w = max(w, static_cast<unsigned>(s8[i]));
     w = __reduce_max_sync(0xffffffffu, w);
     if ((threadIdx.x & 31) == 0 && w) atomicMax(&st->worst[a], w);
   }
@@ -79,12 +128,12 @@ __device__ __forceinline__ void sel_worst(const SelectBatch& B, SelectState* st,
 
 // one pass's digit counts of this block's keys into H[slot][256] (slot = array * nr + rank)
 __device__ __forceinline__ void sel_count(const SelectBatch& B, SelectState* st, int pass, unsigned* H,
-                                          SelectShared& S, int64_t tid, int64_t stride) {
+                                          SelectShared& S) {
   const int nr = B.nr;
   const int shift = 56 - 8 * pass;
   const unsigned long long mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
-  int64_t off = 0;
-  for (int a = 0; a < B.narrays; ++a) {
+  const ArrayPart P(B.narrays);
+  for (int a = P.a0; a < B.narrays; a += P.da) {
     for (int i = threadIdx.x; i < nr * 256; i += blockDim.x) S.sh[i >> 8][i & 255] = 0u;
     if (threadIdx.x < nr) S.spre[threadIdx.x] = __ldcg(&st->pre[a * nr + threadIdx.x]);
     __syncthreads();
@@ -96,32 +145,42 @@ __device__ __forceinline__ void sel_count(const SelectBatch& B, SelectState* st,
           break;
         }
       S.srep[threadIdx.x] = r0;
-      if (blockIdx.x == 0) st->rep[a * nr + threadIdx.x] = r0;
+      if (P.lb == 0) st->rep[a * nr + threadIdx.x] = r0;
     }
     __syncthreads();
     // passes 0-1 read every key; later passes only the keys that matched a 16-bit prefix
-    const unsigned long long* keys = pass < 2 ? B.keys[a] : B.cand + off;
+    const unsigned long long* keys = pass < 2 ? B.keys[a] : B.cand + array_offset(B, a);
     const int64_t count = pass < 2 ? B.count[a] : static_cast<int64_t>(__ldcg(&st->cand_n[a]));
-    off += B.count[a];
     // a thread's run of equal (rank, digit) hits is counted in registers and flushed to the
     // block histogram when it changes: the top digits of KS keys repeat (shared exponents)
     int run_r = -1;
     unsigned run_d = 0, run_n = 0;
-    for (int64_t i = tid; i < count; i += stride) {
-      const unsigned long long key = __ldcg(keys + i);
-      const unsigned d = static_cast<unsigned>(key >> shift) & 255u;
-      const unsigned long long top = key & mask;
-      int hr = -1;
-      for (int r = 0; r < nr; ++r)
-        if (S.srep[r] == r && top == S.spre[r]) hr = r;
-      if (hr < 0) continue;
-      if (hr == run_r && d == run_d) {
-        ++run_n;
-      } else {
-        if (run_n) atomicAdd(&S.sh[run_r][run_d], run_n);
-        run_r = hr;
-        run_d = d;
-        run_n = 1;
+    const int64_t stride = P.stride();
+    for (int64_t i0 = P.tid(); i0 < count; i0 += kSelUnroll * stride) {
+      unsigned long long kk[kSelUnroll];  // kSelUnroll loads in flight per thread
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u) {
+        const int64_t i = i0 + u * stride;
+        kk[u] = i < count ? __ldcg(keys + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u) {
+        if (i0 + u * stride >= count) break;
+        const unsigned long long key = kk[u];
+        const unsigned d = static_cast<unsigned>(key >> shift) & 255u;
+        const unsigned long long top = key & mask;
+        int hr = -1;
+        for (int r = 0; r < nr; ++r)
+          if (S.srep[r] == r && top == S.spre[r]) hr = r;
+        if (hr < 0) continue;
+        if (hr == run_r && d == run_d) {
+          ++run_n;
+        } else {
+          if (run_n) atomicAdd(&S.sh[run_r][run_d], run_n);
+          run_r = hr;
+          run_d = d;
+          run_n = 1;
+        }
       }
     }
     if (run_n) atomicAdd(&S.sh[run_r][run_d], run_n);
@@ -178,29 +237,37 @@ __device__ __forceinline__ void sel_pick(const SelectBatch& B, SelectState* st, 
 }
 
 // the keys still matching a rank's 16-bit prefix, per array, into B.cand (after pass 1's pick)
-__device__ __forceinline__ void sel_compact(const SelectBatch& B, SelectState* st, SelectShared& S, int64_t stride) {
+__device__ __forceinline__ void sel_compact(const SelectBatch& B, SelectState* st, SelectShared& S) {
   const int nr = B.nr, lane = threadIdx.x & 31;
-  int64_t off = 0;
-  for (int a = 0; a < B.narrays; ++a) {
+  const ArrayPart P(B.narrays);
+  for (int a = P.a0; a < B.narrays; a += P.da) {
     if (threadIdx.x < nr) S.spre[threadIdx.x] = __ldcg(&st->pre[a * nr + threadIdx.x]);
     __syncthreads();
     const unsigned long long* keys = B.keys[a];
-    unsigned long long* cand = B.cand + off;
-    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < B.count[a]; base += stride) {
-      const int64_t i = base + threadIdx.x;  // whole warps iterate together (ballot below)
-      const unsigned long long key = i < B.count[a] ? __ldcg(keys + i) : ~0ull;
-      const unsigned long long top = key & (~0ull << 48);
-      bool hit = false;
-      for (int r = 0; r < nr; ++r) hit |= i < B.count[a] && top == S.spre[r];
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (m) {
-        unsigned long long at = 0;
-        if (lane == 0) at = atomicAdd(&st->cand_n[a], static_cast<unsigned long long>(__popc(m)));
-        at = __shfl_sync(0xffffffffu, at, 0);
-        if (hit) cand[at + __popc(m & ((1u << lane) - 1u))] = key;
+    unsigned long long* cand = B.cand + array_offset(B, a);
+    const int64_t n = B.count[a], stride = P.stride();
+    for (int64_t base = int64_t(P.lb) * blockDim.x; base < n; base += kSelUnroll * stride) {
+      unsigned long long kk[kSelUnroll];
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u) {
+        const int64_t i = base + u * stride + threadIdx.x;
+        kk[u] = i < n ? __ldcg(keys + i) : ~0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u) {
+        const int64_t i = base + u * stride + threadIdx.x;  // whole warps iterate together (ballot below)
+        const unsigned long long top = kk[u] & (~0ull << 48);
+        bool hit = false;
+        for (int r = 0; r < nr; ++r) hit |= i < n && top == S.spre[r];
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) {
+          unsigned long long at = 0;
+          if (lane == 0) at = atomicAdd(&st->cand_n[a], static_cast<unsigned long long>(__popc(m)));
+          at = __shfl_sync(0xffffffffu, at, 0);
+          if (hit) cand[at + __popc(m & ((1u << lane) - 1u))] = kk[u];
+        }
       }
     }
-    off += B.count[a];
     __syncthreads();
   }
 }
@@ -224,16 +291,16 @@ __global__ void __launch_bounds__(256) select_kernel(SelectBatch B, SelectState*
     st->hist[i / (slots * 256)][(i / 256) % slots][i & 255] = 0u;
   sel_init(B, st, tid, stride);
   grid.sync();
-  sel_worst(B, st, tid, stride);
+  sel_worst(B, st);
   const int gwarp = static_cast<int>(tid >> 5), nwarps = static_cast<int>(stride >> 5);
   for (int pass = 0; pass < kSelectPasses; ++pass) {
     unsigned* H = &st->hist[pass][0][0];
-    sel_count(B, st, pass, H, S, tid, stride);
+    sel_count(B, st, pass, H, S);
     grid.sync();
     sel_pick(B, st, pass, H, gwarp, nwarps);
     grid.sync();
     if (pass == 1) {
-      sel_compact(B, st, S, stride);
+      sel_compact(B, st, S);
       grid.sync();
     }
   }
@@ -248,10 +315,8 @@ __global__ void __launch_bounds__(256) select_init_kernel(SelectBatch B, SelectS
 }
 __global__ void __launch_bounds__(256) select_count_kernel(SelectBatch B, SelectState* st, int pass, unsigned* H) {
   __shared__ SelectShared S;
-  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  if (pass == 0) sel_worst(B, st, tid, stride);
-  sel_count(B, st, pass, H, S, tid, stride);
+  if (pass == 0) sel_worst(B, st);
+  sel_count(B, st, pass, H, S);
 }
 __global__ void __launch_bounds__(256) select_pick_kernel(SelectBatch B, SelectState* st, int pass, const unsigned* H) {
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -259,7 +324,7 @@ __global__ void __launch_bounds__(256) select_pick_kernel(SelectBatch B, SelectS
 }
 __global__ void __launch_bounds__(256) select_compact_kernel(SelectBatch B, SelectState* st) {
   __shared__ SelectShared S;
-  sel_compact(B, st, S, int64_t(gridDim.x) * blockDim.x);
+  sel_compact(B, st, S);
 }
 __global__ void __launch_bounds__(256) select_out_kernel(SelectBatch B, SelectState* st) {
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
