@@ -347,21 +347,6 @@ __device__ __forceinline__ double ks_tail_lane_sample(const ReplicateArgs& a, do
   return ks_tail_lane(a, g, norm, S, C, D, v, m, endpoints);
 }
 
-// The same from dense counts of the values kKsHead+1..K (counts[v - kKsHead - 1], global memory)
-__device__ __forceinline__ KsOut ks_tail_dense(const ReplicateArgs& a, int r, double g, double norm, uint32_t kmax,
-                                               double S, uint32_t C, double D, const uint32_t* counts,
-                                               uint32_t* queue, int lane, Work& wk) {
-  KsParams p = ks_params(a);
-  p.H = static_cast<uint32_t>(kKsHead + a.dense_words);  // kmax <= K <= H: no values above
-  p.from_head = true;
-  p.S0 = __shfl_sync(0xffffffffu, S, r);
-  p.C0 = __shfl_sync(0xffffffffu, C, r);
-  p.D0 = __shfl_sync(0xffffffffu, D, r);
-  // ks_scan reads counts[k] for k > kKsHead
-  return ks_scan<uint16_t, false>(p, g, norm, kmax, const_cast<uint32_t*>(counts) - (kKsHead + 1), nullptr, 0u, queue,
-                                  lane, wk);
-}
-
 // One replicate's second attempt on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative:
 // draw into v, fit, score.  Returns the status (1 retried, 2 failed twice).
 template <bool kCount>
@@ -619,17 +604,28 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     if (kCount) wk.ks_tails += warp_sum_u32(ends);
     __syncwarp();
     unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail);
-    if (a.dense_words) {  // dense finite support: tiles over the counts of kKsHead+1..kmax
-      for (; need; need &= need - 1) {
-        const int r = __ffs(need) - 1;
-        const double gr = __shfl_sync(0xffffffffu, g, r);
-        const double nr = __shfl_sync(0xffffffffu, norm, r);
-        const uint32_t kmax = __shfl_sync(0xffffffffu, vmax, r);
-        const uint32_t* counts = reinterpret_cast<const uint32_t*>(
-            a.pre_tail + (a.first + r0 + r - a.pre_first) * a.vals_stride);
-        const KsOut ko = ks_tail_dense(a, r, gr, nr, kmax, hS, hC, hD, counts, queue, lane, wk);
-        if (lane == r) my_ks = ko.D;
+    if (a.dense_words) {  // dense finite support (K <= kDenseMaxK): the head walk continues
+      // lane by lane over the row's counts of kKsHead+1..kmax, the reference's cumulative
+      // form (gof.py:60-70) in the head's arithmetic; no endpoint formulas, no warp scans
+      const uint32_t* counts = reinterpret_cast<const uint32_t*>(a.pre_tail + row * a.vals_stride);
+      const double inv = 1.0 / norm;
+      const bool fast_exp = fabs(g) <= 100.0;  // |g ln k| < 708 for k <= 1024
+      double S = hS, D = hD;
+      uint32_t C = hC;
+      bool live = tail;
+      for (uint32_t k = kKsHead + 1; __any_sync(0xffffffffu, live && k <= vmax); ++k) {
+        if (live && k <= vmax) {
+          const double x = -g * __ldg(a.logs + k);
+          S += fast_exp ? exp_bounded(x) : exp(x);
+          C += counts[k - (kKsHead + 1)];
+          const double F = S * inv, E = static_cast<double>(C) * a.inv_n;
+          const double gap = fabs(F - E);
+          D = gap > D ? gap : D;
+          if (D > (1.0 - E) + kKsMargin && D > (1.0 - F) + kKsMargin) live = false;
+        }
       }
+      if (tail) my_ks = D;
+      need = 0;
     }
     uint32_t pv[kOverCap / 32], pm = 0;
     auto issue = [&](int r) {
