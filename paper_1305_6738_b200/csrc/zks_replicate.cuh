@@ -367,7 +367,10 @@ __device__ __forceinline__ KsParams ks_params(const ReplicateArgs& a) {
 }
 
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads, 1) replicate_kernel(ReplicateArgs a) {
+#ifndef ZKS_REPL_MINB
+#define ZKS_REPL_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, ZKS_REPL_MINB) replicate_kernel(ReplicateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
