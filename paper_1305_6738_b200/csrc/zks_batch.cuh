@@ -774,8 +774,25 @@ constexpr int kCutTabBits = 10;  // the cut table: one entry per 2^22-wide range
 // The cut table of a sampling table: entry i covers the words t in [i 2^22, (i+1) 2^22).  With
 // the exact cuts T_j (u > cdf[j] <=> t < T_j, t = T_j undecided), a range holding no cut decides
 // the value 1 + #{j : T_j > t} of all its words: the entry is the count increment 1 << 8(v-1)
-// for v <= 4, and 0 (queue for the exact search) for v = 5 or a range holding a cut.
-__device__ __forceinline__ void build_cut_table(uint32_t* tab, const uint32_t tcut[4]) {
+// for v <= 4.  A range above h_3 whose extreme uniforms (u_max = 1 - i 2^-10 and u_min =
+// 1 - (i+1) 2^-10 + 2^-53, the bounds of u for a staged word or a Philox draw whose top 32 bits
+// lie in the range) see the same count c of the first 64 cdf entries below them decides the value
+// v = c + 1 <= 64 of all its words (no cdf entry lies in [u_min, u_max), so no staged word of it
+// is undecided either): the entry is kDirect | v, counted straight into the lane's bin.  Any
+// other range is 0: queued for the exact search.  head64 = cdf[0..63] (+inf from L-1 on).
+constexpr uint32_t kDirect = 0x80000000u;
+__device__ __forceinline__ uint32_t count_below(const double* head64, double u) {
+  uint32_t lo = 0, hi = 64;  // #{j < 64 : head64[j] < u}
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (head64[mid] < u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ void build_cut_table(uint32_t* tab, const uint32_t tcut[4], const double* head64) {
   for (int i = threadIdx.x; i < (1 << kCutTabBits); i += blockDim.x) {
     const uint32_t lo = static_cast<uint32_t>(i) << (32 - kCutTabBits);
     const uint32_t hi = lo + ((1u << (32 - kCutTabBits)) - 1u);
@@ -786,12 +803,19 @@ __device__ __forceinline__ void build_cut_table(uint32_t* tab, const uint32_t tc
       c += tcut[j] > hi;
       cut |= tcut[j] >= lo && tcut[j] <= hi;
     }
-    tab[i] = (cut || c == 4) ? 0u : (1u << (8 * c));
+    uint32_t e = (cut || c == 4) ? 0u : (1u << (8 * c));
+    if (!cut && c == 4) {
+      const double umax = 1.0 - static_cast<double>(i) * 0x1p-10;
+      const double umin = (1.0 - static_cast<double>(i + 1) * 0x1p-10) + 0x1p-53;
+      const uint32_t cmin = count_below(head64, umin), cmax = count_below(head64, umax);
+      if (cmin == cmax && cmax < 64u) e = kDirect | (cmax + 1u);
+    }
+    tab[i] = e;
   }
 }
 constexpr int kPreMaxN = 65535;     // largest n of the two-kernel path (u16 counts; tail rows of 2n B)
 constexpr int kDenseMaxK = 1024;       // finite supports kept as dense counts above the head
-constexpr int kNarrowBinsMaxN = 8160;  // a lane resolves <= n/32 + 1 queued draws: u8 bins up to here
+constexpr int kNarrowBinsMaxN = 3968;  // a lane bins <= n/32 + 1 queued and <= n/32 + 4 direct draws: u8 up to here
 // per-warp smem of draw_stats_kernel: bins [v][lane] (u8, or u16 above kNarrowBinsMaxN) + queue
 __host__ __device__ constexpr int draw_warp_bytes(bool wide) { return (kKsHead + 1) * 32 * (wide ? 2 : 1) + kDrawQueue * 8; }
 
@@ -891,6 +915,10 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
         e = 0u;
         big = false;
       }
+      if (e & kDirect) {  // a value 5..kKsHead decided by its range: the lane's own bin
+        ++bins[(e & 0xffu) * 32 + lane];
+        e = 0u;
+      }
       acc += e;
       const unsigned bm = __ballot_sync(0xffffffffu, big);
       if (big) queue[qn + __popc(bm & lt)] = w4[w];
@@ -987,13 +1015,18 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   uint32_t* ctab = reinterpret_cast<uint32_t*>(smem + guide_bytes);
   unsigned char* wbase = smem + guide_bytes + (4 << kCutTabBits) + warp * (draw_warp_bytes(kWide) + a.dense_words * 4);
   // lane-private counts of the values 5..kKsHead, value-major ([v][lane]): a lane resolves at
-  // most one queued draw per pop and there are <= n/32 + 1 pops (u8 up to kNarrowBinsMaxN)
+  // most one queued draw per pop and there are <= n/32 + 1 pops, plus its direct draws (<= 4 per
+  // step of its <= n/128 + 1 steps): u8 up to kNarrowBinsMaxN
   BinT* bins = reinterpret_cast<BinT*>(wbase);
   void* queue = wbase + (kKsHead + 1) * 32 * sizeof(BinT);
   uint32_t* dense = a.dense_words ? reinterpret_cast<uint32_t*>(wbase + draw_warp_bytes(kWide)) : nullptr;
   for (int i = lane; i < a.dense_words; i += 32) dense[i] = 0u;
   load_guide(guide, a.guide, 1);
-  build_cut_table(ctab, a.tcut);
+  // cdf[0..63] staged in warp 0's queue (not in use yet) for the cut table's direct entries
+  double* head64 = reinterpret_cast<double*>(smem + guide_bytes + (4 << kCutTabBits) + (kKsHead + 1) * 32 * sizeof(BinT));
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) head64[j] = j + 1 < static_cast<int>(a.L) ? __ldg(a.cdf + j) : __longlong_as_double(0x7ff0000000000000ll);
+  __syncthreads();
+  build_cut_table(ctab, a.tcut, head64);
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
