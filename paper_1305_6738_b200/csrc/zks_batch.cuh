@@ -223,7 +223,7 @@ __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double 
     if (H >= 2) hist[2] = c2;
   }
   __syncwarp();
-  const KsOut ko = ks_scan<uint16_t, false>(ks_params(a), g, norm, kmax, hist, v, static_cast<uint32_t>(n), queue, lane, wk);
+  const KsOut ko = ks_scan<uint16_t, false, true>(ks_params(a), g, norm, kmax, hist, v, static_cast<uint32_t>(n), queue, lane, wk);
   const int top = ko.used_pages ? a.hist_words : round_up(static_cast<int>(min(kmax, H)) + 1, 4);
   clear_hist(hist, min(top, a.hist_words), lane);
   return ko.D;
@@ -296,7 +296,7 @@ __device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r
   p.S0 = __shfl_sync(0xffffffffu, S, r);
   p.C0 = __shfl_sync(0xffffffffu, C, r);
   p.D0 = __shfl_sync(0xffffffffu, D, r);
-  return ks_scan<uint16_t, false>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
+  return ks_scan<uint16_t, false, true>(p, g, norm, kmax, hist, over, over_n, queue, lane, wk);
 }
 
 // Tail of this lane's own replicate (kmax > kKsHead), lane-parallel: its m values above the head

@@ -254,7 +254,9 @@ __device__ __forceinline__ void bitonic_sort_warp(uint32_t (&r)[kOverCap / 32], 
 // KS of one sample with counts of 1..H in `hist`; values above H are found in
 // over_vals[0..over_n) (which may also hold values <= H: they are ignored).  `queue` is
 // kKsQueueWords u32 of per-warp shared memory.  `hist` is left dirty (see used_pages).
-template <typename VT, bool kArg>
+// kCompact: over_vals is the caller's scratch; each page pass keeps only the values above its
+// page (compacted in place), so later passes read the remaining tail instead of all of it.
+template <typename VT, bool kArg, bool kCompact = false>
 __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax, uint32_t* hist,
                          const VT* over_vals, uint32_t over_n, uint32_t* queue, int lane, Work& wk) {
   KsCtx c;
@@ -418,12 +420,29 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       for (int i = lane; i < p.hist_words; i += 32) hist[i] = 0u;
       __syncwarp();
       uint64_t next = ~0ull;
-      for (uint32_t i = lane; i < over_n; i += 32) {
-        const uint64_t v = static_cast<uint64_t>(over_vals[i]);
-        if (v >= pa && v <= pb)
-          atomicAdd(hist + (v - pa), 1u);
-        else if (v > pb)
-          next = v < next ? v : next;
+      if (kCompact) {
+        const unsigned lt = (1u << lane) - 1u;
+        VT* keep_out = const_cast<VT*>(over_vals);
+        uint32_t kept = 0;
+        for (uint32_t i0 = 0; i0 < over_n; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          const uint64_t v = i < over_n ? static_cast<uint64_t>(over_vals[i]) : 0ull;
+          if (v >= pa && v <= pb) atomicAdd(hist + (v - pa), 1u);
+          const bool keep = v > pb;
+          if (keep) next = v < next ? v : next;
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (keep) keep_out[kept + __popc(km & lt)] = static_cast<VT>(v);  // slot <= i: read already
+          kept += __popc(km);
+        }
+        over_n = kept;
+      } else {
+        for (uint32_t i = lane; i < over_n; i += 32) {
+          const uint64_t v = static_cast<uint64_t>(over_vals[i]);
+          if (v >= pa && v <= pb)
+            atomicAdd(hist + (v - pa), 1u);
+          else if (v > pb)
+            next = v < next ? v : next;
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {

@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_REPL_MINB) replicate_kernel(Repl
       bool used_pages = false;
       if (ok) {
         const double norm = model_norm(M, g, lane, wk);
-        const KsOut ko = ks_scan<uint16_t, false>(ks_params(a), g, norm, st.vmax, hist, slab, st.over, queue, lane, wk);
+        const KsOut ko = ks_scan<uint16_t, false, true>(ks_params(a), g, norm, st.vmax, hist, slab, st.over, queue, lane, wk);
         ks = ko.D;
         used_pages = ko.used_pages;
         gh = g;
