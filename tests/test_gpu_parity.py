@@ -143,6 +143,7 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (None, 1.6, 9000, 3, 0, 24),  # two-kernel path with u16 draw bins
         (1000, 1.0, 5000, 2, 0, 24),
         (None, 1.9, 40000, 4, 0, 8),  # two-kernel path near its u16 limit
+        (None, 1.25, 30000, 3, 0, 8),  # ~9000 tail values over ~60 pages: page passes compact the tail
         (None, 2.3, 131, 8, 0, 96),  # n not a multiple of 4: the draw kernel's masked last step
         (1000, 0.5, 100, 5, 0, 128),  # n < 128 with tails of ~75 values above the head: warp-scored
         (1000, 0.9, 90, 6, 1, 128),  # tails around kLaneTailMax: lane- and warp-scored in one warp
