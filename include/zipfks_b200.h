@@ -162,6 +162,16 @@ int zks_normaliser(zks_engine* engine, double gamma, int32_t support_k, double* 
 int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, uint64_t index, int64_t count,
                         double* out_dev);
 
+/* The same stream for an explicit Philox4x64 key (k0, k1) = SeedSequence(key).generate_state(2,
+ * uint64): RandomStream(key) for keys other than [seed, repetition, index] (distribution.py:
+ * 173-180 accepts any SeedSequence entropy; the host derives the key, the device the uniforms).
+ * Asynchronous. */
+/* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (default 4 GiB,
+ * 0 restores it): a cell whose rows exceed it runs chunk by chunk.  Results do not depend on it. */
+int zks_engine_set_chunk_bytes(zks_engine* engine, uint64_t bytes);
+
+int zks_stream_uniforms_key(zks_engine* engine, uint64_t k0, uint64_t k1, int64_t count, double* out_dev);
+
 /* Inverse-transform draws for given uniforms: searchsorted(cdf, u, 'left') + 1 clamped to the
  * table length (sample, distribution.py:190-201).  Asynchronous. */
 int zks_draw(zks_engine* engine, const zks_table* table, const double* u_dev, int64_t count, int64_t* out_dev);

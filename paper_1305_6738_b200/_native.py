@@ -42,6 +42,8 @@ EXPORTS = (
     "zks_select_dist_end",
     "zks_normaliser",
     "zks_stream_uniforms",
+    "zks_stream_uniforms_key",
+    "zks_engine_set_chunk_bytes",
     "zks_draw",
     "zks_fit_samples",
     "zks_series_eval",
@@ -123,6 +125,8 @@ def load() -> ctypes.CDLL:
     lib.zks_select_dist_end.argtypes = [vp]
     lib.zks_normaliser.argtypes = [vp, ctypes.c_double, i32, dp]
     lib.zks_stream_uniforms.argtypes = [vp, u64, u64, u64, i64, dp]
+    lib.zks_stream_uniforms_key.argtypes = [vp, u64, u64, i64, dp]
+    lib.zks_engine_set_chunk_bytes.argtypes = [vp, u64]
     lib.zks_draw.argtypes = [vp, vp, dp, i64, dp]
     lib.zks_engine_set_counters.argtypes = [vp, dp]
     lib.zks_fit_samples.argtypes = [vp, i32, dp, dp, i64, i32, ctypes.POINTER(ZksMleSettings), dp, dp, dp, dp, dp, dp,

@@ -198,7 +198,7 @@ __device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int 
 
 // KS of the stored sample v[0..n): histogram of 1..H, pages above H from v itself.
 __device__ __forceinline__ double ks_from_sample(const ReplicateArgs& a, double g, double norm, uint32_t kmax,
-                                                 uint32_t* hist, uint32_t* queue, const uint16_t* v, int lane, Work& wk) {
+                                                 uint32_t* hist, uint32_t* queue, uint16_t* v, int lane, Work& wk) {
   const int n = static_cast<int>(a.n);
   const uint32_t H = static_cast<uint32_t>(a.H);
   // values 1 and 2 (most of the mass for gamma >~ 1.5) are counted in registers: a shared
@@ -286,7 +286,7 @@ __device__ __forceinline__ bool ks_lane_head(const ReplicateArgs& a, bool on, do
 // kKsHead among over[0..over_n), warp-cooperatively.
 __device__ __forceinline__ KsOut ks_tail_from_head(const ReplicateArgs& a, int r, double g, double norm, uint32_t kmax,
                                                    double S, uint32_t C, double D, uint32_t* hist, int hist_words,
-                                                   uint32_t page, uint32_t* queue, const uint16_t* over,
+                                                   uint32_t page, uint32_t* queue, uint16_t* over,
                                                    uint32_t over_n, int lane, Work& wk) {
   KsParams p = ks_params(a);
   p.H = kKsHead;
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, vmax, r);
-      const uint16_t* over =
+      uint16_t* over =
           m <= kOverCap ? stage : a.pre_tail + (a.first + r0 + r - a.pre_first) * a.vals_stride;
       const KsOut ko =
           ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, kFitHistWords, kFitHistWords, queue, over, m, lane, wk);

@@ -59,31 +59,35 @@ struct zks_engine {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   double* logs = nullptr;
-  uint16_t* slab = nullptr;
-  size_t slab_bytes = 0;
-  zks::SelectState* sel = nullptr;
-  double* sel_out = nullptr;
   // pinned staging ring: table uploads stay asynchronous w.r.t. queued kernels
   double* staging = nullptr;
   cudaEvent_t staging_done[kStagingSlots] = {};
   int staging_next = 0;
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
   int mle_mode = ZKS_MLE_TABLE;
+  uint64_t pre_cap = kPreBytes;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes)
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
-  // per-stream scratch: the replicate kernels' work counter and the pre-drawn rows (two-kernel
-  // path), so cells enqueued on different streams run concurrently without sharing either
+  // per-stream scratch: everything a launch writes besides its caller-owned outputs (the work
+  // counter, the pre-drawn rows of the two-kernel path, the overflow slab of replicate_kernel, the
+  // selection state, its candidates and single-call outputs), so cells and selections enqueued
+  // on different streams run concurrently without sharing any of it
   struct Scratch {
     unsigned long long* work = nullptr;
     void* pre = nullptr;
     size_t pre_bytes = 0;
+    uint16_t* slab = nullptr;
+    size_t slab_bytes = 0;
+    zks::SelectState* sel = nullptr;
+    double* sel_out = nullptr;
+    void* cand = nullptr;  // selection candidates (keys matching a 16-bit prefix)
+    size_t cand_bytes = 0;
   };
   std::map<cudaStream_t, Scratch> scratch;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
   int select_blocks = 0;            // resident grid of the cooperative selection kernel
-  void* cand = nullptr;             // selection candidates (keys matching a 16-bit prefix)
-  size_t cand_bytes = 0;
   zks::SelectBatch dist{};          // the distributed selection in progress (zks_select_dist_*)
+  zks::SelectState* dist_sel = nullptr;  // ... and the state it works in (its stream's scratch)
   bool dist_active = false;
   int dist_blocks = 1;
   // per-kernel timing (zks_engine_set_timing): event pairs around launches on the engine stream
@@ -144,8 +148,14 @@ cudaError_t scratch_for(zks_engine* e, zks_engine::Scratch** out) {
   auto it = e->scratch.find(e->stream);
   if (it == e->scratch.end()) {
     zks_engine::Scratch sc;
-    const cudaError_t err = cudaMalloc(&sc.work, sizeof(unsigned long long));
-    if (err != cudaSuccess) return err;
+    cudaError_t err = cudaMalloc(&sc.work, sizeof(unsigned long long));
+    if (err == cudaSuccess) err = cudaMalloc(&sc.sel, sizeof(zks::SelectState));
+    if (err == cudaSuccess) err = cudaMalloc(&sc.sel_out, zks::kMaxRanks * sizeof(double));
+    if (err != cudaSuccess) {
+      cudaFree(sc.work);
+      cudaFree(sc.sel);
+      return err;
+    }
     it = e->scratch.emplace(e->stream, sc).first;
   }
   *out = &it->second;
@@ -188,7 +198,23 @@ struct zks_table {
   uint32_t len = 0;
   double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
   uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on staged 32-bit words
+  // stream ordering: the upload (and guide build) runs on `home`; another stream's first use
+  // waits on `ready`; the free waits on every stream that used the table
+  cudaStream_t home = nullptr;
+  cudaEvent_t ready = nullptr;
+  mutable std::vector<cudaStream_t> users;
 };
+
+namespace {
+// order the engine stream's coming use of table t after its upload
+cudaError_t table_use(zks_engine* e, const zks_table* t) {
+  if (e->stream == t->home) return cudaSuccess;
+  if (std::find(t->users.begin(), t->users.end(), e->stream) != t->users.end()) return cudaSuccess;
+  const cudaError_t err = cudaStreamWaitEvent(e->stream, t->ready, 0);
+  if (err == cudaSuccess) t->users.push_back(e->stream);
+  return err;
+}
+}  // namespace
 
 extern "C" {
 
@@ -213,7 +239,6 @@ int zks_engine_create(int device, const double* logs_host, int64_t logs_len, zks
   cudaError_t err = cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaMalloc(&e->logs, kLogsLen * sizeof(double));
   if (err == cudaSuccess) err = cudaMemcpy(e->logs, logs_host, kLogsLen * sizeof(double), cudaMemcpyHostToDevice);
-  if (err == cudaSuccess) err = cudaMalloc(&e->sel, sizeof(zks::SelectState));
   if (err == cudaSuccess) err = cudaMallocHost(&e->staging, kStagingSlots * kStagingLen * sizeof(double));
   for (int i = 0; i < kStagingSlots && err == cudaSuccess; ++i)
     err = cudaEventCreateWithFlags(&e->staging_done[i], cudaEventDisableTiming);
@@ -230,15 +255,17 @@ void zks_engine_destroy(zks_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
+  cudaDeviceSynchronize();  // queued work on every stream that used this engine's scratch
   cudaFree(e->logs);
-  cudaFree(e->slab);
-  cudaFree(e->sel);
-  cudaFree(e->sel_out);
   for (auto& kv : e->scratch) {
-    cudaFree(kv.second.work);
-    if (kv.second.pre) cudaFree(kv.second.pre);
+    zks_engine::Scratch& sc = kv.second;
+    cudaFree(sc.work);
+    if (sc.pre) cudaFree(sc.pre);
+    cudaFree(sc.slab);
+    cudaFree(sc.sel);
+    cudaFree(sc.sel_out);
+    if (sc.cand) cudaFree(sc.cand);
   }
-  if (e->cand) cudaFree(e->cand);
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
   for (auto& t : e->timed) {
@@ -262,6 +289,12 @@ int zks_engine_sync(zks_engine* e) {
   if (!e) return fail(ZKS_EINVAL, "engine is NULL");
   ZKS_CUDA(cudaSetDevice(e->device));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
+  return ZKS_OK;
+}
+
+int zks_engine_set_chunk_bytes(zks_engine* e, uint64_t bytes) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  e->pre_cap = bytes ? bytes : kPreBytes;
   return ZKS_OK;
 }
 
@@ -338,6 +371,9 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
       err = launched(e);
     }
   }
+  t->home = e->stream;
+  if (err == cudaSuccess) err = cudaEventCreateWithFlags(&t->ready, cudaEventDisableTiming);
+  if (err == cudaSuccess) err = cudaEventRecord(t->ready, e->stream);
   if (err != cudaSuccess) {
     zks_table_destroy(t);
     return fail(ZKS_ECUDA, "table upload failed: %s", cudaGetErrorString(err));
@@ -349,9 +385,25 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
 void zks_table_destroy(zks_table* t) {
   if (!t) return;
   if (t->engine && t->cdf) {
-    cudaSetDevice(t->engine->device);
-    cudaFreeAsync(t->cdf, t->engine->stream);  // ordered after every queued use of the table
+    zks_engine* e = t->engine;
+    cudaSetDevice(e->device);
+    // the free runs on the engine's current stream after every queued use on the others
+    std::vector<cudaStream_t> others = t->users;
+    others.push_back(t->home);
+    for (cudaStream_t s : others) {
+      if (s == e->stream) continue;
+      cudaEvent_t ev = nullptr;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaDeviceSynchronize();
+        break;
+      }
+      cudaEventRecord(ev, s);
+      cudaStreamWaitEvent(e->stream, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    cudaFreeAsync(t->cdf, e->stream);
   }
+  if (t->ready) cudaEventDestroy(t->ready);
   delete t;
 }
 
@@ -412,6 +464,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   if (c->count == 0) return ZKS_OK;
   if (!ks_dev || !gh_dev || !st_dev) return fail(ZKS_EINVAL, "output pointer is NULL");
   ZKS_CUDA(cudaSetDevice(e->device));
+  ZKS_CUDA(table_use(e, t));
 
   zks::ReplicateArgs a;
   a.cdf = t->cdf;
@@ -506,22 +559,22 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   blocks = std::min<int64_t>(blocks, (int64_t)((c->count + per_block - 1) / per_block));
   a.slab = nullptr;
   a.slab_cap = 0;
-  if (!batched && L > static_cast<uint32_t>(a.H)) {
-    // worst case every draw of a replicate lands above the histogram: capacity n per warp
+  if (!batched && !two_kernel && L > static_cast<uint32_t>(a.H)) {
+    // replicate_kernel: worst case every draw of a replicate lands above the histogram, so
+    // capacity n per warp (the two-kernel path keeps its tails in the pre-drawn rows instead)
     const size_t per_warp = size_t(c->n) * sizeof(uint16_t);
     int64_t max_blocks = int64_t(kSlabBudget / (per_warp * zks::kWarps));
     if (max_blocks < 1) return fail(ZKS_EINVAL, "sample size %lld too large for the overflow slab", (long long)c->n);
     blocks = std::min(blocks, max_blocks);
     const size_t need = per_warp * zks::kWarps * size_t(blocks);
-    if (need > e->slab_bytes) {
-      ZKS_CUDA(cudaStreamSynchronize(e->stream));
-      cudaFree(e->slab);
-      e->slab = nullptr;
-      e->slab_bytes = 0;
-      ZKS_CUDA(cudaMalloc(&e->slab, need));
-      e->slab_bytes = need;
+    if (need > sc->slab_bytes) {  // stream-ordered: no device-wide synchronisation
+      if (sc->slab) ZKS_CUDA(cudaFreeAsync(sc->slab, e->stream));
+      sc->slab = nullptr;
+      sc->slab_bytes = 0;
+      ZKS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc->slab), need, e->stream));
+      sc->slab_bytes = need;
     }
-    a.slab = e->slab;
+    a.slab = sc->slab;
     a.slab_cap = c->n;
   }
   a.pre_head = nullptr;
@@ -542,7 +595,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     // then fit + score, then the listed retries; chunk by chunk.  Per row: u16 head counts
     // (128 B), log-sum, min / max / m, the tail values, a retry-list slot.
     const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(a.vals_stride) * 2 + 4;
-    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, kPreBytes / row_bytes));
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, e->pre_cap / row_bytes));
     const size_t need = size_t(chunk) * row_bytes + 16;
     if (need > sc->pre_bytes) {
       if (sc->pre) ZKS_CUDA(cudaFreeAsync(sc->pre, e->stream));
@@ -640,7 +693,8 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
 // the full arrays' lengths the ranks refer to when this GPU holds shards
 int select_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,
                  const int64_t* ranks_host, int32_t nranks, double* const* out_dev, const uint8_t* const* status_dev,
-                 uint8_t* const* worst_dev, const int64_t* global_counts, zks::SelectBatch* out) {
+                 uint8_t* const* worst_dev, const int64_t* global_counts, zks::SelectBatch* out,
+                 zks::SelectState** sel, double** sel_out) {
   if (!e || !values_dev || !counts || !ranks_host || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
   if (narrays < 1 || narrays > zks::kSelMaxArrays)
     return fail(ZKS_EINVAL, "narrays %d outside [1, %d]", narrays, zks::kSelMaxArrays);
@@ -666,16 +720,20 @@ int select_batch(zks_engine* e, const double* const* values_dev, const int64_t* 
     }
   }
   ZKS_CUDA(cudaSetDevice(e->device));
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
   int64_t total = 0;
   for (int a = 0; a < narrays; ++a) total += counts[a];
-  if (size_t(total) * 8 > e->cand_bytes) {
-    if (e->cand) ZKS_CUDA(cudaFreeAsync(e->cand, e->stream));
-    e->cand = nullptr;
-    e->cand_bytes = 0;
-    ZKS_CUDA(cudaMallocAsync(&e->cand, std::max<size_t>(size_t(total) * 8, 8), e->stream));
-    e->cand_bytes = std::max<size_t>(size_t(total) * 8, 8);
+  if (size_t(total) * 8 > sc->cand_bytes) {
+    if (sc->cand) ZKS_CUDA(cudaFreeAsync(sc->cand, e->stream));
+    sc->cand = nullptr;
+    sc->cand_bytes = 0;
+    ZKS_CUDA(cudaMallocAsync(&sc->cand, std::max<size_t>(size_t(total) * 8, 8), e->stream));
+    sc->cand_bytes = std::max<size_t>(size_t(total) * 8, 8);
   }
-  B.cand = static_cast<unsigned long long*>(e->cand);
+  B.cand = static_cast<unsigned long long*>(sc->cand);
+  *sel = sc->sel;
+  *sel_out = sc->sel_out;
   return ZKS_OK;
 }
 
@@ -687,8 +745,10 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
                            const int64_t* ranks_host, int32_t nranks, double* const* out_dev,
                            const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
   zks::SelectBatch B;
+  zks::SelectState* st = nullptr;
+  double* unused = nullptr;
   const int rc = select_batch(e, values_dev, counts, narrays, ranks_host, nranks, out_dev, status_dev, worst_dev,
-                              nullptr, &B);
+                              nullptr, &B, &st, &unused);
   if (rc) return rc;
   int64_t most = 0;
   for (int a = 0; a < narrays; ++a) most = std::max<int64_t>(most, counts[a]);
@@ -702,7 +762,6 @@ int zks_select_ranks_batch(zks_engine* e, const double* const* values_dev, const
       std::max<int64_t>(1, std::min<int64_t>(e->select_blocks, (most * narrays + 255) / 256)));
   {
     Timed tm(e, ZKS_KERNEL_SELECT);
-    zks::SelectState* st = e->sel;
     void* args[] = {&B, &st};
     ZKS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(zks::select_kernel), dim3(blocks), dim3(256),
                                          args, 0, e->stream));
@@ -721,8 +780,9 @@ int zks_select_dist_begin(zks_engine* e, const double* const* values_dev, const 
                           double* const* out_dev, const uint8_t* const* status_dev, uint8_t* const* worst_dev) {
   if (!global_counts) return fail(ZKS_EINVAL, "NULL argument");
   zks::SelectBatch B;
+  double* unused = nullptr;
   const int rc = select_batch(e, values_dev, counts, narrays, ranks_host, nranks, out_dev, status_dev, worst_dev,
-                              global_counts, &B);
+                              global_counts, &B, &e->dist_sel, &unused);
   if (rc) return rc;
   e->dist = B;
   e->dist_active = true;
@@ -730,7 +790,7 @@ int zks_select_dist_begin(zks_engine* e, const double* const* values_dev, const 
   for (int a = 0; a < narrays; ++a) most = std::max<int64_t>(most, counts[a]);
   e->dist_blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 2, (most * narrays + 255) / 256)));
   Timed tm(e, ZKS_KERNEL_SELECT);
-  zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->sel);
+  zks::select_init_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->dist_sel);
   ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
@@ -740,7 +800,7 @@ int zks_select_dist_count(zks_engine* e, int32_t pass, uint32_t* hist_dev) {
   if (!e->dist_active || pass < 0 || pass >= zks::kSelectPasses) return fail(ZKS_EINVAL, "no selection pass %d", pass);
   ZKS_CUDA(cudaSetDevice(e->device));
   Timed tm(e, ZKS_KERNEL_SELECT);
-  zks::select_count_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->sel, pass, hist_dev);
+  zks::select_count_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->dist_sel, pass, hist_dev);
   ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
@@ -752,12 +812,12 @@ int zks_select_dist_pick(zks_engine* e, int32_t pass, const uint32_t* hist_dev) 
   {
     Timed tm(e, ZKS_KERNEL_SELECT);
     const int slots = e->dist.narrays * e->dist.nr;
-    zks::select_pick_kernel<<<(unsigned)((slots + 7) / 8), 256, 0, e->stream>>>(e->dist, e->sel, pass, hist_dev);
+    zks::select_pick_kernel<<<(unsigned)((slots + 7) / 8), 256, 0, e->stream>>>(e->dist, e->dist_sel, pass, hist_dev);
     ZKS_CUDA(launched(e));
   }
   if (pass == 1) {
     Timed tm(e, ZKS_KERNEL_SELECT);
-    zks::select_compact_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->sel);
+    zks::select_compact_kernel<<<(unsigned)e->dist_blocks, 256, 0, e->stream>>>(e->dist, e->dist_sel);
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
@@ -769,7 +829,7 @@ int zks_select_dist_end(zks_engine* e) {
   ZKS_CUDA(cudaSetDevice(e->device));
   e->dist_active = false;
   Timed tm(e, ZKS_KERNEL_SELECT);
-  zks::select_out_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->sel);
+  zks::select_out_kernel<<<1, 256, 0, e->stream>>>(e->dist, e->dist_sel);
   ZKS_CUDA(launched(e));
   return ZKS_OK;
 }
@@ -778,10 +838,11 @@ int zks_select_ranks(zks_engine* e, const double* values_dev, int64_t count, con
                      int32_t nranks, double* out_host) {
   if (!e || !out_host) return fail(ZKS_EINVAL, "NULL argument");
   ZKS_CUDA(cudaSetDevice(e->device));
-  if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
-  const int rc = zks_select_ranks_async(e, values_dev, count, ranks_host, nranks, e->sel_out);
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  const int rc = zks_select_ranks_async(e, values_dev, count, ranks_host, nranks, sc->sel_out);
   if (rc) return rc;
-  ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, nranks * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  ZKS_CUDA(cudaMemcpyAsync(out_host, sc->sel_out, nranks * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
   return ZKS_OK;
 }
@@ -794,13 +855,14 @@ int zks_normaliser(zks_engine* e, double gamma, int32_t support_k, double* out_h
   if (support_k == 0 && gamma < zks::kMinUnboundedGamma)
     return fail(ZKS_EINVAL, "unbounded support requires gamma >= 1.05, got %g", gamma);
   ZKS_CUDA(cudaSetDevice(e->device));
-  if (!e->sel_out) ZKS_CUDA(cudaMalloc(&e->sel_out, zks::kMaxRanks * sizeof(double)));
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
   {
     Timed tm(e, ZKS_KERNEL_OTHER);
-    zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, e->sel_out);
+    zks::normaliser_kernel<<<1, 32, 0, e->stream>>>(gamma, support_k, e->logs, sc->sel_out);
     ZKS_CUDA(launched(e));
   }
-  ZKS_CUDA(cudaMemcpyAsync(out_host, e->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  ZKS_CUDA(cudaMemcpyAsync(out_host, sc->sel_out, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   ZKS_CUDA(cudaStreamSynchronize(e->stream));
   return ZKS_OK;
 }
@@ -852,7 +914,22 @@ int zks_stream_uniforms(zks_engine* e, uint64_t seed, uint64_t rep, uint64_t idx
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (nb + 255) / 256));
   {
     Timed tm(e, ZKS_KERNEL_OTHER);
-    zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, count, out_dev);
+    zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, rep, idx, 0, count, out_dev);
+    ZKS_CUDA(launched(e));
+  }
+  return ZKS_OK;
+}
+
+int zks_stream_uniforms_key(zks_engine* e, uint64_t k0, uint64_t k1, int64_t count, double* out_dev) {
+  if (!e || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (count < 0) return fail(ZKS_EINVAL, "count must be >= 0");
+  if (count == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t nb = (count + 3) / 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (nb + 255) / 256));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(k0, k1, 0, 1, count, out_dev);
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
@@ -863,6 +940,7 @@ int zks_draw(zks_engine* e, const zks_table* t, const double* u_dev, int64_t cou
   if (count < 0) return fail(ZKS_EINVAL, "count must be >= 0");
   if (count == 0) return ZKS_OK;
   ZKS_CUDA(cudaSetDevice(e->device));
+  ZKS_CUDA(table_use(e, t));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (count + 255) / 256));
   {
     Timed tm(e, ZKS_KERNEL_OTHER);

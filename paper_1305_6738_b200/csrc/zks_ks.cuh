@@ -18,6 +18,7 @@
 // E(k) = C(k) / n and the head F(k) as the running sum of (k^-g * (1/norm)), as the reference
 // writes them, so trivial samples reproduce the reference's exact values (0, 2/3, ...).
 #pragma once
+#include <type_traits>
 #include <cstdint>
 
 #include "zks_series.cuh"
@@ -254,11 +255,13 @@ __device__ __forceinline__ void bitonic_sort_warp(uint32_t (&r)[kOverCap / 32], 
 // KS of one sample with counts of 1..H in `hist`; values above H are found in
 // over_vals[0..over_n) (which may also hold values <= H: they are ignored).  `queue` is
 // kKsQueueWords u32 of per-warp shared memory.  `hist` is left dirty (see used_pages).
-// kCompact: over_vals is the caller's scratch; each page pass keeps only the values above its
-// page (compacted in place), so later passes read the remaining tail instead of all of it.
+// kCompact: over_vals is the caller's scratch (hence non-const); each page pass keeps only the
+// values above its page (compacted in place), so later passes read the remaining tail instead of
+// all of it, and the caller's list is consumed.
 template <typename VT, bool kArg, bool kCompact = false>
 __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax, uint32_t* hist,
-                         const VT* over_vals, uint32_t over_n, uint32_t* queue, int lane, Work& wk) {
+                         typename std::conditional<kCompact, VT*, const VT*>::type over_vals, uint32_t over_n,
+                         uint32_t* queue, int lane, Work& wk) {
   KsCtx c;
   c.g = g;
   c.inv = 1.0 / norm;
@@ -420,9 +423,9 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       for (int i = lane; i < p.hist_words; i += 32) hist[i] = 0u;
       __syncwarp();
       uint64_t next = ~0ull;
-      if (kCompact) {
+      if constexpr (kCompact) {
         const unsigned lt = (1u << lane) - 1u;
-        VT* keep_out = const_cast<VT*>(over_vals);
+        VT* keep_out = over_vals;
         uint32_t kept = 0;
         for (uint32_t i0 = 0; i0 < over_n; i0 += 32) {
           const uint32_t i = i0 + lane;

@@ -68,9 +68,10 @@ struct ReplicateArgs {
   uint64_t ubuf_first;
   // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: u16 counts of
   // the values 1..kKsHead at pre_head[i * kKsHead] (128-byte rows), the m = pre_m[i] values
-  // above kKsHead at pre_tail[i * vals_stride], log-sum / min / max
+  // above kKsHead at pre_tail[i * vals_stride], log-sum / min / max.  pre_tail is consumed:
+  // fit_ks_kernel's page passes compact a long tail in place (ks_scan<..., kCompact>)
   const uint16_t* pre_head;
-  const uint16_t* pre_tail;
+  uint16_t* pre_tail;
   const uint32_t* pre_m;
   const double* pre_ls;
   const uint32_t* pre_min;
@@ -468,9 +469,10 @@ __global__ void guide_kernel(const double* __restrict__ cdf, uint32_t L, uint16_
 }
 
 // RandomStream.uniforms (distribution.py:186-187) for one stream, block-parallel
-__global__ void uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t idx, int64_t count, double* out) {
-  uint64_t k0, k1;
-  stream_key(seed, rep, idx, k0, k1);
+// keyed = 1: (seed, rep) is the Philox key itself (host-derived SeedSequence of another key)
+__global__ void uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t idx, int keyed, int64_t count, double* out) {
+  uint64_t k0 = seed, k1 = rep;
+  if (!keyed) stream_key(seed, rep, idx, k0, k1);
   const int64_t nb = (count + 3) >> 2;
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
        b += static_cast<int64_t>(gridDim.x) * blockDim.x) {

@@ -153,16 +153,23 @@ class RandomStream:
 
     Bit-exact with ``numpy.random.Generator(Philox(SeedSequence(key))).random`` as the
     reference uses it (distribution.py:173-187).  Successive ``uniforms`` calls continue
-    the stream.
+    the stream.  Replicate keys ``[base_seed, repetition, index]`` are hashed on the device
+    (the hot path's derivation); any other SeedSequence entropy the reference accepts (an int,
+    a sequence of any length) gets its Philox key from numpy's SeedSequence on the host -- the
+    reference's own dependency -- and its uniforms from the device.
     """
 
-    __slots__ = ("_key", "_offset")
+    __slots__ = ("_key", "_philox", "_offset")
 
     def __init__(self, key) -> None:
-        key = [int(key)] if isinstance(key, (int, np.integer)) else [int(x) for x in key]
-        if len(key) != 3 or any(not 0 <= x < 1 << 64 for x in key):
-            raise ValueError("device streams are keyed by [base_seed, repetition, index], each in [0, 2**64)")
-        self._key = tuple(key)
+        words = [int(key)] if isinstance(key, (int, np.integer)) else [int(x) for x in key]
+        self._philox = None
+        if len(words) == 3 and all(0 <= x < 1 << 64 for x in words):
+            self._key = tuple(words)
+        else:
+            k = np.random.SeedSequence(key).generate_state(2, np.uint64)  # raises as the reference does
+            self._key = None
+            self._philox = (int(k[0]), int(k[1]))
         self._offset = 0
 
     @classmethod
@@ -177,7 +184,10 @@ class RandomStream:
         eng = get_engine()
         total = self._offset + int(count)
         buf = torch.empty(max(total, 1), dtype=torch.float64, device=f"cuda:{eng.device}")
-        eng.uniforms(*self._key, total, buf)
+        if self._philox is not None:
+            eng.uniforms_key(*self._philox, total, buf)
+        else:
+            eng.uniforms(*self._key, total, buf)
         out = buf[self._offset : total].cpu().numpy()
         self._offset = total
         return out

@@ -246,6 +246,15 @@ class Engine:
         _native.check(self.lib.zks_stream_uniforms(self.handle, int(seed), int(repetition), int(index), int(count),
                                                    out.data_ptr()))
 
+    def set_chunk_bytes(self, nbytes: int = 0) -> None:
+        """Budget of one chunk of pre-drawn rows (0 = the default 4 GiB); results never depend on it."""
+        _native.check(self.lib.zks_engine_set_chunk_bytes(self.handle, int(nbytes)))
+
+    def uniforms_key(self, k0: int, k1: int, count: int, out) -> None:
+        """Uniforms of an explicit Philox key (a host-derived SeedSequence of any other key)."""
+        self.bind_stream()
+        _native.check(self.lib.zks_stream_uniforms_key(self.handle, int(k0), int(k1), int(count), out.data_ptr()))
+
     def draw(self, table: DrawTable, u, out) -> None:
         self.bind_stream()
         _native.check(self.lib.zks_draw(self.handle, table.handle, u.data_ptr(), u.numel(), out.data_ptr()))

@@ -204,8 +204,10 @@ def order_quantiles(stats, levels: Sequence[float]) -> list[float]:
     """Order statistics at zero-based ranks floor(R * level) (montecarlo.py:119-136).
 
     ``stats`` may be a sequence, a numpy array or a CUDA float64 tensor; the selection runs
-    on the device (radix select over the order-preserving bit patterns of the values, so
-    the values must be non-negative, as KS statistics are).
+    on the device: a radix select over order-preserving 64-bit keys of the values.  For
+    non-negative values (KS statistics) the key is the IEEE bit pattern itself; any other input
+    is selected on sign-flipped keys (negative values: all bits inverted; others: the sign bit
+    set), with NaNs canonicalised to sort last, as ``np.sort`` orders them.
     """
     torch = _torch()
     on_device = isinstance(stats, torch.Tensor) and stats.is_cuda
@@ -217,15 +219,26 @@ def order_quantiles(stats, levels: Sequence[float]) -> list[float]:
     ranks = quantile_ranks(count, levels)
     eng = _engine()
     if on_device:
-        values = stats.to(torch.float64).contiguous()
+        values = stats.to(torch.float64).contiguous().reshape(-1)
     else:
-        values = torch.from_numpy(arr).to(f"cuda:{eng.device}")
-    if bool((values < 0).any()) or bool(torch.isnan(values).any()):
-        raise ValueError("order_quantiles on the device needs non-negative, non-NaN values")
-    values = values + 0.0  # canonicalise -0.0 to +0.0 (order-preserving bit patterns)
+        values = torch.from_numpy(arr.reshape(-1)).to(f"cuda:{eng.device}")
+    values = values + 0.0  # canonicalise -0.0 to +0.0 (np.sort treats them as equal)
+    nan = torch.isnan(values)
+    signed = bool((values < 0).any()) or bool(nan.any())
+    if signed:
+        bits = torch.where(nan, torch.full_like(values, float("nan")), values).view(torch.int64)
+        sign = torch.tensor(-(1 << 63), dtype=torch.int64, device=values.device)
+        keys = torch.where(bits < 0, ~bits, bits ^ sign).view(torch.float64)
+    else:
+        keys = values
     out = []
     for i in range(0, len(ranks), 16):
-        out.extend(eng.select_ranks(values, ranks[i : i + 16]))
+        chunk = torch.empty(len(ranks[i : i + 16]), dtype=torch.float64, device=values.device)
+        eng.select_ranks(keys, ranks[i : i + 16], out=chunk)
+        if signed:  # back from keys: a set top bit marks a non-negative value
+            kb = chunk.view(torch.int64)
+            chunk = torch.where(kb < 0, kb ^ sign, ~kb).view(torch.float64)
+        out.extend(float(x) for x in chunk.cpu().tolist())
     return out
 
 
@@ -239,8 +252,14 @@ class _CellPlan:
     host: object = None        # (quantiles, worst) copied to the host by _fetch_plans
 
 
+def _keep(keep, cfg, rep, slab, first, stop) -> None:
+    """Test hook: a stream-ordered copy of one (cell, repetition)'s per-replicate outputs."""
+    if keep is not None:
+        keep[(cfg.gamma, cfg.n, rep)] = tuple(t[first:stop].clone() for t in (slab.ks, slab.gh, slab.st))
+
+
 def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, reduce=None,
-                  kernel_events: list | None = None) -> None:
+                  kernel_events: list | None = None, keep: dict | None = None) -> None:
     """Queue every repetition of one cell: replicates -> selection, all async.
 
     ``shard`` = (first, stop) restricts this process to replicate indices [first, stop); the
@@ -269,27 +288,31 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, re
             if kernel_events is not None:
                 k1.record(stream)
                 kernel_events.append((k0, k1))
-            plan.worst[rep] = slab.st[first:stop].max()
-        if reduce is None:
-            for i in range(0, len(ranks), 16):
-                eng.select_ranks(slab.ks[:total], ranks[i : i + 16], out=plan.quantiles[rep, i : i + 16])
-        else:
-            eng.select_dist([(slab.ks[first:stop], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
-                             for i in range(0, len(ranks), 16)], total, reduce)
+            _keep(keep, cfg, rep, slab, first, stop)
+        # the selection launch also reduces the repetition's worst status (first rank chunk)
+        jobs = [(slab.ks[first:stop], ranks[i : i + 16], plan.quantiles[rep, i : i + 16])
+                + ((slab.st[first:stop], plan.worst[rep : rep + 1]) if i == 0 else ())
+                for i in range(0, len(ranks), 16)]
+        for job in jobs:  # rank chunks differ in length: one launch each
+            if reduce is None:
+                eng.select_many([job])
+            else:
+                eng.select_dist([job], total, reduce)
     plan.finished.record(stream)
 
 
 # n range whose sweep rows share staged draw words.  Below 128 the lane-per-replicate kernel
 # regenerates its streams: strided per-lane reads of staged rows measured slower than Philox there.
 _STAGE_MIN_N, _STAGE_MAX_N = 128, 16384
-_STAGE_BYTES = 8 << 30                   # staging buffer budget (one chunk per 10^6-replicate row up to n = 2000)
+_STAGE_BYTES = 8 << 30                   # staging buffer budget (one chunk per 10^6-replicate row up to n = 2000;
+                                         # tests shrink it to force chunked rows)
 
 
 def _stage_key(cfg: SimulationConfig):
     return (cfg.support.k, cfg.n, cfg.base_seed, cfg.replicates, cfg.repetitions, cfg.quantiles)
 
 
-def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None) -> None:
+def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
     """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
@@ -304,7 +327,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
     staged = _STAGE_MIN_N <= n <= _STAGE_MAX_N
     if len(plans) < 2:
         for plan in plans:
-            _enqueue_cell(eng, plan, shard=shard, reduce=reduce, kernel_events=kernel_events)
+            _enqueue_cell(eng, plan, shard=shard, reduce=reduce, kernel_events=kernel_events, keep=keep)
         return
     total = cfg0.replicates
     first, stop = shard if shard is not None else (0, total)
@@ -350,6 +373,8 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
                 if kernel_events is not None:
                     k1.record(stream)
                     kernel_events.append((k0, k1))
+        for plan, out in zip(plans, outs):
+            _keep(keep, plan.config, rep, out, first, stop)
         # the row's cells in batched selections; the first rank chunk also takes the worst status
         # (multi-GPU: over this rank's shard, digit histograms summed by `reduce`; the worst
         # status is this rank's, all-reduced by the caller)
@@ -388,14 +413,14 @@ def _prefetch_tables(eng, configs) -> None:
         _PENDING[(eng.device, *key)] = _POOL.submit(sampling_cdf, cfg.gamma, cfg.support)
 
 
-def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None) -> None:
+def _enqueue_plans(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
     """Queue many cells, grouping those that can share uniform streams (_enqueue_group)."""
     _prefetch_tables(eng, [p.config for p in plans])
     groups: dict = {}
     for plan in plans:
         groups.setdefault(_stage_key(plan.config), []).append(plan)
     for group in groups.values():
-        _enqueue_group(eng, group, shard=shard, reduce=reduce, kernel_events=kernel_events)
+        _enqueue_group(eng, group, shard=shard, reduce=reduce, kernel_events=kernel_events, keep=keep)
 
 
 def _fetch_plans(plans: list[_CellPlan]) -> None:

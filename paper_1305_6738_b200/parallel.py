@@ -27,7 +27,9 @@ from .montecarlo import (
     SimulationError,
     _CellPlan,
     _engine,
+    _enqueue,
     _enqueue_plans,
+    _failure,
     _fetch_plans,
     _finish_cell,
     _slab,
@@ -123,19 +125,48 @@ def build_table(
     shard = shard_bounds(replicates, world, rank)
     _slab(eng, padded_size(replicates, world))
     _enqueue_plans(eng, plans, shard=shard, reduce=histogram_reducer(group))
-    worst = torch.stack([p.worst.max() for p in plans]).to(torch.int32)
+    # every rank's worst status per (cell, repetition), so every rank raises the same error
+    worst = torch.stack([p.worst for p in plans]).to(torch.int32)
     dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
-    for plan, w in zip(plans, worst.tolist()):
-        plan.worst.fill_(w if w < _native.STATUS_FAILED else 0)
+    worst_host = worst.cpu().numpy()
+    for plan, w in zip(plans, worst_host):
+        plan.worst.copy_(torch.from_numpy(np.where(w < _native.STATUS_FAILED, w, 0).astype(np.uint8)))
     _fetch_plans(plans)
     cells = {}
-    for plan, w in zip(plans, worst.tolist()):
+    for plan, w in zip(plans, worst_host):
         cfg = plan.config
-        if w >= _native.STATUS_FAILED:
-            raise SimulationError(f"table cell (gamma={cfg.gamma}, n={cfg.n}) failed: a replicate failed twice")
+        if w.max() >= _native.STATUS_FAILED:
+            err = _first_failure(eng, cfg, int(np.flatnonzero(w >= _native.STATUS_FAILED)[0]), shard, group)
+            raise SimulationError(f"table cell (gamma={cfg.gamma}, n={cfg.n}) failed: {err}") from err
         cells[(cfg.gamma, cfg.n)] = tuple(c for _, c in _finish_cell(eng, plan, shard=shard))
     return CutoffTable(support=support, levels=levels, gammas=gammas, ns=ns, cells=cells, replicates=replicates,
                        repetitions=repetitions, base_seed=base_seed)
+
+
+def _first_failure(eng, cfg: SimulationConfig, repetition: int, shard: tuple[int, int], group) -> SimulationError:
+    """The reference's error for the first replicate of ``repetition`` that failed twice
+    (montecarlo.py:106-116), agreed by every rank: each re-runs its shard of that repetition,
+    an all-reduce MIN finds the first failing index and its owner contributes the mean log."""
+    import torch
+    import torch.distributed as dist
+
+    first, stop = shard
+    slab = _slab(eng, cfg.replicates)
+    idx, mean_log = cfg.replicates, 0.0
+    if stop > first:
+        _enqueue(eng, cfg, repetition, first, stop - first, slab, offset=first)
+        st = slab.st[first:stop].cpu().numpy()
+        bad = np.flatnonzero(st == _native.STATUS_FAILED)
+        if bad.size:
+            idx = first + int(bad[0])
+            mean_log = float(slab.gh[idx : idx + 1].cpu().numpy()[0])
+    dev = f"cuda:{eng.device}"
+    at = torch.tensor([idx], dtype=torch.int64, device=dev)
+    dist.all_reduce(at, op=dist.ReduceOp.MIN, group=group)
+    idx0 = int(at.item())
+    ml = torch.tensor([mean_log if idx == idx0 else 0.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(ml, op=dist.ReduceOp.SUM, group=group)
+    return _failure(cfg, repetition, idx0, float(ml.item()))
 
 
 def gathered_order(values_by_rank: list[np.ndarray], total: int) -> np.ndarray:

@@ -212,3 +212,18 @@ def test_fit_bespoke(zk):
     cfg = zk.SimulationConfig(n=500, support=zk.Support.unbounded(), gamma=report.gamma_hat, base_seed=5,
                               replicates=20000, repetitions=2)
     assert [c for _, c in zk.run_simulation(cfg)] == cut
+
+
+@pytest.mark.parametrize("key", [5, 0, [1, 2, 3, 4, 5], [7], [], 2**100, [2**64 - 1, 3, 2**32 + 7], [1, 2, 2**64]])
+def test_random_stream_any_seedsequence_key(zk, key):
+    # RandomStream takes whatever SeedSequence takes (distribution.py:173-180); continuing calls
+    # continue the stream
+    want = 1.0 - np.random.Generator(np.random.Philox(np.random.SeedSequence(key))).random(23)
+    s = zk.RandomStream(key)
+    got = np.concatenate([s.uniforms(5), s.uniforms(18)])
+    assert got.tobytes() == want.tobytes()
+
+
+def test_random_stream_rejects_what_seedsequence_rejects(zk):
+    with pytest.raises(ValueError):
+        zk.RandomStream([-1, 2, 3])

@@ -9,6 +9,7 @@ Tiers (BASELINE.json north_star):
 All calls go through the C ABI (libzks_b200.so).
 """
 import os
+import re
 
 import numpy as np
 import pytest
@@ -213,6 +214,28 @@ def test_order_quantiles_exact(zk):
     assert zk.order_quantiles(dup, [0.1, 0.5, 0.9]) == port.order_quantiles(dup, [0.1, 0.5, 0.9])
     with pytest.raises(ValueError):
         zk.order_quantiles([], [0.9])
+
+
+def test_order_quantiles_signed_and_nan(zk):
+    # the reference sorts any float64 array (montecarlo.py:119-136): negative values, -0.0,
+    # infinities and NaNs (last, as np.sort puts them) select like np.sort
+    from oracle import port
+
+    rng = np.random.default_rng(23)
+    levels = (0.001, 0.1, 0.25, 0.5, 0.75, 0.9, 0.95, 0.99, 0.999)
+    for count in (100, 4097, 300000):
+        x = rng.standard_normal(count) * 10.0 ** rng.integers(-300, 300, count)
+        x[::7] = -0.0
+        x[::11] = 0.0
+        x[3::13] = -np.inf
+        x[5::17] = np.inf
+        want = port.order_quantiles(x, levels)
+        np.testing.assert_array_equal(zk.order_quantiles(x, levels), want)
+        x[1::5] = np.nan
+        x[2::9] = -np.nan
+        np.testing.assert_array_equal(zk.order_quantiles(x, levels), port.order_quantiles(x, levels))
+    neg = -rng.random(1000)
+    np.testing.assert_array_equal(zk.order_quantiles(neg, levels), port.order_quantiles(neg, levels))
 
 
 def test_double_failure_raises_with_diagnostics(zk):
@@ -421,3 +444,159 @@ def test_distributed_select_over_shards_matches_whole_array(zk, split):
     for out in outs:
         assert out.cpu().tolist() == want.cpu().tolist()
     engines[1].close()
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_slab_and_selection_on_two_streams_match_sequential(zk, direct):
+    # every scratch buffer a launch writes (overflow slab of replicate_kernel at n > 65535 and in
+    # direct-MLE mode, selection state and candidates) is per stream; tables built on one stream
+    # are waited for by the first use on another
+    import torch
+
+    from paper_1305_6738_b200 import engine
+    from paper_1305_6738_b200.distribution import Support, sampling_cdf
+
+    eng = engine.get_engine()
+    cells = [(None, 1.5, 70000, 24), (None, 1.3, 66000, 24), (None, 1.7, 700, 600), (1000, 0.9, 3000, 600)]
+    ranks = [3, 10, 20]
+
+    def run(streams, fresh):
+        outs = []
+        if fresh:
+            eng.clear_tables()
+        for i, (K, g, n, R) in enumerate(cells):
+            with torch.cuda.stream(streams[i % len(streams)]):
+                table = eng.table(g, K, lambda: sampling_cdf(g, Support(K)))  # built on this stream
+                ks = torch.empty(R, dtype=torch.float64, device="cuda")
+                gh = torch.empty_like(ks)
+                st = torch.empty(R, dtype=torch.uint8, device="cuda")
+                q = torch.empty(len(ranks), dtype=torch.float64, device="cuda")
+                eng.run_replicates(table, K, g, n, 5, 0, 0, R, ks, gh, st)
+                eng.select_ranks(ks, ranks, out=q)
+                outs.append((ks, gh, st, q))
+        torch.cuda.synchronize()
+        eng.bind_stream()
+        return [tuple(x.cpu().numpy() for x in o) for o in outs]
+
+    eng.set_mle_mode(direct)
+    try:
+        seq = run([torch.cuda.current_stream()], True)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        par = run([s1, s2], True)
+        par2 = run([s2, s1], False)  # tables now used on the other stream
+    finally:
+        eng.set_mle_mode(False)
+    for a, b, c in zip(seq, par, par2):
+        for x, y, z in zip(a, b, c):
+            np.testing.assert_array_equal(x, y)
+            np.testing.assert_array_equal(x, z)
+
+
+def test_parallel_build_table_failure_names_the_replicate(zk):
+    # multi-GPU build_table raises the single-GPU (reference) message: first failing replicate,
+    # its repetition and mean log (montecarlo.py:106-116), agreed over the ranks
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_6738_b200 import parallel
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        kw = dict(ns=(3,), gammas=(1.0, -30.0), support=zk.Support.finite(20), base_seed=5, replicates=100,
+                  repetitions=2)
+        with pytest.raises(zk.SimulationError) as single:
+            zk.build_table(**kw)
+        with pytest.raises(zk.SimulationError) as multi:
+            parallel.build_table(**kw)
+        assert str(multi.value) == str(single.value)
+        assert re.search(r"failed: replicate \d+ \(repetition 0, gamma=-30.0, n=3, support=20\) failed twice: "
+                         r"estimating equation has no root .*\(mean log of data: ", str(multi.value))
+    finally:
+        dist.destroy_process_group()
+
+
+def _row_outputs(zk, K, n, gammas, R, seed=3):
+    """Per-replicate (ks, gamma_hat, status) of a sweep row through build_table's scheduler."""
+    import torch
+
+    from paper_1305_6738_b200 import montecarlo as mc
+
+    eng = mc._engine()
+    plans = [mc._CellPlan(zk.SimulationConfig(n=n, support=zk.Support(K), gamma=g, base_seed=seed, replicates=R,
+                                              repetitions=1)) for g in gammas]
+    keep = {}
+    mc._enqueue_plans(eng, plans, keep=keep)
+    torch.cuda.synchronize()
+    return {g: tuple(t.cpu().numpy() for t in keep[(g, n, 0)]) for g in gammas}
+
+
+@pytest.mark.parametrize("K,n", [(None, 300), (None, 5000), (None, 12000), (1000, 300), (1000, 5000), (1000, 12000)])
+def test_chunked_rows_match_single_chunk(zk, monkeypatch, K, n):
+    # the staged words and the pre-drawn rows both run in >= 3 chunks (budgets shrunk): every
+    # replicate's (ks, gamma_hat, status) equals the single-chunk run's and the unstaged cell's
+    from paper_1305_6738_b200 import montecarlo as mc
+
+    R = 20000 if n <= 5000 else 6000
+    gammas = (0.8, 1.6) if K else (1.6, 2.5)
+    eng = mc._engine()
+    whole = _row_outputs(zk, K, n, gammas, R)
+    stride = eng.staging_stride(n)
+    monkeypatch.setattr(mc, "_STAGE_BYTES", 4 * stride * (R // 3 + 1))  # 3 staging chunks
+    eng.set_chunk_bytes(max(1, (R // 4) * (200 + 4 * n)))  # >= 4 pre-drawn row chunks
+    try:
+        chunked = _row_outputs(zk, K, n, gammas, R)
+    finally:
+        eng.set_chunk_bytes(0)
+    for g in gammas:
+        for a, b in zip(whole[g], chunked[g]):
+            np.testing.assert_array_equal(a, b)
+        cell = run_cell(K, g, n, 3, 0, 0, R)
+        for a, b in zip(whole[g], cell):
+            np.testing.assert_array_equal(a, b)
+        assert (whole[g][2] == 0).mean() > 0.99
+
+
+@pytest.mark.parametrize("direct", [False, True])
+@pytest.mark.parametrize("gamma,n,idxs", [(2.0, 1_000_000, (0, 1, 2)), (1.5, 100_000, (0, 7)), (1.3, 70_000, (3,))])
+def test_large_n_per_replicate_oracle_parity(zk, direct, gamma, n, idxs):
+    # n > 65535 (BASELINE config 4 at n = 10^6; heavy tails through the overflow slab and its
+    # in-place page compaction): per replicate against the oracle at 1e-10
+    from oracle import port
+    from paper_1305_6738_b200 import engine
+
+    eng = engine.get_engine()
+    eng.set_mle_mode(direct)
+    try:
+        for i in idxs:
+            ks, gh, st = run_cell(None, gamma, n, 1, 0, i, 1)
+            want_ks, want_gh, want_st = port.replicate(gamma, None, n, 1, i, 0)
+            assert st[0] == want_st
+            assert close(ks[0], want_ks), (i, ks[0], want_ks)
+            assert close(gh[0], want_gh), (i, gh[0], want_gh)
+    finally:
+        eng.set_mle_mode(False)
+
+
+@pytest.mark.parametrize("K", [100, 500, 1000])
+def test_truncated_corner_negative_gamma_hat(zk, K):
+    # K in {100, 500, 1000}, gamma = 0.25, n = 10: gamma_hat is often negative (the finite
+    # bracket [-20, 20]) and values above 64 are scored past the lane-walk head
+    from oracle import port
+
+    R = 400
+    ks, gh, st = run_cell(K, 0.25, 10, 1, 0, 0, R)
+    neg = 0
+    for i in range(R):
+        want_ks, want_gh, want_st = port.replicate(0.25, K, 10, 1, i, 0)
+        assert st[i] == want_st, i
+        assert close(ks[i], want_ks), (i, ks[i], want_ks)
+        assert close(gh[i], want_gh), (i, gh[i], want_gh)
+        neg += want_gh < 0
+    assert neg > R // 10
