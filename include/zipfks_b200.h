@@ -76,7 +76,7 @@ int zks_engine_launches(zks_engine* engine, unsigned long long* out);
  * engine stream; zks_engine_kernel_times synchronises the stream, writes the summed milliseconds
  * and launch counts per kind (arrays of ZKS_KERNEL_KINDS) since the last call, and resets. */
 enum {
-  ZKS_KERNEL_STAGE = 0,  /* stage_uniforms_kernel: staged draw words of a sweep */
+  ZKS_KERNEL_ROW = 0,    /* row_draw_kernel: a row's streams drawn + sorted once, counted per cell */
   ZKS_KERNEL_DRAW = 1,   /* draw_stats_kernel: samples -> head counts, tail values, log-sums */
   ZKS_KERNEL_FIT = 2,    /* fit_ks_kernel: exponent fits + KS of pre-drawn rows */
   ZKS_KERNEL_RETRY = 3,  /* retry_kernel: second attempts */
@@ -104,19 +104,17 @@ void zks_table_destroy(zks_table* table);
 int zks_run_replicates(zks_engine* engine, const zks_table* table, const zks_cell* cell, double* ks_dev,
                        double* gamma_hat_dev, uint8_t* status_dev);
 
-/* Sweeps: the cells of build_table share base_seed (montecarlo.py:276-277), so cells with the
- * same n and repetition consume identical uniform streams.  zks_stage_uniforms writes the
- * draws of replicate indices [first, first+count) once as 32-bit words -- the top half of each
- * Philox word, t = x >> 32 (row i = index first+i, n words, row stride zks_staging_stride(n)
- * words); zks_run_replicates_staged then runs one cell's replicates from them instead of
- * regenerating the streams (a replicate whose words leave a draw undecided is redrawn from
- * Philox).  Results are identical to zks_run_replicates.  Both asynchronous. */
-int64_t zks_staging_stride(int64_t n);
-int zks_stage_uniforms(zks_engine* engine, uint64_t base_seed, uint64_t repetition, uint64_t first, uint64_t count,
-                       int64_t n, uint32_t* words_dev);
-int zks_run_replicates_staged(zks_engine* engine, const zks_table* table, const zks_cell* cell, const uint32_t* words_dev,
-                              uint64_t u_first, uint64_t u_count, double* ks_dev, double* gamma_hat_dev,
-                              uint8_t* status_dev);
+/* Sweep rows: the cells of build_table share base_seed (montecarlo.py:276-277), so cells with
+ * the same n and repetition consume identical uniform streams.  One call runs replicates
+ * [first, first+count) of ncells (<= 32) such cells -- cells[j] must differ only in gamma, with
+ * tables[j] its sampling table and ks_dev[j] / gamma_hat_dev[j] / status_dev[j] its outputs as
+ * in zks_run_replicates.  For 128 <= n <= 16384 each replicate's stream is drawn and its 53-bit
+ * keys sorted ONCE on chip, and every cell's counts come from where its cdf cuts fall among
+ * them; other sizes run cell by cell.  Results equal zks_run_replicates per cell bit for bit
+ * (single cells of that size take the same kernel).  Replaces build_table's per-cell
+ * run_simulation loop (montecarlo.py:263-314, 194-212) for one row.  Asynchronous. */
+int zks_run_cells(zks_engine* engine, int32_t ncells, const zks_table* const* tables, const zks_cell* cells,
+                  double* const* ks_dev, double* const* gamma_hat_dev, uint8_t* const* status_dev);
 
 /* Order statistics at zero-based `ranks_host[i]` of `count` non-negative doubles, written to
  * out_host[i].  Replaces the np.sort + index of order_quantiles (montecarlo.py:119-136); the
@@ -166,7 +164,7 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * uint64): RandomStream(key) for keys other than [seed, repetition, index] (distribution.py:
  * 173-180 accepts any SeedSequence entropy; the host derives the key, the device the uniforms).
  * Asynchronous. */
-/* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (default 4 GiB,
+/* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (default 16 GiB,
  * 0 restores it): a cell whose rows exceed it runs chunk by chunk.  Results do not depend on it. */
 int zks_engine_set_chunk_bytes(zks_engine* engine, uint64_t bytes);
 

@@ -14,7 +14,7 @@ ZKS_OK, ZKS_EINVAL, ZKS_ECUDA = 0, 1, 2
 STATUS_OK, STATUS_RETRIED, STATUS_FAILED = 0, 1, 2
 MLE_TABLE, MLE_DIRECT = 0, 1
 KERNEL_KINDS = ("stage", "draw", "fit", "retry", "batch", "single", "select", "other")  # ZKS_KERNEL_*
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # every symbol include/zipfks_b200.h declares
 EXPORTS = (
@@ -30,9 +30,7 @@ EXPORTS = (
     "zks_table_create",
     "zks_table_destroy",
     "zks_run_replicates",
-    "zks_staging_stride",
-    "zks_stage_uniforms",
-    "zks_run_replicates_staged",
+    "zks_run_cells",
     "zks_select_ranks",
     "zks_select_ranks_async",
     "zks_select_ranks_batch",
@@ -112,10 +110,7 @@ def load() -> ctypes.CDLL:
     lib.zks_table_destroy.argtypes = [vp]
     lib.zks_table_destroy.restype = None
     lib.zks_run_replicates.argtypes = [vp, vp, ctypes.POINTER(ZksCell), dp, dp, dp]
-    lib.zks_staging_stride.argtypes = [i64]
-    lib.zks_staging_stride.restype = i64
-    lib.zks_stage_uniforms.argtypes = [vp, u64, u64, u64, u64, i64, dp]
-    lib.zks_run_replicates_staged.argtypes = [vp, vp, ctypes.POINTER(ZksCell), dp, u64, u64, dp, dp, dp]
+    lib.zks_run_cells.argtypes = [vp, i32, dp, dp, dp, dp, dp]
     lib.zks_select_ranks.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_async.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp, dp, dp]
@@ -137,8 +132,7 @@ def load() -> ctypes.CDLL:
     lib.zks_fit_eval.argtypes = [vp, i32, dp, i64, dp, dp, dp]
     lib.zks_probe_peaks.argtypes = [vp, dp]
     for name in EXPORTS:
-        if name not in ("zks_version", "zks_last_error", "zks_engine_destroy", "zks_table_destroy",
-                        "zks_staging_stride"):
+        if name not in ("zks_version", "zks_last_error", "zks_engine_destroy", "zks_table_destroy"):
             getattr(lib, name).restype = ctypes.c_int
     if lib.zks_version() != ABI_VERSION:
         raise ImportError(f"{LIB}: ABI version {lib.zks_version()} != {ABI_VERSION}; rebuild")

@@ -13,6 +13,7 @@
 #include "../../include/zipfks_b200.h"
 #include "zks_replicate.cuh"
 #include "zks_batch.cuh"
+#include "zks_rows.cuh"
 #include "zks_samples.cuh"
 #include "zks_select.cuh"
 #include "zks_probe.cuh"
@@ -45,11 +46,8 @@ constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
 constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
-constexpr int64_t kBatchMaxN = 1024;                  // n up to which the lane-batch layout applies
-                                                      // (replicate_batch_kernel below kLaneDrawMaxN,
-                                                      // retry_kernel's layout on the two-kernel path)
-constexpr uint64_t kPreBytes = uint64_t(4) << 30;     // pre-drawn rows per chunk (bytes)
-constexpr uint32_t kBatchHist = 512;                  // its per-warp histogram bins
+constexpr uint64_t kPreBytes = uint64_t(16) << 30;    // pre-drawn rows per chunk (bytes)
+constexpr uint32_t kBatchHist = 512;                  // batch / retry histogram bins above K = 1024
 
 }  // namespace
 
@@ -67,7 +65,7 @@ struct zks_engine {
   int mle_mode = ZKS_MLE_TABLE;
   uint64_t pre_cap = kPreBytes;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes)
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
-  std::map<std::pair<const void*, size_t>, int> occupancy;  // (kernel, smem) -> blocks per SM
+  std::map<std::tuple<const void*, size_t, int>, int> occupancy;  // (kernel, smem, threads) -> blocks per SM
   // per-stream scratch: everything a launch writes besides its caller-owned outputs (the work
   // counter, the pre-drawn rows of the two-kernel path, the overflow slab of replicate_kernel, the
   // selection state, its candidates and single-call outputs), so cells and selections enqueued
@@ -197,7 +195,8 @@ struct zks_table {
   uint16_t* guide = nullptr;
   uint32_t len = 0;
   double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
-  uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on staged 32-bit words
+  uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on the top 32 bits of Philox words
+  unsigned long long* mcut = nullptr;  // exact 53-bit cuts of cdf[0..63] (row_draw_kernel)
   // stream ordering: the upload (and guide build) runs on `home`; another stream's first use
   // waits on `ready`; the free waits on every stream that used the table
   cudaStream_t home = nullptr;
@@ -218,7 +217,7 @@ cudaError_t table_use(zks_engine* e, const zks_table* t) {
 
 extern "C" {
 
-int zks_version(void) { return 2; }
+int zks_version(void) { return 3; }
 
 const char* zks_last_error(void) { return g_error.c_str(); }
 
@@ -347,10 +346,13 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;
   const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
-  cudaError_t err = cudaMallocAsync(&mem, cdf_slots * sizeof(double) + zks::kGuideEntries * sizeof(uint16_t), e->stream);
+  const size_t guide_bytes = (size_t(zks::kGuideEntries) * sizeof(uint16_t) + 15) & ~size_t(15);
+  cudaError_t err =
+      cudaMallocAsync(&mem, cdf_slots * sizeof(double) + guide_bytes + 64 * sizeof(unsigned long long), e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
     t->guide = reinterpret_cast<uint16_t*>(t->cdf + cdf_slots);
+    t->mcut = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(t->guide) + guide_bytes);
   }
   if (err == cudaSuccess) {
     // stage through a pinned slot so the copy never waits for kernels already queued
@@ -368,6 +370,11 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
     {
       Timed tm(e, ZKS_KERNEL_OTHER);
       zks::guide_kernel<<<(zks::kGuideEntries + 255) / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->guide);
+      err = launched(e);
+    }
+    if (err == cudaSuccess) {
+      Timed tm(e, ZKS_KERNEL_OTHER);
+      zks::cut_kernel<<<1, 64, 0, e->stream>>>(t->cdf, t->len, t->mcut);
       err = launched(e);
     }
   }
@@ -407,66 +414,25 @@ void zks_table_destroy(zks_table* t) {
   delete t;
 }
 
-namespace {
-struct Staged {
-  const uint32_t* u;
-  int64_t stride;
-  uint64_t first, count;
-  int64_t n;
-};
-int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
-                        uint8_t* st_dev, const Staged* staged);
-}  // namespace
-
-int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
-                       uint8_t* st_dev) {
-  return run_replicates_impl(e, t, c, ks_dev, gh_dev, st_dev, nullptr);
-}
-
-int64_t zks_staging_stride(int64_t n) { return (n + 3) / 4 * 4; }
-
-int zks_stage_uniforms(zks_engine* e, uint64_t seed, uint64_t repetition, uint64_t first, uint64_t count, int64_t n,
-                       uint32_t* u_dev) {
-  if (!e || !u_dev) return fail(ZKS_EINVAL, "NULL argument");
-  if (n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)n);
-  if (count == 0) return ZKS_OK;
-  ZKS_CUDA(cudaSetDevice(e->device));
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 8, (int64_t)((count + 7) / 8)));
-  {
-    Timed tm(e, ZKS_KERNEL_STAGE);
-    zks::stage_uniforms_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(seed, repetition, first, count, n,
-                                                                       zks_staging_stride(n), u_dev, e->counters);
-    ZKS_CUDA(launched(e));
-  }
-  return ZKS_OK;
-}
-
-int zks_run_replicates_staged(zks_engine* e, const zks_table* t, const zks_cell* c, const uint32_t* u_dev,
-                              uint64_t u_first, uint64_t u_count, double* ks_dev, double* gh_dev, uint8_t* st_dev) {
-  if (!u_dev) return fail(ZKS_EINVAL, "NULL argument");
-  if (!c) return fail(ZKS_EINVAL, "cell is NULL");
-  const Staged s{u_dev, zks_staging_stride(c->n), u_first, u_count, c->n};
-  return run_replicates_impl(e, t, c, ks_dev, gh_dev, st_dev, &s);
-}
-
 }  // extern "C"
 
 namespace {
 
-int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
-                        uint8_t* st_dev, const Staged* staged) {
-  if (!e || !t || !c) return fail(ZKS_EINVAL, "engine/table/cell is NULL");
+int check_cell(const zks_table* t, const zks_cell* c) {
+  if (!t || !c) return fail(ZKS_EINVAL, "table/cell is NULL");
   if (c->n < 1) return fail(ZKS_EINVAL, "sample size must be >= 1, got %lld", (long long)c->n);
   if (c->support_k < 0 || c->support_k == 1 || c->support_k > 32766)
     return fail(ZKS_EINVAL, "finite support bound must be in [2, 32766], got %d", c->support_k);
   const uint32_t L = c->support_k ? static_cast<uint32_t>(c->support_k) : 65535u;
   if (t->len != L) return fail(ZKS_EINVAL, "table length %u does not match support (%u)", t->len, L);
-  if (c->count == 0) return ZKS_OK;
-  if (!ks_dev || !gh_dev || !st_dev) return fail(ZKS_EINVAL, "output pointer is NULL");
-  ZKS_CUDA(cudaSetDevice(e->device));
-  ZKS_CUDA(table_use(e, t));
+  return ZKS_OK;
+}
 
-  zks::ReplicateArgs a;
+// the per-cell launch arguments every replicate kernel shares
+int cell_args(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev, uint8_t* st_dev,
+              zks_engine::Scratch* sc, zks::ReplicateArgs& a) {
+  const uint32_t L = t->len;
+  a = zks::ReplicateArgs{};
   a.cdf = t->cdf;
   a.guide = t->guide;
   a.guide_fine = t->guide + 2 * zks::kGuideLevel;
@@ -489,46 +455,254 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   a.ks_out = ks_dev;
   a.gh_out = gh_dev;
   a.st_out = st_dev;
-  zks_engine::Scratch* sc = nullptr;
-  ZKS_CUDA(scratch_for(e, &sc));
   a.work = sc->work;
   a.counters = e->counters;
-  a.ubuf = nullptr;
-  a.ubuf_stride = 0;
-  a.ubuf_first = 0;
-  if (staged) {
-    if (c->first < staged->first || c->first + c->count > staged->first + staged->count || staged->n != c->n)
-      return fail(ZKS_EINVAL, "staged uniforms do not cover replicates [%llu, %llu) of n = %lld",
-                  (unsigned long long)c->first, (unsigned long long)(c->first + c->count), (long long)c->n);
-    a.ubuf = staged->u;
-    a.ubuf_stride = staged->stride;
-    a.ubuf_first = staged->first;
-  }
+  a.guide_levels = L > 4096u ? 2 : 1;
   a.use_table = e->mle_mode == ZKS_MLE_TABLE;
   if (a.use_table) {
     zks::FitTable* T = nullptr;
     const int rc = fit_table_for(e, c->support_k, &T);
     if (rc) return rc;
     a.fit = *T;
-  } else {
-    a.fit = zks::FitTable{};
   }
+  return ZKS_OK;
+}
 
+// blocks per SM of a kernel at a dynamic shared-memory size (cached; sets the opt-in ceiling)
+int occupancy_of(zks_engine* e, const void* kernel, size_t smem, int threads, int* per) {
+  const auto key = std::make_tuple(kernel, smem, threads);
+  auto it = e->occupancy.find(key);
+  if (it == e->occupancy.end()) {
+    int optin = 0;
+    ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    cudaFuncAttributes fa;
+    ZKS_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);  // dynamic ceiling next to the static smem
+    if (smem > size_t(dyn_max)) return fail(ZKS_EINVAL, "kernel needs %zu B of shared memory (%d available)", smem, dyn_max);
+    ZKS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+    int p = 0;
+    ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, kernel, threads, smem));
+    if (p < 1) return fail(ZKS_ECUDA, "kernel does not fit (smem %zu)", smem);
+    it = e->occupancy.emplace(key, p).first;
+  }
+  *per = it->second;
+  return ZKS_OK;
+}
+
+// The two-kernel layout (kLaneDrawMaxN <= n <= kPreMaxN, table MLE) for ncells cells of one row
+// (equal n, support, seed, repetition and replicate range; gammas differ): per chunk of
+// replicates the draw phase writes every cell's pre-drawn rows -- row_draw_kernel (n <=
+// kRowMaxN: each stream drawn and sorted once for all cells) or draw_stats_kernel per cell --
+// then per cell fit_ks_kernel and retry_kernel.
+int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                 double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+  const zks_cell& c0 = cells[0];
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  const bool rows = c0.n <= zks::kRowMaxN;
+  std::vector<zks::ReplicateArgs> args(ncells);
+  for (int j = 0; j < ncells; ++j) {
+    ZKS_CUDA(table_use(e, tables[j]));
+    const int rc = cell_args(e, tables[j], &cells[j], ks_dev[j], gh_dev[j], st_dev[j], sc, args[j]);
+    if (rc) return rc;
+  }
+  // finite supports up to 1024 fit the retry histogram whole; otherwise 512 bins + ordered overflow
+  const uint32_t L = tables[0]->len;
+  int H = static_cast<int>(L <= 1024u ? L : kBatchHist);
+  int hist_words = std::max(zks::round_up(std::max(H, 4) + 1, 4), zks::kLaneHistWords);
+  int vals_stride = zks::round_up(static_cast<int>(c0.n), 4);
+  int dense_words = 0;
+  // finite supports above the head and up to kDenseMaxK: dense counts instead of value lists
+  if (c0.support_k > static_cast<int>(zks::kKsHead) && c0.support_k <= zks::kDenseMaxK) {
+    dense_words = c0.support_k - static_cast<int>(zks::kKsHead);
+    vals_stride = std::max(vals_stride, zks::round_up(2 * dense_words, 4));
+  }
+  for (auto& a : args) {
+    a.H = H;
+    a.hist_words = hist_words;
+    a.vals_stride = vals_stride;
+    a.batch = 32;
+    a.dense_words = dense_words;
+    a.slab = nullptr;
+    a.slab_cap = 0;
+  }
   const bool counting = e->counters != nullptr;
-  const bool batched = a.use_table && c->n <= kBatchMaxN;
-  const bool two_kernel = a.use_table && c->n >= zks::kLaneDrawMaxN && c->n <= zks::kPreMaxN;
-  a.guide_levels = L > 4096u ? 2 : 1;
+  const size_t guide_bytes = zks::round_up(args[0].guide_levels * zks::kGuideLevel * 2, 16);
+  // per row and cell: u16 head counts (128 B), log-sum, min / max / m, the tail slot, a
+  // retry-list slot; per cell region 256-byte aligned
+  const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(vals_stride) * 2 + 4;
+  const uint64_t chunk =
+      std::max<uint64_t>(1, std::min<uint64_t>(c0.count, e->pre_cap / (row_bytes * uint64_t(ncells))));
+  const size_t region = (size_t(chunk) * row_bytes + 16 + 255) & ~size_t(255);
+  const size_t need = region * size_t(ncells);
+  if (need > sc->pre_bytes) {
+    if (sc->pre) ZKS_CUDA(cudaFreeAsync(sc->pre, e->stream));
+    sc->pre = nullptr;
+    sc->pre_bytes = 0;
+    ZKS_CUDA(cudaMallocAsync(&sc->pre, need, e->stream));
+    sc->pre_bytes = need;
+  }
+  struct Pre {
+    uint16_t* head;
+    double* ls;
+    uint32_t *mn, *mx, *m;
+    uint16_t* tail;
+    uint32_t* retry;
+  };
+  std::vector<Pre> pre(ncells);
+  for (int j = 0; j < ncells; ++j) {
+    unsigned char* base = static_cast<unsigned char*>(sc->pre) + region * j;
+    Pre& p = pre[j];
+    p.head = reinterpret_cast<uint16_t*>(base);
+    p.ls = reinterpret_cast<double*>(p.head + chunk * zks::kKsHead);
+    p.mn = reinterpret_cast<uint32_t*>(p.ls + chunk);
+    p.mx = p.mn + chunk;
+    p.m = p.mx + chunk;
+    p.tail = reinterpret_cast<uint16_t*>(p.m + chunk);
+    p.retry = reinterpret_cast<uint32_t*>(p.tail + chunk * vals_stride);  // vals_stride % 4 == 0
+  }
+  // the retry kernel's per-warp sample store grows with n: fewer warps per block for large n
+  const int rwarps = static_cast<int>(std::max<size_t>(
+      1, std::min<size_t>(zks::kWarps, (size_t(227) * 1024 - guide_bytes) /
+                                           size_t(zks::retry_warp_bytes(hist_words, vals_stride)))));
+  auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
+  auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
+  const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
+  const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(hist_words, vals_stride);
+  int fper = 0, rper = 0;
+  if (int rc = occupancy_of(e, reinterpret_cast<const void*>(fit), fsmem, zks::kThreads, &fper)) return rc;
+  if (int rc = occupancy_of(e, reinterpret_cast<const void*>(again), rsmem, 32 * rwarps, &rper)) return rc;
+  // draw phase
+  const bool wide = c0.n > zks::kNarrowBinsMaxN;
+  auto draw = counting ? (wide ? zks::draw_stats_kernel<true, true> : zks::draw_stats_kernel<true, false>)
+                       : (wide ? zks::draw_stats_kernel<false, true> : zks::draw_stats_kernel<false, false>);
+  const size_t dsmem = zks::round_up(zks::kGuideLevel * 2, 16) + (size_t(4) << zks::kCutTabBits) +
+                       size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(dense_words) * 4);
+  auto rowk = counting ? zks::row_draw_kernel<true> : zks::row_draw_kernel<false>;
+  // warps per row block: each takes cells w, w + W, ...; W in 4..8 with the fewest idle cell slots
+  int row_warps = 4;
+  for (int w = 4; w <= zks::kWarps; ++w)
+    if ((ncells + w - 1) / w * w - ncells <= (ncells + row_warps - 1) / row_warps * row_warps - ncells) row_warps = w;
+  const size_t rsmem_row = zks::row_smem_bytes(static_cast<int>(c0.n), dense_words, row_warps);
+  int dper = 0;
+  if (rows) {
+    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), rsmem_row, 32 * row_warps, &dper)) return rc;
+  } else {
+    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(draw), dsmem, zks::kThreads, &dper)) return rc;
+  }
+  zks::RowArgs ra{};
+  if (rows) {
+    ra.seed = c0.base_seed;
+    ra.rep = c0.repetition;
+    ra.n = static_cast<int>(c0.n);
+    ra.vals_stride = vals_stride;
+    ra.dense_words = dense_words;
+    ra.ncells = ncells;
+    ra.bucket_bits = zks::row_bucket_bits(ra.n);
+    ra.logs = e->logs;
+    ra.counters = e->counters;
+    for (int j = 0; j < ncells; ++j) {
+      zks::RowCell& rc = ra.cell[j];
+      rc.cdf = tables[j]->cdf;
+      rc.guide = tables[j]->guide;
+      rc.guide_fine = tables[j]->guide + 2 * zks::kGuideLevel;
+      rc.mcut = tables[j]->mcut;
+      rc.L = tables[j]->len;
+      rc.guide_levels = args[j].guide_levels;
+    }
+  }
+  for (uint64_t off = 0; off < c0.count; off += chunk) {
+    const uint64_t cnt = std::min<uint64_t>(chunk, c0.count - off);
+    std::vector<zks::ReplicateArgs> sub(args);
+    for (int j = 0; j < ncells; ++j) {
+      zks::ReplicateArgs& s = sub[j];
+      s.first = c0.first + off;
+      s.count = cnt;
+      s.ks_out = ks_dev[j] + off;
+      s.gh_out = gh_dev[j] + off;
+      s.st_out = st_dev[j] + off;
+      s.pre_head = pre[j].head;
+      s.pre_tail = pre[j].tail;
+      s.pre_m = pre[j].m;
+      s.pre_ls = pre[j].ls;
+      s.pre_min = pre[j].mn;
+      s.pre_max = pre[j].mx;
+      s.pre_first = s.first;
+    }
+    if (rows) {
+      ra.first = c0.first + off;
+      ra.count = cnt;
+      for (int j = 0; j < ncells; ++j) {
+        zks::RowCell& rc = ra.cell[j];
+        rc.head = pre[j].head;
+        rc.tail = pre[j].tail;
+        rc.m = pre[j].m;
+        rc.ls = pre[j].ls;
+        rc.mn = pre[j].mn;
+        rc.mx = pre[j].mx;
+      }
+      const int64_t rblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)cnt));
+      Timed tm(e, ZKS_KERNEL_ROW);
+      rowk<<<(unsigned)rblocks, 32 * row_warps, rsmem_row, e->stream>>>(ra);
+      ZKS_CUDA(launched(e));
+    } else {
+      for (int j = 0; j < ncells; ++j) {
+        const zks::ReplicateArgs& s = sub[j];
+        const int64_t dblocks =
+            std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)((cnt + 7) / 8)));
+        Timed tm(e, ZKS_KERNEL_DRAW);
+        draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(s, pre[j].head, pre[j].tail, pre[j].m,
+                                                                     pre[j].ls, pre[j].mn, pre[j].mx);
+        ZKS_CUDA(launched(e));
+      }
+    }
+    const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * fper, (int64_t)((cnt + 255) / 256)));
+    for (int j = 0; j < ncells; ++j) {
+      ZKS_CUDA(cudaMemsetAsync(sub[j].work, 0, sizeof(unsigned long long), e->stream));
+      ZKS_CUDA(cudaMemsetAsync(pre[j].retry, 0, sizeof(uint32_t), e->stream));
+      {
+        Timed tm(e, ZKS_KERNEL_FIT);
+        fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub[j], pre[j].retry);
+        ZKS_CUDA(launched(e));
+      }
+      {
+        Timed tm(e, ZKS_KERNEL_RETRY);
+        again<<<(unsigned)e->sms, 32 * rwarps, rsmem, e->stream>>>(sub[j], pre[j].retry);
+        ZKS_CUDA(launched(e));
+      }
+    }
+  }
+  return ZKS_OK;
+}
+
+int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
+                        uint8_t* st_dev) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  if (int rc = check_cell(t, c)) return rc;
+  if (c->count == 0) return ZKS_OK;
+  if (!ks_dev || !gh_dev || !st_dev) return fail(ZKS_EINVAL, "output pointer is NULL");
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const bool table_mode = e->mle_mode == ZKS_MLE_TABLE;
+  if (table_mode && c->n >= zks::kLaneDrawMaxN && c->n <= zks::kPreMaxN)
+    return run_pre_rows(e, 1, &t, c, &ks_dev, &gh_dev, &st_dev);
+  ZKS_CUDA(table_use(e, t));
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  zks::ReplicateArgs a;
+  if (int rc = cell_args(e, t, c, ks_dev, gh_dev, st_dev, sc, a)) return rc;
+  const uint32_t L = t->len;
+  const bool counting = e->counters != nullptr;
+  const bool batched = table_mode && c->n < zks::kLaneDrawMaxN;
   const size_t guide_bytes = zks::round_up(a.guide_levels * zks::kGuideLevel * 2, 16);
   void (*kernel)(zks::ReplicateArgs);
   size_t smem;
   int64_t per_block;  // replicates one block takes per work item round
-  if (batched || two_kernel) {
+  if (batched) {
     // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
-    // (the histogram of the batch kernel, and of retry_kernel on the two-kernel path)
     a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
     a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
     a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
-    a.batch = 32;  // one replicate per lane (n < kLaneDrawMaxN)
+    a.batch = 32;  // one replicate per lane
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
     smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride);
     per_block = int64_t(zks::kWarps) * a.batch;
@@ -540,28 +714,14 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     per_block = zks::kWarps;
   }
   int per_sm = 0;
-  if (!two_kernel) {
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), smem);
-    auto it = e->occupancy.find(key);
-    if (it == e->occupancy.end()) {
-      // one per-function ceiling for every launch size (the attribute is not per launch)
-      int optin = 0;
-      ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-      if (smem > size_t(optin)) return fail(ZKS_EINVAL, "replicate kernel needs %zu B of shared memory", smem);
-      ZKS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-      ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, zks::kThreads, smem));
-      if (per_sm < 1) return fail(ZKS_ECUDA, "replicate kernel does not fit (smem %zu)", smem);
-      it = e->occupancy.emplace(key, per_sm).first;
-    }
-    per_sm = it->second;
-  }
+  if (int rc = occupancy_of(e, reinterpret_cast<const void*>(kernel), smem, zks::kThreads, &per_sm)) return rc;
   int64_t blocks = int64_t(e->sms) * std::max(per_sm, 1);
   blocks = std::min<int64_t>(blocks, (int64_t)((c->count + per_block - 1) / per_block));
   a.slab = nullptr;
   a.slab_cap = 0;
-  if (!batched && !two_kernel && L > static_cast<uint32_t>(a.H)) {
+  if (!batched && L > static_cast<uint32_t>(a.H)) {
     // replicate_kernel: worst case every draw of a replicate lands above the histogram, so
-    // capacity n per warp (the two-kernel path keeps its tails in the pre-drawn rows instead)
+    // capacity n per warp
     const size_t per_warp = size_t(c->n) * sizeof(uint16_t);
     int64_t max_blocks = int64_t(kSlabBudget / (per_warp * zks::kWarps));
     if (max_blocks < 1) return fail(ZKS_EINVAL, "sample size %lld too large for the overflow slab", (long long)c->n);
@@ -577,109 +737,6 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     a.slab = sc->slab;
     a.slab_cap = c->n;
   }
-  a.pre_head = nullptr;
-  a.pre_tail = nullptr;
-  a.pre_m = nullptr;
-  a.pre_ls = nullptr;
-  a.pre_min = nullptr;
-  a.pre_max = nullptr;
-  a.pre_first = 0;
-  a.dense_words = 0;
-  if (two_kernel) {
-    // finite supports above the head and up to kDenseMaxK: dense counts instead of value lists
-    if (c->support_k > static_cast<int>(zks::kKsHead) && c->support_k <= zks::kDenseMaxK) {
-      a.dense_words = c->support_k - static_cast<int>(zks::kKsHead);
-      a.vals_stride = std::max(a.vals_stride, zks::round_up(2 * a.dense_words, 4));
-    }
-    // draw phase in its own high-occupancy kernel (head counts + tail values per replicate),
-    // then fit + score, then the listed retries; chunk by chunk.  Per row: u16 head counts
-    // (128 B), log-sum, min / max / m, the tail values, a retry-list slot.
-    const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(a.vals_stride) * 2 + 4;
-    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(c->count, e->pre_cap / row_bytes));
-    const size_t need = size_t(chunk) * row_bytes + 16;
-    if (need > sc->pre_bytes) {
-      if (sc->pre) ZKS_CUDA(cudaFreeAsync(sc->pre, e->stream));
-      sc->pre = nullptr;
-      sc->pre_bytes = 0;
-      ZKS_CUDA(cudaMallocAsync(&sc->pre, need, e->stream));
-      sc->pre_bytes = need;
-    }
-    uint16_t* phead = reinterpret_cast<uint16_t*>(sc->pre);
-    double* pls = reinterpret_cast<double*>(phead + chunk * zks::kKsHead);
-    uint32_t* pmin = reinterpret_cast<uint32_t*>(pls + chunk);
-    uint32_t* pmax = pmin + chunk;
-    uint32_t* pm = pmax + chunk;
-    uint16_t* ptail = reinterpret_cast<uint16_t*>(pm + chunk);
-    uint32_t* retry = reinterpret_cast<uint32_t*>(ptail + chunk * a.vals_stride);  // vals_stride % 4 == 0
-    const bool wide = c->n > zks::kNarrowBinsMaxN;
-    auto draw = counting ? (wide ? zks::draw_stats_kernel<true, true> : zks::draw_stats_kernel<true, false>)
-                         : (wide ? zks::draw_stats_kernel<false, true> : zks::draw_stats_kernel<false, false>);
-    // the retry kernel's per-warp sample store grows with n: fewer warps per block for large n
-    const int rwarps = static_cast<int>(std::max<size_t>(
-        1, std::min<size_t>(zks::kWarps, (size_t(227) * 1024 - guide_bytes) /
-                                             size_t(zks::retry_warp_bytes(a.hist_words, a.vals_stride)))));
-    auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
-    auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
-    const size_t dsmem = zks::round_up(zks::kGuideLevel * 2, 16) + (size_t(4) << zks::kCutTabBits) +
-                         size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(a.dense_words) * 4);
-    const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
-    const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(a.hist_words, a.vals_stride);
-    int dper = 0, fper = 0;
-    {
-      int optin = 0;
-      ZKS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
-      const std::pair<const void*, size_t> keys[3] = {{reinterpret_cast<const void*>(draw), dsmem},
-                                                      {reinterpret_cast<const void*>(fit), fsmem},
-                                                      {reinterpret_cast<const void*>(again), rsmem}};
-      for (const auto& key : keys) {
-        if (e->occupancy.find(key) != e->occupancy.end()) continue;
-        int per = 0;
-        ZKS_CUDA(cudaFuncSetAttribute(key.first, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-        ZKS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, key.first, zks::kThreads, key.second));
-        if (per < 1) return fail(ZKS_ECUDA, "batch kernel does not fit (smem %zu)", key.second);
-        e->occupancy.emplace(key, per);
-      }
-      dper = e->occupancy[keys[0]];
-      fper = e->occupancy[keys[1]];
-    }
-    zks::ReplicateArgs sub = a;
-    for (uint64_t off = 0; off < c->count; off += chunk) {
-      const uint64_t cnt = std::min<uint64_t>(chunk, c->count - off);
-      sub.first = c->first + off;
-      sub.count = cnt;
-      sub.ks_out = ks_dev + off;
-      sub.gh_out = gh_dev + off;
-      sub.st_out = st_dev + off;
-      sub.pre_head = phead;
-      sub.pre_tail = ptail;
-      sub.pre_m = pm;
-      sub.pre_ls = pls;
-      sub.pre_min = pmin;
-      sub.pre_max = pmax;
-      sub.pre_first = sub.first;
-      const int64_t dblocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * dper, (int64_t)((cnt + 7) / 8)));
-      {
-        Timed tm(e, ZKS_KERNEL_DRAW);
-        draw<<<(unsigned)dblocks, zks::kThreads, dsmem, e->stream>>>(sub, phead, ptail, pm, pls, pmin, pmax);
-        ZKS_CUDA(launched(e));
-      }
-      const int64_t fblocks =
-          std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * fper, (int64_t)((cnt + 255) / 256)));
-      ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
-      ZKS_CUDA(cudaMemsetAsync(retry, 0, sizeof(uint32_t), e->stream));
-      {
-        Timed tm(e, ZKS_KERNEL_FIT);
-        fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub, retry);
-        ZKS_CUDA(launched(e));
-      }
-      {
-        Timed tm(e, ZKS_KERNEL_RETRY);
-        again<<<(unsigned)e->sms, 32 * rwarps, rsmem, e->stream>>>(sub, retry);
-        ZKS_CUDA(launched(e));
-      }
-    }
-    return ZKS_OK;
-  }
   ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
   {
     Timed tm(e, batched ? ZKS_KERNEL_BATCH : ZKS_KERNEL_SINGLE);
@@ -689,6 +746,41 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   return ZKS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int zks_run_replicates(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
+                       uint8_t* st_dev) {
+  return run_replicates_impl(e, t, c, ks_dev, gh_dev, st_dev);
+}
+
+int zks_run_cells(zks_engine* e, int32_t ncells, const zks_table* const* tables, const zks_cell* cells,
+                  double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+  if (!e || !tables || !cells || !ks_dev || !gh_dev || !st_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (ncells < 1 || ncells > zks::kRowMaxCells)
+    return fail(ZKS_EINVAL, "ncells %d outside [1, %d]", ncells, zks::kRowMaxCells);
+  const zks_cell& c0 = cells[0];
+  for (int j = 0; j < ncells; ++j) {
+    if (int rc = check_cell(tables[j], &cells[j])) return rc;
+    const zks_cell& c = cells[j];
+    if (c.support_k != c0.support_k || c.n != c0.n || c.base_seed != c0.base_seed || c.repetition != c0.repetition ||
+        c.first != c0.first || c.count != c0.count)
+      return fail(ZKS_EINVAL, "cells of one call must differ only in gamma (cell %d)", j);
+    if (c.count && (!ks_dev[j] || !gh_dev[j] || !st_dev[j])) return fail(ZKS_EINVAL, "output pointer %d is NULL", j);
+  }
+  if (c0.count == 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  if (e->mle_mode == ZKS_MLE_TABLE && c0.n >= zks::kLaneDrawMaxN && c0.n <= zks::kRowMaxN)
+    return run_pre_rows(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
+  for (int j = 0; j < ncells; ++j)  // other sizes: cell by cell (independent streams per launch)
+    if (int rc = run_replicates_impl(e, tables[j], &cells[j], ks_dev[j], gh_dev[j], st_dev[j])) return rc;
+  return ZKS_OK;
+}
+
+}  // extern "C"
+
+namespace {
 // the batch of a selection call (validation, candidate buffer); `global_counts` (optional) are
 // the full arrays' lengths the ranks refer to when this GPU holds shards
 int select_batch(zks_engine* e, const double* const* values_dev, const int64_t* counts, int32_t narrays,

@@ -1,0 +1,324 @@
+// Sweep rows: one replicate stream drawn once, counted for every gamma of the row.
+//
+// build_table seeds every cell with the same base_seed (pkg/src/zipfks/montecarlo.py:276-277),
+// so the cells of a row (equal n and repetition, gammas differ) draw replicate index i from the
+// identical uniforms u_j = 1 - m_j 2^-53, m_j = x_j >> 11 of Philox word x_j
+// (distribution.py:182-187).  A cell's sample is sample() (distribution.py:190-201) of those
+// uniforms: value v_j = 1 + #{k : cdf[k] < u_j}, clamped to L.  Since u > h <=> m < M(h), the
+// exact 53-bit cut M(h) = #{m : 1 - m 2^-53 > h}, a cell's counts of the values 1..64 follow
+// from where its 64 cuts M_k = M(cdf[k]) fall among the row's keys:
+//   #{v_j >= k + 2} = P_k = #{m_j < M_k} (cdf non-decreasing => M non-increasing),
+//   count(1) = n - P_0,  count(k) = P_{k-2} - P_{k-1} (k = 2..64),
+// and the P_63 keys below M_63 are exactly the draws above 64, resolved one by one by the guide
+// + cdf search.  So per row the kernel draws and buckets n keys once (Philox4x64 + a counting
+// sort by the keys' top bits, on chip) and per cell does 64 short bucket scans plus its tail --
+// instead of generating or re-reading and classifying all n draws once per gamma.  Entries of
+// the cut table from L - 1 on are 0 (the clamp to L: no draw counts above it).
+//
+// Output per (cell, replicate) is draw_stats_kernel's pre-drawn row (zks_batch.cuh): u16 counts
+// of 1..64, the tail values or, for 64 < K <= 1024, u32 counts of 65..vmax, log-sum, min, max,
+// tail length -- the input of fit_ks_kernel / retry_kernel.  Single cells in the same n range
+// run through here too (ncells = 1), so a cell's results do not depend on whether it was
+// computed alone or in a row.
+//
+// Keys are only bucketed (about two per bucket, buckets in key order), not sorted: a cut's
+// position is its bucket's start plus the keys of that bucket below it, and the tail is every
+// key below M_63 -- all keys of the buckets under M_63's bucket and those of that bucket below
+// it.  The order inside a bucket comes from shared-memory atomics and varies between runs, so
+// everything summed over keys is order-free: the log-sum is accumulated in 128-bit fixed point
+// (every ln v, v >= 2, is a multiple of 2^-53 below 2^4: ln v 2^53 is an exact integer < 2^57),
+// exact and therefore identical for any order; the tail list's order does not matter to the
+// fit kernel (it sorts, or histograms, the tail).
+#pragma once
+#include "zks_batch.cuh"
+
+namespace zks {
+
+constexpr int kRowMaxCells = 32;
+constexpr int kRowMaxN = 16384;      // keys (8 B each) + buckets of one row in shared memory
+constexpr int kRowStageMaxN = 6144;  // up to here the draw pass parks the keys in shared memory for
+                                     // the scatter pass; above it the scatter pass regenerates them
+#ifndef ZKS_ROW_MINB
+#define ZKS_ROW_MINB 3
+#endif
+
+// Exact 53-bit cut of a cdf entry h: the smallest m <= 2^53 with 1 - m 2^-53 <= h (so u > h
+// <=> m < M).  1 - m 2^-53 is exact for every m <= 2^53; the estimate from (1 - h) 2^53 is off
+// by at most one or two and fixed by the exact test.  h >= 1 (and +inf) gives 0.
+__device__ __forceinline__ unsigned long long exact_cut(double h) {
+  if (!(h < 1.0)) return 0ull;
+  constexpr unsigned long long kTop = 1ull << 53;
+  const double d = (1.0 - h) * 0x1p53;
+  unsigned long long m = d >= 0x1p53 ? kTop : static_cast<unsigned long long>(ceil(d));
+  auto le = [h](unsigned long long mm) { return 1.0 - static_cast<double>(mm) * 0x1p-53 <= h; };
+  while (m > 0ull && le(m - 1ull)) --m;
+  while (m < kTop && !le(m)) ++m;
+  return m;
+}
+
+// The cut table of a sampling table (64 entries; from L - 1 on: 0, the clamp)
+__global__ void cut_kernel(const double* __restrict__ cdf, uint32_t L, unsigned long long* mcut) {
+  const int j = threadIdx.x;
+  if (j < 64) mcut[j] = static_cast<uint32_t>(j) + 1u < L ? exact_cut(cdf[j]) : 0ull;
+}
+
+struct RowCell {
+  const double* cdf;
+  const uint16_t* guide;       // levels 1 and 2 (global memory)
+  const uint16_t* guide_fine;  // fine level 2
+  const unsigned long long* mcut;
+  uint32_t L;
+  int guide_levels;
+  // this chunk's pre-drawn rows of the cell (row i = replicate first + i)
+  uint16_t* head;
+  uint16_t* tail;
+  uint32_t* m;
+  double* ls;
+  uint32_t* mn;
+  uint32_t* mx;
+};
+
+struct RowArgs {
+  uint64_t seed, rep, first, count;
+  int n;
+  int vals_stride;   // u16 slots per tail row (u32 counts when dense)
+  int dense_words;   // K - kKsHead for kKsHead < K <= kDenseMaxK, else 0
+  int ncells;
+  int bucket_bits;   // keys are bucketed by their top bits: 2^bucket_bits buckets
+  const double* logs;
+  unsigned long long* counters;
+  RowCell cell[kRowMaxCells];
+};
+
+__host__ __device__ constexpr int row_bucket_bits(int n) {
+  int b = 0;
+  while ((1 << b) < n) ++b;  // ceil(log2 n)
+  b -= 1;                    // about two keys per bucket
+  return b < 4 ? 4 : (b > 13 ? 13 : b);
+}
+// shared memory of one block of `warps` warps: keys (+ the parked draw pass), bucket starts and
+// ends, per-warp dense histograms
+__host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps) {
+  return size_t(round_up(n, 2)) * 8 * (n <= kRowStageMaxN ? 2 : 1) + (size_t(1) << row_bucket_bits(n)) * 8 +
+         size_t(warps) * dense_words * 4;
+}
+
+// 128-bit fixed-point sums (units of 2^-53): hi:lo += x
+__device__ __forceinline__ void add128(unsigned long long& hi, unsigned long long& lo, unsigned long long xhi,
+                                       unsigned long long xlo) {
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(xlo), "l"(xhi));
+}
+// ln v in units of 2^-53, exactly (ln v < 16 is a multiple of 2^-53 for v >= 2; ln 1 = 0)
+__device__ __forceinline__ unsigned long long log_fixed(const double* __restrict__ logs, uint32_t v) {
+  return __double2ull_rz(__ldg(logs + v) * 0x1p53);
+}
+
+// one cell of the row, by one warp: counts of 1..64 from the cut positions, the tail by search
+template <bool kCount>
+__device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uint64_t i,
+                                         const unsigned long long* __restrict__ keys, const uint32_t* bstart,
+                                         const uint32_t* bend, uint32_t* dense, int lane, unsigned long long& tails) {
+  const int n = a.n;
+  const int shift = 53 - a.bucket_bits;
+  const uint32_t nbk = 1u << a.bucket_bits;
+  // P = #{keys < M}: the start of M's bucket plus that bucket's keys below M
+  auto pos = [&](unsigned long long M) -> uint32_t {
+    const uint32_t bk = static_cast<uint32_t>(M >> shift);
+    if (bk >= nbk) return static_cast<uint32_t>(n);
+    uint32_t p = bstart[bk];
+    const uint32_t e = bend[bk];
+    for (uint32_t s = p; s < e; ++s) p += keys[s] < M;
+    return p;
+  };
+  const unsigned long long Ma = __ldg(C.mcut + lane), Mb = __ldg(C.mcut + 32 + lane);
+  const uint32_t Pa = pos(Ma), Pb = pos(Mb);
+  const uint32_t Pa_up = __shfl_up_sync(0xffffffffu, Pa, 1), Pb_up = __shfl_up_sync(0xffffffffu, Pb, 1);
+  const uint32_t Pa31 = __shfl_sync(0xffffffffu, Pa, 31);
+  const uint32_t c0 = (lane ? Pa_up : static_cast<uint32_t>(n)) - Pa;  // count of value lane + 1
+  const uint32_t c1 = (lane ? Pb_up : Pa31) - Pb;                       // count of value lane + 33
+  const uint32_t T = __shfl_sync(0xffffffffu, Pb, 31);                  // draws above kKsHead
+  // the tail: every key below M_63, i.e. keys[0, E) of the buckets up to M_63's, filtered
+  unsigned long long shi = 0, slo = 0;  // log-sum, 2^-53 units
+  uint32_t vtop = 0, vlow = 0xffffffffu;
+  if (T) {
+    const unsigned long long M63 = __shfl_sync(0xffffffffu, Mb, 31);
+    const uint32_t bk = static_cast<uint32_t>(M63 >> shift);
+    const uint32_t E = bk >= nbk ? static_cast<uint32_t>(n) : bend[bk];
+    const bool two = C.guide_levels == 2;
+    const unsigned lt = (1u << lane) - 1u;
+    uint16_t* tail = C.tail + i * a.vals_stride;
+    uint32_t m = 0;
+    for (uint32_t t0 = 0; t0 < E; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      const unsigned long long key = t < E ? keys[t] : ~0ull;
+      const bool in = key < M63;
+      uint32_t v = 0;
+      if (in) {
+        const double u = 1.0 - static_cast<double>(key) * 0x1p-53;  // exact
+        uint32_t lo, hi;
+        guide_bracket_fine(u, C.guide, C.guide_fine, two, lo, hi);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (__ldg(C.cdf + mid) >= u)
+            hi = mid;
+          else
+            lo = mid + 1;
+        }
+        v = min(lo + 1, C.L);
+        add128(shi, slo, 0ull, log_fixed(a.logs, v));
+        vtop = max(vtop, v);
+        vlow = min(vlow, v);
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        if (dense)
+          atomicAdd(dense + (v - kKsHead - 1), 1u);
+        else
+          tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+      }
+      m += __popc(bm);
+    }
+    vtop = warp_max_u32(vtop);
+    vlow = warp_min_u32(vlow);
+  }
+  {  // the head's share of the log-sum: count x ln k, exact
+    const unsigned long long l0 = log_fixed(a.logs, lane + 1), l1 = log_fixed(a.logs, lane + 33);
+    add128(shi, slo, __umul64hi(c0, l0), static_cast<unsigned long long>(c0) * l0);
+    add128(shi, slo, __umul64hi(c1, l1), static_cast<unsigned long long>(c1) * l1);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, shi, o), olo = __shfl_xor_sync(0xffffffffu, slo, o);
+    add128(shi, slo, ohi, olo);
+  }
+  const double log_sum = static_cast<double>(shi) * 0x1p11 + static_cast<double>(slo) * 0x1p-53;
+  const unsigned h0 = __ballot_sync(0xffffffffu, c0 != 0u), h1 = __ballot_sync(0xffffffffu, c1 != 0u);
+  const uint32_t vmin = h0 ? static_cast<uint32_t>(__ffs(h0)) : h1 ? 32u + __ffs(h1) : vlow;
+  const uint32_t vmax = T ? vtop : h1 ? 64u - __clz(h1) : 32u - __clz(h0);
+  uint16_t* head = C.head + i * kKsHead;
+  head[lane] = static_cast<uint16_t>(c0);  // n <= kRowMaxN: u16 counts
+  head[lane + 32] = static_cast<uint16_t>(c1);
+  if (dense) {  // counts of kKsHead+1..vmax into the row's tail slot (what fit_ks_kernel reads)
+    __syncwarp();
+    uint32_t* out = reinterpret_cast<uint32_t*>(C.tail + i * a.vals_stride);
+    const int used = vmax > kKsHead ? static_cast<int>(vmax - kKsHead) : 0;
+    for (int k = lane; k < used; k += 32) {
+      out[k] = dense[k];
+      dense[k] = 0u;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    C.ls[i] = log_sum;
+    C.mn[i] = vmin;
+    C.mx[i] = vmax;
+    C.m[i] = T;
+  }
+  if (kCount) tails += T;
+}
+
+// One block per replicate row (grid-stride over the chunk's rows): draw the n Philox words of
+// stream (seed, rep, first + i), bucket their 53-bit keys in shared memory (a count pass, a
+// scan, a scatter pass), then the block's warps take the row's cells (warp w: cells w, w + W, ...).
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const __grid_constant__ RowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  const bool parked = n <= kRowStageMaxN;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* raw = keys + round_up(n, 2);  // the draw pass's keys in stream order (parked)
+  const int nbk = 1 << a.bucket_bits;
+  const int shift = 53 - a.bucket_bits;
+  uint32_t* bstart = reinterpret_cast<uint32_t*>(keys + round_up(n, 2) * (parked ? 2 : 1));
+  uint32_t* bend = bstart + nbk;  // counts, then running scatter positions = bucket ends
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  uint32_t* dense = a.dense_words ? bend + nbk + warp * a.dense_words : nullptr;
+  __shared__ unsigned long long key_sh[2];
+  __shared__ uint32_t wsum[kWarps];
+  for (int k = lane; k < a.dense_words; k += 32) dense[k] = 0u;
+  const int nb = (n + 3) >> 2;
+  unsigned long long tails = 0, rows = 0;
+  for (uint64_t i = blockIdx.x; i < a.count; i += gridDim.x) {
+    // 1. stream key (one warp), zeroed bucket counts
+    if (warp == 0) {
+      uint64_t k0, k1;
+      stream_key(a.seed, a.rep, a.first + i, k0, k1);
+      if (lane == 0) {
+        key_sh[0] = k0;
+        key_sh[1] = k1;
+      }
+    }
+    for (int b = threadIdx.x; b < nbk; b += blockDim.x) bend[b] = 0u;
+    __syncthreads();
+    const uint64_t k0 = key_sh[0], k1 = key_sh[1];
+    // 2. draw pass: bucket sizes (and the keys parked in stream order)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const Block4 x = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        if (4 * b + w < n) {
+          const unsigned long long m = x.w[w] >> 11;
+          atomicAdd(bend + (m >> shift), 1u);
+          if (parked) raw[4 * b + w] = m;
+        }
+      }
+    }
+    __syncthreads();
+    // 3. exclusive scan of the bucket sizes (each thread a contiguous segment)
+    {
+      const int seg = (nbk + blockDim.x - 1) / blockDim.x;
+      const int b0 = min(nbk, static_cast<int>(threadIdx.x) * seg), b1 = min(nbk, b0 + seg);
+      uint32_t s = 0;
+      for (int b = b0; b < b1; ++b) s += bend[b];
+      uint32_t incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      uint32_t run = incl - s;
+      for (int w = 0; w < warp; ++w) run += wsum[w];
+      for (int b = b0; b < b1; ++b) {
+        const uint32_t c = bend[b];
+        bstart[b] = run;
+        bend[b] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    // 4. scatter pass (bend[b] ends as the end of bucket b)
+    if (parked) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const unsigned long long m = raw[j];
+        keys[atomicAdd(bend + (m >> shift), 1u)] = m;
+      }
+    } else {
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const Block4 x = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const unsigned long long m = x.w[w] >> 11;
+          if (4 * b + w < n) keys[atomicAdd(bend + (m >> shift), 1u)] = m;
+        }
+      }
+    }
+    __syncthreads();
+    // 5. the row's cells, warp w takes cells w, w + W, ...
+    for (int c = warp; c < a.ncells; c += warps) row_cell<kCount>(a, a.cell[c], i, keys, bstart, bend, dense, lane, tails);
+    ++rows;
+    __syncthreads();  // keys and buckets are reused by the next row
+  }
+  if (kCount && lane == 0) {
+    if (threadIdx.x == 0 && rows) {
+      atomicAdd(a.counters + 1, rows * static_cast<unsigned long long>(n));  // Philox draws
+      atomicAdd(a.counters + kWorkFields, rows * static_cast<unsigned long long>(n));  // keys bucketed
+      atomicAdd(a.counters + kWorkFields + 2, rows * static_cast<unsigned long long>(a.ncells));
+    }
+    if (tails) atomicAdd(a.counters + kWorkFields + 3, tails);
+  }
+}
+
+}  // namespace zks

@@ -138,24 +138,23 @@ class Engine:
             )
         )
 
-    def staging_stride(self, n: int) -> int:
-        return int(self.lib.zks_staging_stride(int(n)))
-
-    def stage_uniforms(self, seed: int, repetition: int, first: int, count: int, n: int, out) -> None:
-        """Staged 32-bit draw words of replicate indices [first, first+count) into device int32 ``out``."""
+    def run_cells(self, tables, support_k: int | None, gammas, n: int, base_seed: int, repetition: int, first: int,
+                  count: int, outs) -> None:
+        """Enqueue replicates [first, first+count) of the cells of one sweep row (same n, support,
+        seed, repetition; gammas differ; <= 32 cells): ``outs[j]`` = (ks, gamma_hat, status) device
+        tensors of cell j.  Each replicate stream is drawn once for all cells (zks_run_cells)."""
+        m = len(gammas)
+        cells = (_native.ZksCell * m)(*[
+            _native.ZksCell(support_k=0 if support_k is None else int(support_k), reserved=0, gamma=float(g), n=int(n),
+                            base_seed=int(base_seed), repetition=int(repetition), first=int(first), count=int(count))
+            for g in gammas])
+        vp = ctypes.c_void_p
+        handles = (vp * m)(*[t.handle.value for t in tables])
+        ks = (vp * m)(*[o[0].data_ptr() for o in outs])
+        gh = (vp * m)(*[o[1].data_ptr() for o in outs])
+        st = (vp * m)(*[o[2].data_ptr() for o in outs])
         self.bind_stream()
-        _native.check(self.lib.zks_stage_uniforms(self.handle, int(seed), int(repetition), int(first), int(count),
-                                                  int(n), out.data_ptr()))
-
-    def run_replicates_staged(self, table: DrawTable, support_k, gamma, n, base_seed, repetition, first, count,
-                              u, u_first, u_count, ks, gamma_hat, status) -> None:
-        cell = _native.ZksCell(support_k=0 if support_k is None else int(support_k), reserved=0, gamma=float(gamma),
-                               n=int(n), base_seed=int(base_seed), repetition=int(repetition), first=int(first),
-                               count=int(count))
-        self.bind_stream()
-        _native.check(self.lib.zks_run_replicates_staged(self.handle, table.handle, ctypes.byref(cell), u.data_ptr(),
-                                                         int(u_first), int(u_count), ks.data_ptr(),
-                                                         gamma_hat.data_ptr(), status.data_ptr()))
+        _native.check(self.lib.zks_run_cells(self.handle, m, handles, cells, ks, gh, st))
 
     def select_ranks(self, values, ranks: list[int], out=None):
         """Order statistics of a device float64 tensor at zero-based ranks.
@@ -247,7 +246,7 @@ class Engine:
                                                    out.data_ptr()))
 
     def set_chunk_bytes(self, nbytes: int = 0) -> None:
-        """Budget of one chunk of pre-drawn rows (0 = the default 4 GiB); results never depend on it."""
+        """Budget of one chunk of pre-drawn rows (0 = the default 16 GiB); results never depend on it."""
         _native.check(self.lib.zks_engine_set_chunk_bytes(self.handle, int(nbytes)))
 
     def uniforms_key(self, k0: int, k1: int, count: int, out) -> None:

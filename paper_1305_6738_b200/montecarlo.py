@@ -301,30 +301,25 @@ def _enqueue_cell(eng, plan: _CellPlan, shard: tuple[int, int] | None = None, re
     plan.finished.record(stream)
 
 
-# n range whose sweep rows share staged draw words.  Below 128 the lane-per-replicate kernel
-# regenerates its streams: strided per-lane reads of staged rows measured slower than Philox there.
-_STAGE_MIN_N, _STAGE_MAX_N = 128, 16384
-_STAGE_BYTES = 8 << 30                   # staging buffer budget (one chunk per 10^6-replicate row up to n = 2000;
-                                         # tests shrink it to force chunked rows)
-
-
 def _stage_key(cfg: SimulationConfig):
     return (cfg.support.k, cfg.n, cfg.base_seed, cfg.replicates, cfg.repetitions, cfg.quantiles)
 
 
+_ROW_CELLS = 32  # cells per zks_run_cells call
+
+
 def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
-    """Queue cells that differ only in gamma, sharing one uniform stream per replicate.
+    """Queue cells that differ only in gamma (one sweep row), sharing one uniform stream per replicate.
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
-    equal n draw from identical uniforms: for 128 <= n <= 16384 they are generated once per chunk
-    of replicate indices (zks_stage_uniforms) and every cell's replicate kernels read them.  The
+    equal n draw from identical uniforms: zks_run_cells draws each replicate's stream once for
+    all of them (128 <= n <= 16384; other sizes run cell by cell inside the same call).  The
     cells' order statistics are selected in batched launches.  Results are identical to running
     the cells one by one.
     """
     torch = _torch()
     cfg0 = plans[0].config
     n = cfg0.n
-    staged = _STAGE_MIN_N <= n <= _STAGE_MAX_N
     if len(plans) < 2:
         for plan in plans:
             _enqueue_cell(eng, plan, shard=shard, reduce=reduce, kernel_events=kernel_events, keep=keep)
@@ -333,13 +328,6 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
     first, stop = shard if shard is not None else (0, total)
     dev = f"cuda:{eng.device}"
     ranks = quantile_ranks(total, cfg0.quantiles)
-    stride = eng.staging_stride(n)
-    chunk = max(1, min(stop - first, _STAGE_BYTES // (4 * stride)))
-    key = ("stage", eng.device)
-    ubuf = _SLABS.get(key)
-    if staged and (ubuf is None or ubuf.numel() < chunk * stride):
-        ubuf = torch.empty(chunk * stride, dtype=torch.int32, device=dev)  # 32-bit staged words
-        _SLABS[key] = ubuf
     outs = []
     stream = eng.bind_stream()
     # one allocation (and one fill) for the whole row's quantiles and worst statuses
@@ -354,25 +342,18 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
         outs.append(_Slab(eng, max(total, 1)))
     tables = [_table(eng, p.config) for p in plans]
     for rep in range(cfg0.repetitions):
-        if not staged:  # independent streams per cell; only the selection is batched
-            for plan, table, out in zip(plans, tables, outs):
-                cfg = plan.config
-                if stop > first:
-                    eng.run_replicates(table, cfg.support.k, cfg.gamma, n, cfg.base_seed, rep, first, stop - first,
-                                       out.ks[first:], out.gh[first:], out.st[first:])
-        for c0 in range(first, stop, chunk) if staged else ():
-            cnt = min(chunk, stop - c0)
-            eng.stage_uniforms(cfg0.base_seed, rep, c0, cnt, n, ubuf)
-            for plan, table, out in zip(plans, tables, outs):
-                cfg = plan.config
-                if kernel_events is not None:
-                    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    k0.record(stream)
-                eng.run_replicates_staged(table, cfg.support.k, cfg.gamma, n, cfg.base_seed, rep, c0, cnt, ubuf, c0,
-                                          cnt, out.ks[c0:], out.gh[c0:], out.st[c0:])
-                if kernel_events is not None:
-                    k1.record(stream)
-                    kernel_events.append((k0, k1))
+        if stop > first:
+            if kernel_events is not None:  # bench.py: the row's replicate kernels
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record(stream)
+            for j0 in range(0, len(plans), _ROW_CELLS):
+                part = slice(j0, j0 + _ROW_CELLS)
+                eng.run_cells(tables[part], cfg0.support.k, [p.config.gamma for p in plans[part]], n, cfg0.base_seed,
+                              rep, first, stop - first,
+                              [(o.ks[first:], o.gh[first:], o.st[first:]) for o in outs[part]])
+            if kernel_events is not None:
+                k1.record(stream)
+                kernel_events.append((k0, k1))
         for plan, out in zip(plans, outs):
             _keep(keep, plan.config, rep, out, first, stop)
         # the row's cells in batched selections; the first rank chunk also takes the worst status

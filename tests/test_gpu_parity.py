@@ -259,7 +259,7 @@ def test_build_table_matches_run_simulation(zk):
         zk.build_table(ns=(3,), gammas=(-30.0,), support=zk.Support.finite(20), base_seed=5, replicates=100,
                        repetitions=1)
     # a failing cell inside a batched sweep row (worst status through the batched selection),
-    # for the small-n and the staged two-kernel rows
+    # for the small-n rows and the row kernel (one stream per replicate for every gamma)
     with pytest.raises(zk.SimulationError, match=r"gamma=-30.0, n=3"):
         zk.build_table(ns=(3,), gammas=(1.0, -30.0), support=zk.Support.finite(20), base_seed=5, replicates=100,
                        repetitions=2)
@@ -269,8 +269,8 @@ def test_build_table_matches_run_simulation(zk):
 
 
 def test_sweep_with_shared_uniforms_matches_cells(zk):
-    # build_table stages one uniform stream per (n, repetition) for all gammas (128 <= n <= 16384);
-    # every cell must equal its own run_simulation bit for bit
+    # build_table draws each replicate stream once per sweep row for all its gammas (zks_run_cells,
+    # 128 <= n <= 16384); every cell must equal its own run_simulation bit for bit
     table = zk.build_table(ns=(131, 200, 701), gammas=(1.6, 2.2, 3.0), support=zk.Support.unbounded(), base_seed=3,
                            replicates=3000, repetitions=2)  # 131, 701: masked last blocks
     for (g, n), row in table.cells.items():
@@ -301,43 +301,6 @@ def test_sharded_ranges_are_bitwise_identical(zk):
     parts = [run_cell(None, 2.0, 100, 3, 0, a, b - a) for a, b in ((0, 1000), (1000, 3001), (3001, 4096))]
     np.testing.assert_array_equal(ks, np.concatenate([p[0] for p in parts]))
     np.testing.assert_array_equal(gh, np.concatenate([p[1] for p in parts]))
-
-
-@pytest.mark.parametrize("n", [20, 300])
-@pytest.mark.parametrize("j", [0, 2, 9])
-def test_undecided_staged_words_redraw_from_philox(zk, n, j):
-    # a sampling table with cdf[j] strictly inside one staged word's u interval
-    # [1 - (t+1) 2^-32 + 2^-53, 1 - t 2^-32]: that word's value is undecided by its 32 bits
-    # (cut test for j < 4, straddled search for j >= 4), so its replicate must be redrawn from
-    # Philox -- the staged run equals the unstaged one bit for bit (batch kernel at n = 20,
-    # draw kernel at n = 300)
-    import torch
-
-    from paper_1305_6738_b200 import engine
-
-    eng = engine.get_engine()
-    R, K = 64, 20
-    stride = eng.staging_stride(n)
-    u = torch.empty(R * stride, dtype=torch.int32, device="cuda")
-    eng.stage_uniforms(11, 0, 0, R, n, u)
-    t = int(u[5 * stride + 3].item()) & 0xFFFFFFFF  # a word of replicate 5
-    c = 1.0 - (t + 0.5) * 2.0**-32
-    cdf = np.concatenate([np.linspace(c * 0.1, c * 0.9, j), [c], np.linspace(c + (1 - c) * 0.1, 1.0, K - j - 1)])
-    assert np.all(np.diff(cdf) > 0) and cdf.size == K
-    table = engine.DrawTable(eng, cdf)
-    dev = "cuda"
-    outs = []
-    for staged in (False, True):
-        ks = torch.empty(R, dtype=torch.float64, device=dev)
-        gh = torch.empty_like(ks)
-        st = torch.empty(R, dtype=torch.uint8, device=dev)
-        if staged:
-            eng.run_replicates_staged(table, K, 1.0, n, 11, 0, 0, R, u, 0, R, ks, gh, st)
-        else:
-            eng.run_replicates(table, K, 1.0, n, 11, 0, 0, R, ks, gh, st)
-        outs.append((ks.cpu().numpy(), gh.cpu().numpy(), st.cpu().numpy()))
-    for a, b in zip(*outs):
-        np.testing.assert_array_equal(a, b)
 
 
 def test_cells_on_two_streams_match_sequential(zk):
@@ -538,18 +501,16 @@ def _row_outputs(zk, K, n, gammas, R, seed=3):
 
 
 @pytest.mark.parametrize("K,n", [(None, 300), (None, 5000), (None, 12000), (1000, 300), (1000, 5000), (1000, 12000)])
-def test_chunked_rows_match_single_chunk(zk, monkeypatch, K, n):
-    # the staged words and the pre-drawn rows both run in >= 3 chunks (budgets shrunk): every
-    # replicate's (ks, gamma_hat, status) equals the single-chunk run's and the unstaged cell's
+def test_chunked_rows_match_single_chunk(zk, K, n):
+    # the pre-drawn rows of a sweep row run in >= 3 chunks (budget shrunk): every replicate's
+    # (ks, gamma_hat, status) equals the single-chunk run's and the cell's run on its own
     from paper_1305_6738_b200 import montecarlo as mc
 
     R = 20000 if n <= 5000 else 6000
     gammas = (0.8, 1.6) if K else (1.6, 2.5)
     eng = mc._engine()
     whole = _row_outputs(zk, K, n, gammas, R)
-    stride = eng.staging_stride(n)
-    monkeypatch.setattr(mc, "_STAGE_BYTES", 4 * stride * (R // 3 + 1))  # 3 staging chunks
-    eng.set_chunk_bytes(max(1, (R // 4) * (200 + 4 * n)))  # >= 4 pre-drawn row chunks
+    eng.set_chunk_bytes(max(1, (R // 4) * (200 + 4 * n) * len(gammas)))  # >= 4 chunks of pre-drawn rows
     try:
         chunked = _row_outputs(zk, K, n, gammas, R)
     finally:
@@ -600,3 +561,16 @@ def test_truncated_corner_negative_gamma_hat(zk, K):
         assert close(gh[i], want_gh), (i, gh[i], want_gh)
         neg += want_gh < 0
     assert neg > R // 10
+
+
+@pytest.mark.parametrize("K,n", [(None, 128), (None, 16384), (None, 16385), (1000, 128), (1000, 16384), (20, 777)])
+def test_row_kernel_bounds_and_many_cells(zk, K, n):
+    # the row kernel's size bounds (n = 128 and 16384; 16385 runs cell by cell) and rows of more
+    # cells than one call takes (33 gammas: two calls): every cell equals its own run
+    gammas = tuple(np.round(np.linspace(1.2 if K is None else 0.3, 3.5, 33), 6))
+    R = 512
+    rows = _row_outputs(zk, K, n, gammas, R)
+    for g in gammas[::4] + gammas[-1:]:
+        cell = run_cell(K, g, n, 3, 0, 0, R)
+        for a, b in zip(rows[g], cell):
+            np.testing.assert_array_equal(a, b)
