@@ -195,6 +195,7 @@ struct zks_table {
   uint16_t* guide = nullptr;
   uint32_t len = 0;
   double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
+  double tail_mass = 0.0;          // P(X > 64) = 1 - cdf[63]: the row kernel's cost estimate
   uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on the top 32 bits of Philox words
   unsigned long long* mcut = nullptr;  // exact 53-bit cuts of cdf[0..63] (row_draw_kernel)
   // stream ordering: the upload (and guide build) runs on `home`; another stream's first use
@@ -341,6 +342,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   t->len = static_cast<uint32_t>(len);
   for (int j = 0; j < 4; ++j) {
     t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
+    t->tail_mass = len > 64 ? std::max(0.0, 1.0 - cdf_host[63]) : 0.0;
     t->tcut[j] = staged_cut(t->head[j]);
   }
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
@@ -579,10 +581,8 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   const size_t dsmem = zks::round_up(zks::kGuideLevel * 2, 16) + (size_t(4) << zks::kCutTabBits) +
                        size_t(zks::kWarps) * (zks::draw_warp_bytes(wide) + size_t(dense_words) * 4);
   auto rowk = counting ? zks::row_draw_kernel<true> : zks::row_draw_kernel<false>;
-  // warps per row block: each takes cells w, w + W, ...; W in 4..8 with the fewest idle cell slots
-  int row_warps = 4;
-  for (int w = 4; w <= zks::kWarps; ++w)
-    if ((ncells + w - 1) / w * w - ncells <= (ncells + row_warps - 1) / row_warps * row_warps - ncells) row_warps = w;
+  // warps per row block (the cells are spread over them by the schedule below)
+  const int row_warps = std::max(4, std::min(zks::kWarps, ncells));
   const size_t rsmem_row = zks::row_smem_bytes(static_cast<int>(c0.n), dense_words, row_warps);
   int dper = 0;
   if (rows) {
@@ -601,6 +601,35 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     ra.bucket_bits = zks::row_bucket_bits(ra.n);
     ra.logs = e->logs;
     ra.counters = e->counters;
+    // longest processing time first: a cell costs its 64 cut positions and reductions (~one
+    // 32-lane round) plus a guide + cdf search per 32 tail draws (about three rounds each)
+    auto cell_cost = [&](int j) { return 1.0 + 3.0 * double(c0.n) * tables[j]->tail_mass / 32.0; };
+    std::vector<std::pair<double, int>> cost(ncells);
+    for (int j = 0; j < ncells; ++j) cost[j] = {cell_cost(j), j};
+    std::sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<std::vector<int>> lists(row_warps);
+    std::vector<double> load(row_warps, 0.0);
+    for (const auto& cj : cost) {
+      int w = 0;
+      for (int v = 1; v < row_warps; ++v)
+        if (load[v] < load[w]) w = v;
+      lists[w].push_back(cj.second);
+      load[w] += cj.first;
+    }
+    // the least loaded list last (that warp also derives the next row's stream key)
+    auto list_cost = [&](const std::vector<int>& l) {
+      double c = 0.0;
+      for (int j : l) c += cell_cost(j);
+      return c;
+    };
+    std::stable_sort(lists.begin(), lists.end(),
+                     [&](const auto& x, const auto& y) { return list_cost(x) > list_cost(y); });
+    int at = 0;
+    for (int w = 0; w < row_warps; ++w) {
+      ra.wbeg[w] = static_cast<uint8_t>(at);
+      for (int j : lists[w]) ra.order[at++] = static_cast<uint8_t>(j);
+    }
+    for (int w = row_warps; w <= zks::kWarps; ++w) ra.wbeg[w] = static_cast<uint8_t>(at);
     for (int j = 0; j < ncells; ++j) {
       zks::RowCell& rc = ra.cell[j];
       rc.cdf = tables[j]->cdf;

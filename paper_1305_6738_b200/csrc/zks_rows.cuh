@@ -87,20 +87,25 @@ struct RowArgs {
   int bucket_bits;   // keys are bucketed by their top bits: 2^bucket_bits buckets
   const double* logs;
   unsigned long long* counters;
+  // the block's cell schedule: warp w takes cells order[wbeg[w] .. wbeg[w + 1]) (longest
+  // processing time first over the host's cost estimates); the last warp, the least loaded, also
+  // derives the next row's stream key
+  uint8_t order[kRowMaxCells];
+  uint8_t wbeg[kWarps + 1];
   RowCell cell[kRowMaxCells];
 };
 
 __host__ __device__ constexpr int row_bucket_bits(int n) {
   int b = 0;
-  while ((1 << b) < n) ++b;  // ceil(log2 n)
-  b -= 1;                    // about two keys per bucket
-  return b < 4 ? 4 : (b > 13 ? 13 : b);
+  while ((1 << b) < n) ++b;  // ceil(log2 n): about one key per bucket
+  return b < 4 ? 4 : (b > 12 ? 12 : b);  // <= 4096 buckets (32 KB of starts and ends)
 }
-// shared memory of one block of `warps` warps: keys (+ the parked draw pass), bucket starts and
-// ends, per-warp dense histograms
+constexpr int kRowKeyPad = 2;  // sentinel keys (all ones) after the row: pair loads past a bucket's end
+// shared memory of one block of `warps` warps: keys + sentinels (+ the parked draw pass), bucket
+// starts and ends, per-warp dense histograms
 __host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps) {
-  return size_t(round_up(n, 2)) * 8 * (n <= kRowStageMaxN ? 2 : 1) + (size_t(1) << row_bucket_bits(n)) * 8 +
-         size_t(warps) * dense_words * 4;
+  return size_t(round_up(n + kRowKeyPad, 2)) * 8 + (n <= kRowStageMaxN ? size_t(round_up(n, 2)) * 8 : 0) +
+         (size_t(1) << row_bucket_bits(n)) * 8 + size_t(warps) * dense_words * 4;
 }
 
 // 128-bit fixed-point sums (units of 2^-53): hi:lo += x
@@ -121,14 +126,16 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
   const int n = a.n;
   const int shift = 53 - a.bucket_bits;
   const uint32_t nbk = 1u << a.bucket_bits;
-  // P = #{keys < M}: the start of M's bucket plus that bucket's keys below M
+  // P = #{keys < M}: the start of M's bucket plus that bucket's keys below M (about one: the
+  // first two are read unconditionally, the sentinels cover the row's end)
   auto pos = [&](unsigned long long M) -> uint32_t {
     const uint32_t bk = static_cast<uint32_t>(M >> shift);
     if (bk >= nbk) return static_cast<uint32_t>(n);
-    uint32_t p = bstart[bk];
-    const uint32_t e = bend[bk];
-    for (uint32_t s = p; s < e; ++s) p += keys[s] < M;
-    return p;
+    const uint32_t p = bstart[bk], e = bend[bk];
+    const unsigned long long x0 = keys[p], x1 = keys[p + 1];
+    uint32_t r = p + (p < e && x0 < M) + (p + 1 < e && x1 < M);
+    for (uint32_t s = p + 2; s < e; ++s) r += keys[s] < M;
+    return r;
   };
   const unsigned long long Ma = __ldg(C.mcut + lane), Mb = __ldg(C.mcut + 32 + lane);
   const uint32_t Pa = pos(Ma), Pb = pos(Mb);
@@ -219,39 +226,41 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
 
 // One block per replicate row (grid-stride over the chunk's rows): draw the n Philox words of
 // stream (seed, rep, first + i), bucket their 53-bit keys in shared memory (a count pass, a
-// scan, a scatter pass), then the block's warps take the row's cells (warp w: cells w, w + W, ...).
+// scan, a scatter pass), then the block's warps take the row's cells by the host's schedule.
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const __grid_constant__ RowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   const bool parked = n <= kRowStageMaxN;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-  unsigned long long* raw = keys + round_up(n, 2);  // the draw pass's keys in stream order (parked)
+  unsigned long long* raw = keys + round_up(n + kRowKeyPad, 2);  // the draw pass's keys in stream order (parked)
   const int nbk = 1 << a.bucket_bits;
   const int shift = 53 - a.bucket_bits;
-  uint32_t* bstart = reinterpret_cast<uint32_t*>(keys + round_up(n, 2) * (parked ? 2 : 1));
+  uint32_t* bstart = reinterpret_cast<uint32_t*>(raw + (parked ? round_up(n, 2) : 0));
   uint32_t* bend = bstart + nbk;  // counts, then running scatter positions = bucket ends
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   uint32_t* dense = a.dense_words ? bend + nbk + warp * a.dense_words : nullptr;
-  __shared__ unsigned long long key_sh[2];
+  __shared__ unsigned long long key_sh[2][2];  // this row's and the next row's stream keys
   __shared__ uint32_t wsum[kWarps];
   for (int k = lane; k < a.dense_words; k += 32) dense[k] = 0u;
+  if (threadIdx.x < kRowKeyPad) keys[n + threadIdx.x] = ~0ull;
   const int nb = (n + 3) >> 2;
   unsigned long long tails = 0, rows = 0;
-  for (uint64_t i = blockIdx.x; i < a.count; i += gridDim.x) {
-    // 1. stream key (one warp), zeroed bucket counts
-    if (warp == 0) {
-      uint64_t k0, k1;
-      stream_key(a.seed, a.rep, a.first + i, k0, k1);
-      if (lane == 0) {
-        key_sh[0] = k0;
-        key_sh[1] = k1;
-      }
+  if (warp == warps - 1 && blockIdx.x < a.count) {
+    uint64_t k0, k1;
+    stream_key(a.seed, a.rep, a.first + blockIdx.x, k0, k1);
+    if (lane == 0) {
+      key_sh[0][0] = k0;
+      key_sh[0][1] = k1;
     }
+  }
+  int kb = 0;  // key_sh slot of the current row
+  for (uint64_t i = blockIdx.x; i < a.count; i += gridDim.x, kb ^= 1) {
+    // 1. zeroed bucket counts (the stream key was derived during the previous row)
     for (int b = threadIdx.x; b < nbk; b += blockDim.x) bend[b] = 0u;
     __syncthreads();
-    const uint64_t k0 = key_sh[0], k1 = key_sh[1];
+    const uint64_t k0 = key_sh[kb][0], k1 = key_sh[kb][1];
     // 2. draw pass: bucket sizes (and the keys parked in stream order)
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
       const Block4 x = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
@@ -306,8 +315,17 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
       }
     }
     __syncthreads();
-    // 5. the row's cells, warp w takes cells w, w + W, ...
-    for (int c = warp; c < a.ncells; c += warps) row_cell<kCount>(a, a.cell[c], i, keys, bstart, bend, dense, lane, tails);
+    // 5. the row's cells by the schedule; the last warp also derives the next row's stream key
+    for (int c = a.wbeg[warp]; c < a.wbeg[warp + 1]; ++c)
+      row_cell<kCount>(a, a.cell[a.order[c]], i, keys, bstart, bend, dense, lane, tails);
+    if (warp == warps - 1 && i + gridDim.x < a.count) {
+      uint64_t q0, q1;
+      stream_key(a.seed, a.rep, a.first + i + gridDim.x, q0, q1);
+      if (lane == 0) {
+        key_sh[kb ^ 1][0] = q0;
+        key_sh[kb ^ 1][1] = q1;
+      }
+    }
     ++rows;
     __syncthreads();  // keys and buckets are reused by the next row
   }
