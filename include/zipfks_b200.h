@@ -210,6 +210,11 @@ int zks_fit_samples(zks_engine* engine, int32_t support_k, const int64_t* values
  * normaliser = normalization (distribution.py:71-85).  NaN where the series diverges. */
 int zks_series_eval(zks_engine* engine, int32_t support_k, const double* gamma_dev, int64_t count, double* out_dev);
 
+/* tail_mass (series.py:141-160): out_dev[i] = sum_{k >= start_dev[i]} k^-gamma by Euler-Maclaurin
+ * through the third-derivative term; every start must exceed 64 (checked by the shim).
+ * Asynchronous. */
+int zks_tail_mass(zks_engine* engine, double gamma, const double* start_dev, int64_t count, double* out_dev);
+
 /* The exponent for given mean-log targets: Newton/bisection as mle_gamma, or with bisect_only
  * the bisection of _bisect (estimate.py:94-112) on [bracket_lo, bracket_hi].  status 2 =
  * NoRootError.  Asynchronous. */

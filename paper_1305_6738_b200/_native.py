@@ -31,6 +31,7 @@ EXPORTS = (
     "zks_table_destroy",
     "zks_run_replicates",
     "zks_run_cells",
+    "zks_tail_mass",
     "zks_select_ranks",
     "zks_select_ranks_async",
     "zks_select_ranks_batch",
@@ -111,6 +112,7 @@ def load() -> ctypes.CDLL:
     lib.zks_table_destroy.restype = None
     lib.zks_run_replicates.argtypes = [vp, vp, ctypes.POINTER(ZksCell), dp, dp, dp]
     lib.zks_run_cells.argtypes = [vp, i32, dp, dp, dp, dp, dp]
+    lib.zks_tail_mass.argtypes = [vp, ctypes.c_double, dp, i64, dp]
     lib.zks_select_ranks.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_async.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp, dp, dp]

@@ -1163,6 +1163,19 @@ int zks_series_eval(zks_engine* e, int32_t support_k, const double* gamma_dev, i
   return ZKS_OK;
 }
 
+int zks_tail_mass(zks_engine* e, double gamma, const double* start_dev, int64_t count, double* out_dev) {
+  if (!e || !start_dev || !out_dev) return fail(ZKS_EINVAL, "NULL argument");
+  if (count <= 0) return ZKS_OK;
+  ZKS_CUDA(cudaSetDevice(e->device));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(e->sms) * 4, (count + 255) / 256));
+  {
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::tail_mass_kernel<<<(unsigned)blocks, 256, 0, e->stream>>>(gamma, start_dev, count, out_dev);
+    ZKS_CUDA(launched(e));
+  }
+  return ZKS_OK;
+}
+
 int zks_solve_exponents(zks_engine* e, int32_t support_k, const double* target_dev, int64_t count,
                         const zks_mle_settings* settings, int32_t bisect_only, double* gamma_dev, uint8_t* status_dev) {
   if (!e || !target_dev || !gamma_dev || !status_dev) return fail(ZKS_EINVAL, "NULL argument");

@@ -142,6 +142,14 @@ __global__ void __launch_bounds__(kThreads) samples_kernel(SamplesArgs a) {
 
 // Model moments by the reference formulas (direct sums, m-doubling rule): out[4*i..] =
 // (s0, s1, s2, normaliser) at gamma[i].  One warp per exponent.
+// tail_mass (series.py:141-160): sum_{k >= start_i} k^-g, Euler-Maclaurin through the third
+// derivative, vectorised over start
+__global__ void tail_mass_kernel(double g, const double* __restrict__ start, int64_t count, double* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = tail_sum(g, log(start[i]));
+}
+
 __global__ void series_kernel(const double* __restrict__ gamma, int64_t count, int K, const double* logs,
                               double* out) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;

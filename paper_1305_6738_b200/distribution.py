@@ -148,6 +148,36 @@ class Sample:
         return int(self.observations.size)
 
 
+def _check_in_support(model: "ZipfModel", k) -> int:
+    if not isinstance(k, (int, np.integer)) or isinstance(k, bool):
+        raise ValueError(f"support point must be an integer, got {k!r}")
+    k = int(k)
+    if k < 1 or (model.support.is_finite and k > model.support.k):
+        raise ValueError(f"value {k} lies outside the support 1..{model.support}")
+    return k
+
+
+def pmf(model: "ZipfModel", k) -> float:
+    """P(X = k) = k^-gamma / norm (distribution.py:158-161); the normaliser from the device."""
+    k = _check_in_support(model, k)
+    return math.exp(-model.gamma * math.log(k)) * (1.0 / model.norm)
+
+
+def cdf(model: "ZipfModel", k) -> float:
+    """P(X <= k) (distribution.py:164-170), on the device: the power sum over 1..k (the finite
+    normaliser at support k) over the model's normaliser; beyond the partial-table seam of the
+    unbounded model, (norm - tail_mass(gamma, k + 1)) / norm as the reference forms it."""
+    k = _check_in_support(model, k)
+    from .engine import get_engine
+
+    if model.support.is_finite or k <= _PARTIAL_SEAM:
+        head = 1.0 if k == 1 else get_engine().normaliser(model.gamma, k)
+        return float(head / model.norm)
+    from .series import tail_mass
+
+    return float((model.norm - tail_mass(model.gamma, k + 1)) / model.norm)
+
+
 class RandomStream:
     """Deterministic uniform(0, 1] stream keyed ``[seed, repetition, index]``, drawn on the GPU.
 

@@ -298,6 +298,15 @@ class Engine:
                                                gammas.data_ptr(), gammas.numel(), out.data_ptr()))
         return out
 
+    def tail_mass(self, gamma: float, starts):
+        """sum_{k >= s} k^-gamma at device float64 ``starts`` (each > 64)."""
+        torch = _torch()
+        out = torch.empty_like(starts)
+        self.bind_stream()
+        _native.check(self.lib.zks_tail_mass(self.handle, float(gamma), starts.data_ptr(), starts.numel(),
+                                             out.data_ptr()))
+        return out
+
     def solve(self, support_k, targets, settings=None, bisect_only=False):
         torch = _torch()
         g = torch.empty_like(targets)

@@ -82,3 +82,22 @@ def natural_logs(limit: int) -> np.ndarray:
         table.flags.writeable = False
         _cache = table
     return _cache[: limit + 1]
+
+
+_TAIL_MIN_START = 64  # series.py:26
+
+
+def tail_mass(gamma: float, start):
+    """sum_{k >= start} k^-gamma, vectorised over ``start`` (each >= 65), on the device:
+    Euler-Maclaurin through the third-derivative term (series.py:141-160)."""
+    import torch
+
+    from .engine import get_engine
+
+    a = np.asarray(start, dtype=np.float64)
+    if np.any(a < _TAIL_MIN_START + 1):
+        raise ValueError("tail_mass requires start > 64; sum small ranges directly")
+    eng = get_engine()
+    out = eng.tail_mass(gamma, torch.from_numpy(np.ascontiguousarray(a.ravel())).to(f"cuda:{eng.device}"))
+    value = out.cpu().numpy().reshape(a.shape)
+    return float(value) if np.ndim(start) == 0 else value

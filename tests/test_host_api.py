@@ -5,6 +5,7 @@ Mirrors the reference's validation tests — pkg/tests/test_montecarlo.py:36-57,
 names: every error must be raised before the engine is touched, with the reference's
 exception type.
 """
+import os
 from decimal import ROUND_FLOOR, Decimal
 
 import numpy as np
@@ -130,3 +131,45 @@ def test_cutoff_table_lookup_window():
         table.cutoff(1.5, 50, 0.8)  # level not tabulated
     assert issubclass(zk.CutoffLookupError, LookupError)
     assert issubclass(zk.SimulationError, RuntimeError)
+
+
+def _golden_fit():
+    import json
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fit")
+    with open(os.path.join(here, "fit.json")) as fh:
+        return here, json.load(fh)
+
+
+def test_fit_reports_format_like_the_reference():
+    # the reference's machine block carries full-precision values: rebuilt into a FitReport, both
+    # formats reproduce the reference's own stdout of that run (reporting.py:27-62)
+    from paper_1305_6738_b200.bespoke import FitReport, format_human, format_machine
+    from paper_1305_6738_b200.gof import Verdict
+
+    _, cases = _golden_fit()
+    block = dict(line.split("=", 1) for line in cases["inf_bespoke_machine"]["stdout"].strip().splitlines())
+    levels = (0.9, 0.95, 0.99, 0.999)
+    tags = ("90", "95", "99", "999")
+    report = FitReport(n=int(block["n"]), support=zk.Support.unbounded(), gamma_hat=float(block["gamma_hat"]),
+                       ks=float(block["ks"]), ks_argmax=int(block["ks_argmax"]), cutoff_source=block["cutoff_source"],
+                       verdicts=tuple(Verdict(q, float(block[f"cutoff_q{t}"]), block[f"rejected_q{t}"] == "true")
+                                      for q, t in zip(levels, tags)))
+    assert format_machine(report) + "\n" == cases["inf_bespoke_machine"]["stdout"]
+    assert format_human(report) + "\n" == cases["inf_bespoke_human"]["stdout"]
+
+
+def test_observation_files_parse_like_the_reference(tmp_path):
+    from paper_1305_6738_b200.bespoke import ObservationParseError, parse_observations, write_observations
+
+    here, cases = _golden_fit()
+    with pytest.raises(ObservationParseError) as err:
+        parse_observations("bad_token.txt" if os.getcwd() == here else os.path.join(here, "bad_token.txt"))
+    assert str(err.value).endswith(cases["bad_token"]["stderr"].strip().split("bad_token.txt")[1])
+    s = parse_observations(os.path.join(here, "inf_g22_n300.txt"))
+    assert s.n == 300
+    write_observations(s, tmp_path / "o.txt")
+    assert (tmp_path / "o.txt").read_text() == open(os.path.join(here, "inf_g22_n300.txt")).read()
+    (tmp_path / "empty.txt").write_text("  \n")
+    with pytest.raises(ObservationParseError, match="no observations found"):
+        parse_observations(tmp_path / "empty.txt")
