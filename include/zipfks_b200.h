@@ -31,6 +31,9 @@ extern "C" {
 #define ZKS_STATUS_RETRIED 1    /* NoRootError on the first stream, retry at idx + 2^32 ok */
 #define ZKS_STATUS_FAILED 2     /* both streams failed (SimulationError in the shim)      */
 
+#define ZKS_RNG_NUMPY 0      /* replicate streams bit-exact with numpy's Philox4x64-10 (default) */
+#define ZKS_RNG_PHILOX4X32 1 /* opt-in fast streams: Philox4x32-10, tier-3 (Monte Carlo) parity only */
+
 #define ZKS_MLE_TABLE 0   /* model moments from the device fit tables (default)           */
 #define ZKS_MLE_DIRECT 1  /* model moments by direct summation, as the reference forms them */
 
@@ -164,6 +167,13 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * uint64): RandomStream(key) for keys other than [seed, repetition, index] (distribution.py:
  * 173-180 accepts any SeedSequence entropy; the host derives the key, the device the uniforms).
  * Asynchronous. */
+/* Replicate streams of later calls: ZKS_RNG_NUMPY = RandomStream.for_replicate (distribution.py:
+ * 173-187) bit for bit; ZKS_RNG_PHILOX4X32 = an opt-in faster generator keyed by the same
+ * SeedSequence key: different samples, the same distributions, so cutoffs
+ * agree with the default only within Monte Carlo error.  User-facing RandomStream uniforms are
+ * always numpy's. */
+int zks_engine_set_rng(zks_engine* engine, int rng);
+
 /* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (default 16 GiB,
  * 0 restores it): a cell whose rows exceed it runs chunk by chunk.  Results do not depend on it. */
 int zks_engine_set_chunk_bytes(zks_engine* engine, uint64_t bytes);

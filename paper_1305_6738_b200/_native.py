@@ -32,6 +32,7 @@ EXPORTS = (
     "zks_run_replicates",
     "zks_run_cells",
     "zks_tail_mass",
+    "zks_engine_set_rng",
     "zks_select_ranks",
     "zks_select_ranks_async",
     "zks_select_ranks_batch",
@@ -113,6 +114,7 @@ def load() -> ctypes.CDLL:
     lib.zks_run_replicates.argtypes = [vp, vp, ctypes.POINTER(ZksCell), dp, dp, dp]
     lib.zks_run_cells.argtypes = [vp, i32, dp, dp, dp, dp, dp]
     lib.zks_tail_mass.argtypes = [vp, ctypes.c_double, dp, i64, dp]
+    lib.zks_engine_set_rng.argtypes = [vp, ctypes.c_int]
     lib.zks_select_ranks.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_async.argtypes = [vp, dp, i64, dp, i32, dp]
     lib.zks_select_ranks_batch.argtypes = [vp, dp, dp, i32, dp, i32, dp, dp, dp]

@@ -72,7 +72,7 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0;
   for (int b = lane; b < nb; b += 32) {
-    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
     bool vb[4];
     uint32_t x[4];
 #pragma unroll
@@ -105,7 +105,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0;
   for (int b = 0; b < nb; ++b) {
-    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
     bool vb[4];
     uint32_t x[4];
 #pragma unroll
@@ -900,7 +900,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       for (int w = 0; w < 4; ++w) w4[w] = t4[w];
       p = b + 32 < nb ? __ldcs(reinterpret_cast<const uint4*>(urow) + b + 32) : make_uint4(0u, 0u, 0u, 0u);
     } else {
-      const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+      const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         t4[w] = static_cast<uint32_t>(r.w[w] >> 32);

@@ -63,6 +63,7 @@ struct zks_engine {
   int staging_next = 0;
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
   int mle_mode = ZKS_MLE_TABLE;
+  int rng = ZKS_RNG_NUMPY;  // replicate streams: numpy's (bit-exact) or the opt-in fast one
   uint64_t pre_cap = kPreBytes;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes)
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::tuple<const void*, size_t, int>, int> occupancy;  // (kernel, smem, threads) -> blocks per SM
@@ -298,6 +299,13 @@ int zks_engine_set_chunk_bytes(zks_engine* e, uint64_t bytes) {
   return ZKS_OK;
 }
 
+int zks_engine_set_rng(zks_engine* e, int rng) {
+  if (!e) return fail(ZKS_EINVAL, "engine is NULL");
+  if (rng != ZKS_RNG_NUMPY && rng != ZKS_RNG_PHILOX4X32) return fail(ZKS_EINVAL, "unknown stream kind %d", rng);
+  e->rng = rng;
+  return ZKS_OK;
+}
+
 int zks_engine_set_timing(zks_engine* e, int on) {
   if (!e) return fail(ZKS_EINVAL, "engine is NULL");
   e->timing = on != 0;
@@ -460,6 +468,7 @@ int cell_args(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_d
   a.work = sc->work;
   a.counters = e->counters;
   a.guide_levels = L > 4096u ? 2 : 1;
+  a.rng = e->rng;
   a.use_table = e->mle_mode == ZKS_MLE_TABLE;
   if (a.use_table) {
     zks::FitTable* T = nullptr;
@@ -601,6 +610,7 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     ra.bucket_bits = zks::row_bucket_bits(ra.n);
     ra.logs = e->logs;
     ra.counters = e->counters;
+    ra.rng = e->rng;
     // longest processing time first: a cell costs its 64 cut positions and reductions (~one
     // 32-lane round) plus a guide + cdf search per 32 tail draws (about three rounds each)
     auto cell_cost = [&](int j) { return 1.0 + 3.0 * double(c0.n) * tables[j]->tail_mass / 32.0; };

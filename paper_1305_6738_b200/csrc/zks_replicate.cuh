@@ -81,6 +81,7 @@ struct ReplicateArgs {
   // counts of kKsHead+1..K in the row's tail slot instead of a value list (0 = value lists)
   int dense_words;
   double inv_n;  // 1 / n
+  int rng;       // kRngNumpy (bit-exact with the reference) or kRngPhilox4x32 (opt-in fast stream)
   uint32_t tcut[4];     // staged words: u > cdf_head[j] <=> t < tcut[j] (undecided at equality)
   double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
 };
@@ -204,7 +205,7 @@ __device__ __forceinline__ SampleStats sample_pass(const ReplicateArgs& a, uint6
   double ls = 0.0;
   for (int64_t b0 = 0; b0 < nb; b0 += 32) {
     const int64_t b = b0 + lane;
-    const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+    const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
     bool vb[4];
     uint32_t vv[4];
 #pragma unroll

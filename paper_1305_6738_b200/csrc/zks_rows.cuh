@@ -87,6 +87,7 @@ struct RowArgs {
   int bucket_bits;   // keys are bucketed by their top bits: 2^bucket_bits buckets
   const double* logs;
   unsigned long long* counters;
+  int rng;  // kRngNumpy or kRngPhilox4x32
   // the block's cell schedule: warp w takes cells order[wbeg[w] .. wbeg[w + 1]) (longest
   // processing time first over the host's cost estimates); the last warp, the least loaded, also
   // derives the next row's stream key
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
     const uint64_t k0 = key_sh[kb][0], k1 = key_sh[kb][1];
     // 2. draw pass: bucket sizes (and the keys parked in stream order)
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-      const Block4 x = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+      const Block4 x = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         if (4 * b + w < n) {
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
       }
     } else {
       for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        const Block4 x = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
+        const Block4 x = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const unsigned long long m = x.w[w] >> 11;

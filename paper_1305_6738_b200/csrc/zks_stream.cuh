@@ -47,6 +47,48 @@ __device__ __forceinline__ Block4 philox4x64_10(uint64_t c0, uint64_t k0, uint64
   return b;
 }
 
+// Opt-in fast stream (ZKS_RNG_PHILOX4X32, tier-3 parity only): Philox4x32-10
+// (Salmon et al. 2011; the Random123 / curand constants) keyed by the low 64 bits of the same
+// SeedSequence-derived key, the other 64 key bits in the counter's upper words.  Block b's four
+// 64-bit words are the pairs of the 4x32 blocks at counters 2b and 2b + 1, so every consumer
+// still takes x >> 11 as a 53-bit key.  32x32-bit multiplies instead of 64x64: about a quarter
+// of the integer-pipe work of Philox4x64-10 per word.
+constexpr uint32_t kPhilox32M0 = 0xD2511F53u, kPhilox32M1 = 0xCD9E8D57u;
+constexpr uint32_t kPhilox32W0 = 0x9E3779B9u, kPhilox32W1 = 0xBB67AE85u;
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += kPhilox32W0;
+      k1 += kPhilox32W1;
+    }
+    const uint32_t hi0 = __umulhi(kPhilox32M0, c.x), lo0 = kPhilox32M0 * c.x;
+    const uint32_t hi1 = __umulhi(kPhilox32M1, c.z), lo1 = kPhilox32M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
+enum : int { kRngNumpy = 0, kRngPhilox4x32 = 1 };
+
+// Block c0 of a stream: numpy's Philox4x64-10 (bit-exact, the default) or the fast stream
+__device__ __forceinline__ Block4 rng_block(uint64_t c0, uint64_t k0, uint64_t k1, int rng) {
+  if (rng == kRngNumpy) return philox4x64_10(c0, k0, k1);
+  const uint32_t ka = static_cast<uint32_t>(k0), kb = static_cast<uint32_t>(k0 >> 32);
+  const uint32_t c_hi = static_cast<uint32_t>(c0 >> 31);
+  const uint4 p = philox4x32_10(make_uint4(static_cast<uint32_t>(c0 << 1), c_hi, static_cast<uint32_t>(k1),
+                                           static_cast<uint32_t>(k1 >> 32)), ka, kb);
+  const uint4 q = philox4x32_10(make_uint4(static_cast<uint32_t>(c0 << 1) | 1u, c_hi, static_cast<uint32_t>(k1),
+                                           static_cast<uint32_t>(k1 >> 32)), ka, kb);
+  Block4 b;
+  b.w[0] = (static_cast<uint64_t>(p.x) << 32) | q.x;
+  b.w[1] = (static_cast<uint64_t>(p.y) << 32) | q.y;
+  b.w[2] = (static_cast<uint64_t>(p.z) << 32) | q.z;
+  b.w[3] = (static_cast<uint64_t>(p.w) << 32) | q.w;
+  return b;
+}
+
 // u = 1 - (x >> 11) * 2^-53, exactly (the 53-bit integer converts exactly; 1 - m*2^-53 is
 // representable for every m < 2^53).
 __device__ __forceinline__ double uniform_open_closed(uint64_t x) {

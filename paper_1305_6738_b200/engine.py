@@ -65,6 +65,7 @@ class Engine:
         self.handle = handle
         self._tables: OrderedDict[tuple, DrawTable] = OrderedDict()
         self._lock = threading.Lock()
+        self.rng = "numpy"
 
     # -- streams -------------------------------------------------------------
     def bind_stream(self):
@@ -244,6 +245,15 @@ class Engine:
         self.bind_stream()
         _native.check(self.lib.zks_stream_uniforms(self.handle, int(seed), int(repetition), int(index), int(count),
                                                    out.data_ptr()))
+
+    def set_rng(self, kind: str) -> None:
+        """Replicate streams: "numpy" (bit-exact with the reference, default) or "philox4x32"
+        (opt-in fast generator, Monte Carlo parity only)."""
+        kinds = {"numpy": 0, "philox4x32": 1}
+        if kind not in kinds:
+            raise ValueError(f"unknown stream kind {kind!r}; expected one of {sorted(kinds)}")
+        _native.check(self.lib.zks_engine_set_rng(self.handle, kinds[kind]))
+        self.rng = kind
 
     def set_chunk_bytes(self, nbytes: int = 0) -> None:
         """Budget of one chunk of pre-drawn rows (0 = the default 16 GiB); results never depend on it."""

@@ -169,6 +169,18 @@ def _enqueue(eng, config: SimulationConfig, repetition: int, first: int, count: 
     )
 
 
+def set_rng(kind: str = "numpy") -> None:
+    """Choose the replicate streams of later simulations on this process's device.
+
+    ``"numpy"`` (the default) draws every replicate from RandomStream.for_replicate
+    (distribution.py:173-187) bit for bit, so every statistic matches the reference replicate by
+    replicate.  ``"philox4x32"`` is an opt-in faster generator (Philox4x32-10 keyed by the same
+    SeedSequence key, about a quarter of the integer work per draw): the samples differ, their
+    law does not, so cutoffs agree with the default within Monte Carlo error only (tier 3).
+    """
+    _engine().set_rng(kind)
+
+
 # ---------------------------------------------------------------------------
 # reference API
 

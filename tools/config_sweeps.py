@@ -25,13 +25,12 @@ def grid(lo, hi, step):
     return tuple(round(lo + i * step, 10) for i in range(k + 1))
 
 
-def configs(replicates):
+def configs(replicates, ns3):
     return {
         "1": ("config1: untruncated Zipf gamma=2.5, n=100, 10^4 replicates",
               zk.Support.unbounded(), (2.5,), (100,), 10_000),
-        "3": ("config3: truncated Zipf K=1000, gamma 0.5..2.0 step 0.05 x n {10,20,50,100,500,1000,2000,5000,10000}",
-              zk.Support.finite(1000), grid(0.5, 2.0, 0.05), (10, 20, 50, 100, 500, 1000, 2000, 5000, 10000),
-              replicates),
+        "3": (f"config3: truncated Zipf K=1000, gamma 0.5..2.0 step 0.05 x n {{{','.join(map(str, ns3))}}}",
+              zk.Support.finite(1000), grid(0.5, 2.0, 0.05), ns3, replicates),
         "4": ("config4: untruncated Zipf gamma=2.0, n {10^5, 2x10^5, 5x10^5, 10^6}, 10^5 replicates",
               zk.Support.unbounded(), (2.0,), (100_000, 200_000, 500_000, 1_000_000), 100_000),
     }
@@ -42,11 +41,15 @@ def main():
     p.add_argument("--configs", default="1,3,4")
     p.add_argument("--steps", type=int, default=2)
     p.add_argument("--replicates", type=int, default=1_000_000, help="replicates per cell for config 3")
+    p.add_argument("--rng", default="numpy", help="numpy (bit-exact, default) or philox4x32 (opt-in fast stream)")
+    p.add_argument("--ns3", default="10,20,30,40,50,100,500,1000,2000,3000,4000,5000,10000",
+                   help="config-3 sample sizes (the paper's grid <= 10^4)")
     args = p.parse_args()
     eng = get_engine(0)
+    eng.set_rng(args.rng)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
-    table = configs(args.replicates)
+    table = configs(args.replicates, tuple(int(x) for x in args.ns3.split(",")))
     for key in args.configs.split(","):
         name, support, gammas, ns, R = table[key]
         cfgs = [zk.SimulationConfig(n=n, support=support, gamma=g, base_seed=1, replicates=R, repetitions=1)
@@ -81,7 +84,7 @@ def main():
             assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
         reps = args.steps * len(cfgs) * R
         line = {
-            "config": name, "cells": len(cfgs), "replicates_per_cell": R, "steps": args.steps,
+            "config": name, "rng": args.rng, "cells": len(cfgs), "replicates_per_cell": R, "steps": args.steps,
             "ms_per_sweep": total_ms / args.steps, "replicates_per_s": reps / (total_ms / 1e3),
             "draws_per_s": args.steps * R * len(gammas) * sum(ns) / (total_ms / 1e3),
             "per_n_replicates_per_s": {str(n): args.steps * len(gammas) * R / (ms / 1e3) for n, ms in per_n.items()},
