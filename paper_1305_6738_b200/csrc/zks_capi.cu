@@ -198,7 +198,7 @@ struct zks_table {
   double head[4] = {0, 0, 0, 0};  // cdf[0..3], +inf from L-1 on (draw_stats_kernel's head test)
   double tail_mass = 0.0;          // P(X > 64) = 1 - cdf[63]: the row kernel's cost estimate
   uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on the top 32 bits of Philox words
-  unsigned long long* mcut = nullptr;  // exact 53-bit cuts of cdf[0..63] (row_draw_kernel)
+  unsigned long long* mcut = nullptr;  // exact 53-bit cuts of cdf[0..kCutMax) (row_draw_kernel)
   // stream ordering: the upload (and guide build) runs on `home`; another stream's first use
   // waits on `ready`; the free waits on every stream that used the table
   cudaStream_t home = nullptr;
@@ -358,7 +358,8 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
   const size_t guide_bytes = (size_t(zks::kGuideEntries) * sizeof(uint16_t) + 15) & ~size_t(15);
   cudaError_t err =
-      cudaMallocAsync(&mem, cdf_slots * sizeof(double) + guide_bytes + 64 * sizeof(unsigned long long), e->stream);
+      cudaMallocAsync(&mem, cdf_slots * sizeof(double) + guide_bytes + zks::kCutMax * sizeof(unsigned long long),
+                      e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
     t->guide = reinterpret_cast<uint16_t*>(t->cdf + cdf_slots);
@@ -384,7 +385,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
     }
     if (err == cudaSuccess) {
       Timed tm(e, ZKS_KERNEL_OTHER);
-      zks::cut_kernel<<<1, 64, 0, e->stream>>>(t->cdf, t->len, t->mcut);
+      zks::cut_kernel<<<zks::kCutMax / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->mcut);
       err = launched(e);
     }
   }

@@ -10,7 +10,8 @@
 //   #{v_j >= k + 2} = P_k = #{m_j < M_k} (cdf non-decreasing => M non-increasing),
 //   count(1) = n - P_0,  count(k) = P_{k-2} - P_{k-1} (k = 2..64),
 // and the P_63 keys below M_63 are exactly the draws above 64, resolved one by one by the guide
-// + cdf search.  So per row the kernel draws and buckets n keys once (Philox4x64 + a counting
+// + cdf search -- or, for a dense finite support (64 < K <= 1024), counted the same way from all
+// K - 1 cut positions (count(k) = P_{k-2} - P_{k-1}), with no per-draw search at all.  So per row the kernel draws and buckets n keys once (Philox4x64 + a counting
 // sort by the keys' top bits, on chip) and per cell does 64 short bucket scans plus its tail --
 // instead of generating or re-reading and classifying all n draws once per gamma.  Entries of
 // the cut table from L - 1 on are 0 (the clamp to L: no draw counts above it).
@@ -36,7 +37,7 @@ namespace zks {
 
 constexpr int kRowMaxCells = 32;
 constexpr int kRowMaxN = 16384;      // keys (8 B each) + buckets of one row in shared memory
-constexpr int kRowStageMaxN = 6144;  // up to here the draw pass parks the keys in shared memory for
+constexpr int kRowStageMaxN = 2048;  // up to here the draw pass parks the keys in shared memory for
                                      // the scatter pass; above it the scatter pass regenerates them
 #ifndef ZKS_ROW_MINB
 #define ZKS_ROW_MINB 3
@@ -56,10 +57,13 @@ __device__ __forceinline__ unsigned long long exact_cut(double h) {
   return m;
 }
 
-// The cut table of a sampling table (64 entries; from L - 1 on: 0, the clamp)
+// The cut table of a sampling table: kCutMax entries, so a dense finite support (K <= kDenseMaxK)
+// has every cut; from L - 1 on: 0 (the clamp)
+constexpr int kCutMax = 1024;
+static_assert(kCutMax >= kDenseMaxK, "dense supports take every count from cut positions");
 __global__ void cut_kernel(const double* __restrict__ cdf, uint32_t L, unsigned long long* mcut) {
-  const int j = threadIdx.x;
-  if (j < 64) mcut[j] = static_cast<uint32_t>(j) + 1u < L ? exact_cut(cdf[j]) : 0ull;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < kCutMax) mcut[j] = static_cast<uint32_t>(j) + 1u < L ? exact_cut(cdf[j]) : 0ull;
 }
 
 struct RowCell {
@@ -103,10 +107,11 @@ __host__ __device__ constexpr int row_bucket_bits(int n) {
 }
 constexpr int kRowKeyPad = 2;  // sentinel keys (all ones) after the row: pair loads past a bucket's end
 // shared memory of one block of `warps` warps: keys + sentinels (+ the parked draw pass), bucket
-// starts and ends, per-warp dense histograms
+// starts and ends, and (dense supports, n <= kRowDenseHistMaxN) per-warp histograms of 65..K
+constexpr int kRowDenseHistMaxN = 4096;
 __host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps) {
   return size_t(round_up(n + kRowKeyPad, 2)) * 8 + (n <= kRowStageMaxN ? size_t(round_up(n, 2)) * 8 : 0) +
-         (size_t(1) << row_bucket_bits(n)) * 8 + size_t(warps) * dense_words * 4;
+         (size_t(1) << row_bucket_bits(n)) * 8 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
 }
 
 // 128-bit fixed-point sums (units of 2^-53): hi:lo += x
@@ -145,10 +150,39 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
   const uint32_t c0 = (lane ? Pa_up : static_cast<uint32_t>(n)) - Pa;  // count of value lane + 1
   const uint32_t c1 = (lane ? Pb_up : Pa31) - Pb;                       // count of value lane + 33
   const uint32_t T = __shfl_sync(0xffffffffu, Pb, 31);                  // draws above kKsHead
-  // the tail: every key below M_63, i.e. keys[0, E) of the buckets up to M_63's, filtered
   unsigned long long shi = 0, slo = 0;  // log-sum, 2^-53 units
   uint32_t vtop = 0, vlow = 0xffffffffu;
-  if (T) {
+  // dense finite support (kKsHead < K <= kDenseMaxK): u32 counts of kKsHead+1..vmax into the
+  // row's tail slot (what fit_ks_kernel reads) -- from the K - 65 remaining cut positions, or, when
+  // the tail is short against them, from the per-draw searches counted in the warp's histogram
+  // (the same counts and, summed exactly, the same log-sum either way)
+  const bool by_cuts = a.dense_words && (!dense || T >= static_cast<uint32_t>(a.dense_words) / 4u);
+  if (T && by_cuts) {
+    // count(k) = P_{k-2} - P_{k-1}, P_{K-1} = 0: no per-draw search
+    uint32_t* out = reinterpret_cast<uint32_t*>(C.tail + i * a.vals_stride);
+    uint32_t prev = T;  // P_63
+    for (int j0 = kKsHead; j0 < a.dense_words + kKsHead; j0 += 32) {
+      const int j = j0 + lane;
+      const uint32_t P = j < kCutMax ? pos(__ldg(C.mcut + j)) : 0u;
+      uint32_t up = __shfl_up_sync(0xffffffffu, P, 1);
+      if (lane == 0) up = prev;
+      const uint32_t cnt = up - P;  // count of value j + 1
+      const int k = j + 1;
+      if (k <= static_cast<int>(C.L) && k - kKsHead - 1 < a.dense_words) out[k - kKsHead - 1] = cnt;
+      if (cnt) {
+        const unsigned long long lk = log_fixed(a.logs, static_cast<uint32_t>(k));
+        add128(shi, slo, __umul64hi(cnt, lk), static_cast<unsigned long long>(cnt) * lk);
+        vtop = max(vtop, static_cast<uint32_t>(k));
+        vlow = min(vlow, static_cast<uint32_t>(k));
+      }
+      prev = __shfl_sync(0xffffffffu, P, 31);
+      if (prev == 0u) break;  // no draws above this chunk: later counts are never read (k > vmax)
+    }
+    vtop = warp_max_u32(vtop);
+    vlow = warp_min_u32(vlow);
+  } else if (T) {
+    // the tail list: every key below M_63, i.e. keys[0, E) of the buckets up to M_63's, filtered,
+    // each resolved by the guide + cdf search
     const unsigned long long M63 = __shfl_sync(0xffffffffu, Mb, 31);
     const uint32_t bk = static_cast<uint32_t>(M63 >> shift);
     const uint32_t E = bk >= nbk ? static_cast<uint32_t>(n) : bend[bk];
@@ -179,7 +213,7 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
       }
       const unsigned bm = __ballot_sync(0xffffffffu, in);
       if (in) {
-        if (dense)
+        if (a.dense_words)
           atomicAdd(dense + (v - kKsHead - 1), 1u);
         else
           tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
@@ -188,6 +222,15 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
     }
     vtop = warp_max_u32(vtop);
     vlow = warp_min_u32(vlow);
+    if (a.dense_words) {  // the warp's histogram into the row's tail slot, reset
+      __syncwarp();
+      uint32_t* out = reinterpret_cast<uint32_t*>(tail);
+      for (int k = lane; k < static_cast<int>(vtop) - kKsHead; k += 32) {
+        out[k] = dense[k];
+        dense[k] = 0u;
+      }
+      __syncwarp();
+    }
   }
   {  // the head's share of the log-sum: count x ln k, exact
     const unsigned long long l0 = log_fixed(a.logs, lane + 1), l1 = log_fixed(a.logs, lane + 33);
@@ -206,16 +249,6 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
   uint16_t* head = C.head + i * kKsHead;
   head[lane] = static_cast<uint16_t>(c0);  // n <= kRowMaxN: u16 counts
   head[lane + 32] = static_cast<uint16_t>(c1);
-  if (dense) {  // counts of kKsHead+1..vmax into the row's tail slot (what fit_ks_kernel reads)
-    __syncwarp();
-    uint32_t* out = reinterpret_cast<uint32_t*>(C.tail + i * a.vals_stride);
-    const int used = vmax > kKsHead ? static_cast<int>(vmax - kKsHead) : 0;
-    for (int k = lane; k < used; k += 32) {
-      out[k] = dense[k];
-      dense[k] = 0u;
-    }
-    __syncwarp();
-  }
   if (lane == 0) {
     C.ls[i] = log_sum;
     C.mn[i] = vmin;
@@ -241,10 +274,11 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
   uint32_t* bend = bstart + nbk;  // counts, then running scatter positions = bucket ends
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  uint32_t* dense = a.dense_words ? bend + nbk + warp * a.dense_words : nullptr;
+  uint32_t* dense = (a.dense_words && n <= kRowDenseHistMaxN) ? bend + nbk + warp * a.dense_words : nullptr;
+  if (dense)
+    for (int k = lane; k < a.dense_words; k += 32) dense[k] = 0u;
   __shared__ unsigned long long key_sh[2][2];  // this row's and the next row's stream keys
   __shared__ uint32_t wsum[kWarps];
-  for (int k = lane; k < a.dense_words; k += 32) dense[k] = 0u;
   if (threadIdx.x < kRowKeyPad) keys[n + threadIdx.x] = ~0ull;
   const int nb = (n + 3) >> 2;
   unsigned long long tails = 0, rows = 0;
