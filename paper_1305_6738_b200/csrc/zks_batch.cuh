@@ -102,7 +102,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
   const int lane = threadIdx.x & 31;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
-  double ls = 0.0;
+  unsigned long long shi = 0, slo = 0;  // exact log-sum (the row kernels' arithmetic)
   uint32_t mn = 0xffffffffu, mx = 0;
   for (int b = 0; b < nb; ++b) {
     const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
@@ -114,7 +114,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
-        ls += __ldg(a.logs + x[w]);
+        add128(shi, slo, 0ull, log_fixed(a.logs, x[w]));
         mn = min(mn, x[w]);
         mx = max(mx, x[w]);
         if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
@@ -123,7 +123,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
     *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
   }
   DrawStats s;
-  s.log_sum = ls;
+  s.log_sum = fixed_to_double(shi, slo);
   s.vmin = mn;
   s.vmax = mx;
   return s;

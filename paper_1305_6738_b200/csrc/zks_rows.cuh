@@ -114,15 +114,6 @@ __host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int 
          (size_t(1) << row_bucket_bits(n)) * 8 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
 }
 
-// 128-bit fixed-point sums (units of 2^-53): hi:lo += x
-__device__ __forceinline__ void add128(unsigned long long& hi, unsigned long long& lo, unsigned long long xhi,
-                                       unsigned long long xlo) {
-  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(xlo), "l"(xhi));
-}
-// ln v in units of 2^-53, exactly (ln v < 16 is a multiple of 2^-53 for v >= 2; ln 1 = 0)
-__device__ __forceinline__ unsigned long long log_fixed(const double* __restrict__ logs, uint32_t v) {
-  return __double2ull_rz(__ldg(logs + v) * 0x1p53);
-}
 
 // one cell of the row, by one warp: counts of 1..64 from the cut positions, the tail by search
 template <bool kCount>
@@ -242,7 +233,7 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
     const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, shi, o), olo = __shfl_xor_sync(0xffffffffu, slo, o);
     add128(shi, slo, ohi, olo);
   }
-  const double log_sum = static_cast<double>(shi) * 0x1p11 + static_cast<double>(slo) * 0x1p-53;
+  const double log_sum = fixed_to_double(shi, slo);
   const unsigned h0 = __ballot_sync(0xffffffffu, c0 != 0u), h1 = __ballot_sync(0xffffffffu, c1 != 0u);
   const uint32_t vmin = h0 ? static_cast<uint32_t>(__ffs(h0)) : h1 ? 32u + __ffs(h1) : vlow;
   const uint32_t vmax = T ? vtop : h1 ? 64u - __clz(h1) : 32u - __clz(h0);

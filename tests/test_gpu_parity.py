@@ -574,3 +574,25 @@ def test_row_kernel_bounds_and_many_cells(zk, K, n):
         cell = run_cell(K, g, n, 3, 0, 0, R)
         for a, b in zip(rows[g], cell):
             np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("K,n,gammas", [
+    (None, 5, (1.1, 2.0, 3.5)),
+    (None, 37, tuple(np.round(np.linspace(1.1, 3.5, 21), 6))),
+    (None, 127, (1.06, 1.1, 1.3, 2.2, 4.0)),
+    (20, 10, tuple(np.round(np.linspace(0.25, 4.0, 33), 6))),
+    (1000, 100, (0.25, 0.5, 1.0, 2.0)),
+    (20, 3, (1.0, -30.0)),
+])
+def test_small_row_kernel_matches_cells(zk, K, n, gammas):
+    # n < 128 rows: (replicate, cell) pairs lane by lane, streams drawn once per tile; every cell
+    # equals its own run (the lane kernel above n = 16) bit for bit -- long tails (gamma ~ 1.1 at
+    # n = 127), double failures (gamma = -30), rows of more than 32 cells
+    R = 1000
+    rows = _row_outputs(zk, K, n, gammas, R)
+    for g in gammas:
+        cell = run_cell(K, g, n, 3, 0, 0, R)
+        for a, b in zip(rows[g], cell):
+            np.testing.assert_array_equal(a, b)
+    if -30.0 in gammas:
+        assert (rows[-30.0][2] == 2).any()
