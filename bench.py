@@ -119,9 +119,23 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU legs
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_sample_run(replicates: int, workers: int) -> tuple[float, int, float]:
     """The oracle (numpy restatement of the reference, bit-identical to it) over the sampled
-    cells of the sweep with ``workers`` processes; returns (replicates/s, replicates, seconds)."""
+    cells of the sweep with ``workers`` processes (the reference's own Pool driver,
+    montecarlo.py:151-191); returns (replicates/s, replicates, seconds)."""
     from oracle import port
 
     total = 0
@@ -134,6 +148,29 @@ def cpu_sample_run(replicates: int, workers: int) -> tuple[float, int, float]:
     return total / dt, total, dt
 
 
+def cpu_baseline(replicates: int, steps: int = 1, warmup: int = 1) -> dict:
+    """Both CPU legs measure the same thing the same way: the oracle over the sampled cells
+    with all host cores (W = os.cpu_count()) after ``warmup`` untimed passes, plus one pass on a
+    single core (W = 1) over an eighth of the sample.  Run before CUDA is initialised in this
+    process (the Pool forks)."""
+    workers = os.cpu_count() or 1
+    for _ in range(warmup):
+        cpu_sample_run(max(replicates // 8, 512), workers)
+    total, secs = 0, 0.0
+    for _ in range(steps):
+        _, reps, dt = cpu_sample_run(replicates, workers)
+        total += reps
+        secs += dt
+    w1_reps = max(replicates // 8, 512)
+    v1, r1, d1 = cpu_sample_run(w1_reps, 1)
+    return {"value": total / secs, "unit": "replicates/s", "cores": workers, "kind": "port",
+            "sample": cpu_sample_desc(replicates) + f"; {total} replicates in {secs:.1f} s after {warmup} warm-up",
+            "cpu_model": cpu_model(),
+            "w1": {"value": v1, "cores": 1, "sample": f"{len(CPU_SAMPLE_GAMMAS) * len(NS)} cells x {w1_reps} "
+                                                      f"replicates, {r1} in {d1:.1f} s"},
+            "wcores": {"value": total / secs, "cores": workers}}
+
+
 def cpu_sample_desc(replicates: int) -> str:
     return (f"{len(CPU_SAMPLE_GAMMAS)} of 21 gammas {CPU_SAMPLE_GAMMAS} x n {NS} = "
             f"{len(CPU_SAMPLE_GAMMAS) * len(NS)} cells x {replicates} replicates, K=inf, base_seed=1, "
@@ -143,27 +180,21 @@ def cpu_sample_desc(replicates: int) -> str:
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    workers = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_sample_run(args.cpu_replicates, workers)
-    total = 0
-    secs = 0.0
-    for _ in range(args.steps):
-        _, reps, dt = cpu_sample_run(args.cpu_replicates, workers)
-        total += reps
-        secs += dt
-    value = total / secs
+    t0 = time.perf_counter()
+    cpu = cpu_baseline(args.cpu_replicates, steps=args.steps, warmup=args.warmup)
+    value = cpu["value"]
+    secs = time.perf_counter() - t0
     line = {
         "metric": METRIC, "value": value, "unit": "replicates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": len(CPU_SAMPLE_GAMMAS) * len(NS) * args.cpu_replicates / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config2 untruncated sweep (bounded CPU sample)", "support": "inf",
                    "gammas": list(CPU_SAMPLE_GAMMAS), "ns": list(NS), "replicates_per_cell": args.cpu_replicates,
                    "repetitions": 1, "base_seed": 1},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "replicates/s", "cores": workers, "kind": "port",
-                         "sample": cpu_sample_desc(args.cpu_replicates)},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "replicates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": secs,
     }
     print(json.dumps(line), flush=True)
 
@@ -175,69 +206,99 @@ def hbm_peak_gbs() -> tuple[float, str]:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
     except (OSError, KeyError, ValueError):
-        return 7700.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+        return 6650.0, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
 
 
-def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms) -> dict:
-    """Roofline of the dominant kernel of the sweep (largest summed device time in the timed
-    region, CUDA events around every launch on the engine stream).
+def ncu_counts() -> dict:
+    """Per-sweep warp instructions and DRAM bytes of each kernel kind, from the committed ncu
+    launch list of this bench command (tools/ncu_launch_table.py -> profiles/r02_launch_inst.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_launch_inst.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
-    Algorithmic bytes per kernel kind, per sweep, from the reference algorithm's data flow and
-    the in-kernel work counters:
-      stage   4 B per staged draw word written
-      draw    4 B per staged word read + 148 B per pre-drawn row (u16 head counts 128, log-sum 8,
-              min / max / tail length 12) + 2 B per tail value
-      fit     the rows and tail values read back + 17 B per replicate written (ks, gamma_hat, status)
+
+def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms, sm_mhz, sms) -> dict:
+    """The dominant kernel (largest summed device time in the timed region, CUDA events around
+    every launch on the engine stream) against the resource that binds it.
+
+    The replicate math moves few bytes (about 40 B per replicate in and out), so
+    HBM does not bind any kernel of the path; ncu shows them issue- and latency-bound (DRAM a few
+    per cent).  The line therefore reports, per kernel kind, the issue-slot fraction -- warp
+    instructions (the committed ncu launch list of this command) over the SM's issue slots
+    (sms x 4 schedulers x the SM clock sampled during the run) in the kind's measured time -- beside
+    its algorithmic HBM bytes over the measured copy bandwidth, and names the larger one as
+    ``bound``.  Algorithmic bytes per sweep:
+      row     148 B per pre-drawn row written (u16 counts 128, log-sum 8, min / max / tail length
+              12) + 2 B per tail value
+      fit     the same rows read back + 17 B per replicate written (ks, gamma_hat, status)
       batch   17 B per replicate written (n < 128: draws, fits and KS stay on chip)
-      select  8 B per KS value per radix pass (8 passes)
+      select  8 B per KS value per full radix pass (2 full passes, then candidates only)
     """
-    (attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, staged, staged_made, redrawn,
-     pre_rows, pre_tails) = work
+    (attempts, draws, evals, eval_terms, norm_terms, ks_terms, ks_tails, ks_tiles, keys, pre_rows, pre_tails) = work
     per_gpu = R if world == 1 else shard[1] - shard[0]
     small_cells = sum(1 for n in NS if n < 128) * len(GAMMAS)
     row_bytes = 128 + 8 + 12
     alg = {
-        "stage": 4.0 * staged_made,
-        "draw": 4.0 * staged + row_bytes * pre_rows + 2.0 * pre_tails,
+        "row": row_bytes * pre_rows + 2.0 * pre_tails,
         "fit": row_bytes * pre_rows + 2.0 * pre_tails + 17.0 * pre_rows,
         "batch": 17.0 * small_cells * per_gpu,
-        "select": 8.0 * 8 * ncells * R,
+        "select": 8.0 * 2 * ncells * per_gpu,
     }
     steps = max(args.steps, 1)
+    clk_hz = (sm_mhz or 1965.0) * 1e6
+    issue_peak = sms * 4 * clk_hz  # warp instructions per second
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    ncu = ncu_counts()
     kern = {k: {"ms_per_sweep": ms / steps, "launches_per_sweep": n / steps} for k, (ms, n) in ktimes.items() if n}
     kernel_ms = sum(v["ms_per_sweep"] for v in kern.values())
     for k, v in kern.items():
         v["share_of_kernel_time"] = v["ms_per_sweep"] / kernel_ms if kernel_ms else None
-        if k in alg:
+        secs = v["ms_per_sweep"] / 1e3
+        if k in alg and secs:
             v["algorithmic_gb_per_sweep"] = alg[k] / 1e9
-            v["achieved_gbs"] = alg[k] / (v["ms_per_sweep"] / 1e3) / 1e9 if v["ms_per_sweep"] else None
+            v["hbm_frac"] = alg[k] / secs / 1e9 / hbm_peak
+        c = ncu.get("kinds", {}).get(k)
+        if c and secs:
+            v["warp_inst_per_sweep"] = c["warp_inst_per_sweep"]
+            v["issue_frac"] = c["warp_inst_per_sweep"] / secs / issue_peak
+            v["dram_bytes_per_sweep"] = c["dram_bytes_per_sweep"]
+            v["dram_frac"] = c["dram_bytes_per_sweep"] / secs / 1e9 / hbm_peak
     dom = max(kern, key=lambda k: kern[k]["ms_per_sweep"])
-    peak, peak_src = hbm_peak_gbs()
     d = kern[dom]
-    per_launch_bytes = alg.get(dom, 0.0) / max(d["launches_per_sweep"], 1)
-    per_launch_ms = d["ms_per_sweep"] / max(d["launches_per_sweep"], 1)
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms else 0.0
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": KERNEL_NAMES.get(dom, dom), "algorithmic_bytes_per_launch": per_launch_bytes,
-            "launch_ms": per_launch_ms, "peak_source": peak_src,
-            "timing": "CUDA events around every launch on the engine stream, summed over the timed steps"}
-    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh)
-        if tr.get("kernel") == roof["kernel"]:
-            ratio = tr["dram_bytes"] / tr["algorithmic_bytes"]
-            roof["traffic"] = ratio * per_launch_bytes
-            roof["traffic_over_algorithmic"] = ratio
-            roof["traffic_source"] = tr["source"]
-    except (OSError, KeyError, ValueError, ZeroDivisionError):
-        pass
+    launch_ms = d["ms_per_sweep"] / max(d["launches_per_sweep"], 1)
+    issue = d.get("issue_frac")
+    hbm = d.get("hbm_frac", 0.0)
+    if issue is not None and issue >= hbm:
+        per_launch_inst = d["warp_inst_per_sweep"] / max(d["launches_per_sweep"], 1)
+        achieved = per_launch_inst / (launch_ms / 1e3)
+        roof = {"bound": "issue", "achieved": achieved, "peak": issue_peak, "unit": "warp-instructions/s",
+                "frac": achieved / issue_peak,
+                "peak_source": f"{sms} SMs x 4 schedulers x {clk_hz / 1e6:.0f} MHz (median SM clock sampled in the "
+                               f"timed region): one warp instruction per scheduler per cycle",
+                "achieved_source": "warp instructions per launch from the committed ncu launch list of this command "
+                                   f"({ncu.get('source', '?')}) over the CUDA-event launch time"}
+    else:
+        per_launch_bytes = alg.get(dom, 0.0) / max(d["launches_per_sweep"], 1)
+        achieved = per_launch_bytes / (launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "peak_source": hbm_src}
+    dram = d.get("dram_bytes_per_sweep")
+    roof.update({
+        "kernel": KERNEL_NAMES.get(dom, dom), "launch_ms": launch_ms,
+        "traffic": dram / max(d["launches_per_sweep"], 1) if dram is not None else None,
+        "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+        "hbm": {"algorithmic_bytes_per_launch": alg.get(dom, 0.0) / max(d["launches_per_sweep"], 1),
+                "achieved_gbs": alg.get(dom, 0.0) / (d["ms_per_sweep"] / 1e3) / 1e9 if d["ms_per_sweep"] else None,
+                "peak_gbs": hbm_peak, "frac": hbm, "peak_source": hbm_src},
+        "timing": "CUDA events around every launch on the engine stream, summed over the timed steps",
+    })
     # SURVEY.md 8(d)'s compute roofline of the REFERENCE algorithm on the same inputs: W_INT =
     # 5 mulhilo per draw (Philox4x64-10, n draws per replicate), T = the power terms it sums
     # (Newton moment evaluations x their m-rule / K terms, the fitted normaliser, min(kmax, 4096)
     # KS terms; counted in-kernel at the same iterates), each one exp + 3 FMA-class ops;
     # T_ideal = max(W_INT / P_INT, T c_exp / P_FP64) with the pipe peaks probed on this device.
-    # ratio = T_ideal / measured sweep time (> 1: the fit tables and Euler-Maclaurin tails skip
-    # work the reference algorithm does).
     exp_flops = peaks["dfma_flops"] / peaks["exp_per_s"]  # DFMA-equivalent FLOP of one fp64 exp
     terms = eval_terms + norm_terms + ks_terms
     fp64_flops = terms * (exp_flops + 6.0)
@@ -246,20 +307,21 @@ def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms) -> di
     t_fp64 = fp64_flops / peaks["dfma_flops"]
     t_int = mul64 / peaks["mul64_per_s"]
     sweep_s = total_ms / steps / 1e3
-    kernel_s = kernel_ms / 1e3
     roof["compute"] = {
-        "reference_algorithm": {"t_ideal_ms_per_sweep": max(t_fp64, t_int) * 1e3, "bound": "fp64" if t_fp64 > t_int
-                                else "int64_mul", "ratio_to_measured": max(t_fp64, t_int) / sweep_s,
-                                "power_terms": terms, "philox_mulhilo": mul64},
-        "fp64": {"reference_tflop_equiv_per_s": fp64_flops / sweep_s / 1e12, "peak_tflops": peaks["dfma_flops"] / 1e12,
-                 "t_ideal_ms_per_sweep": t_fp64 * 1e3},
-        "int64_mul": {"reference_tmul_per_s": mul64 / sweep_s / 1e12, "peak_tmul_s": peaks["mul64_per_s"] / 1e12,
-                      "t_ideal_ms_per_sweep": t_int * 1e3,
-                      "made_on_device_per_sweep": 5.0 * (draws + staged_made)},
+        "reference_algorithm_at_peak": {
+            "t_ideal_ms_per_sweep": max(t_fp64, t_int) * 1e3, "bound": "fp64" if t_fp64 > t_int else "int64_mul",
+            "speedup_over_reference_algorithm_at_peak": max(t_fp64, t_int) / sweep_s,
+            "note": "the time the REFERENCE algorithm would need on this GPU at its FP64 / 64-bit-multiply peaks, "
+                    "over the measured sweep time: > 1 means the engine does less work than the reference "
+                    "algorithm (fit tables, Euler-Maclaurin KS endpoints, one stream per sweep row)",
+            "power_terms": terms, "philox_mulhilo": mul64},
+        "engine": {"philox_mulhilo_per_sweep": 5.0 * draws,
+                   "int64_mul_frac_of_sweep": 5.0 * draws / peaks["mul64_per_s"] / sweep_s,
+                   "peak_tmul_s": peaks["mul64_per_s"] / 1e12, "peak_dfma_tflops": peaks["dfma_flops"] / 1e12},
         "peak_source": "measured on this device by zks_probe_peaks (DFMA / fp64 exp / 64-bit mulhilo micro-kernels)",
         "work_per_sweep": {"replicates": ncells * per_gpu, "attempts": attempts, "philox_draws": draws,
-                           "staged_words_read": staged, "staged_words_made": staged_made,
-                           "staged_rows_redrawn": redrawn, "moment_evals": evals,
+                           "keys_bucketed": keys, "pre_drawn_rows": pre_rows, "pre_drawn_tail_values": pre_tails,
+                           "moment_evals": evals,
                            "reference_power_terms": {"moments": eval_terms, "normaliser": norm_terms, "ks": ks_terms},
                            "ks_tail_endpoints": ks_tails, "fp64_exp_dfma_equiv": exp_flops},
     }
@@ -268,14 +330,19 @@ def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms) -> di
     return roof
 
 
-KERNEL_NAMES = {"stage": "stage_uniforms_kernel", "draw": "draw_stats_kernel", "fit": "fit_ks_kernel",
+KERNEL_NAMES = {"row": "row_draw_kernel", "draw": "draw_stats_kernel", "fit": "fit_ks_kernel",
                 "retry": "retry_kernel", "batch": "replicate_batch_kernel", "single": "replicate_kernel",
-                "select": "select_pass_kernel", "other": "other"}
+                "select": "select_kernel", "other": "other"}
 
 
 # ----------------------------------------------------------------------------- GPU leg
 
 def run_b200(args, world, rank, local):
+    # the CPU leg first, before this process holds a CUDA context (the reference's Pool forks)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_replicates)
+
     import torch
     import torch.distributed as dist
 
@@ -312,7 +379,7 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize()
 
     # work counters for the roofline: one instrumented sweep outside the timed region
-    counters = torch.zeros(13, dtype=torch.int64, device=dev)
+    counters = torch.zeros(11, dtype=torch.int64, device=dev)
     eng.set_counters(counters)
     sweep()
     torch.cuda.synchronize()
@@ -352,7 +419,16 @@ def run_b200(args, world, rank, local):
     for row in rows.values():
         assert all(0.0 < c < 1.0 for c in row) and list(row) == sorted(row), row
 
-    roof = roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    roof = roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms, clock.get("sm_mhz"), sms)
+    # per sample size: a sweep row's replicates over its span (first start to last finish of its
+    # cells; the cells of a row are computed jointly, one stream per replicate for all gammas)
+    per_n = {}
+    for n in NS:
+        mine = [p for p in plans if p.config.n == n]
+        t0 = min(plans[0].started.elapsed_time(p.started) for p in mine)
+        t1 = max(plans[0].started.elapsed_time(p.finished) for p in mine)
+        per_n[str(n)] = len(mine) * (R if world == 1 else shard[1] - shard[0]) / ((t1 - t0) / 1e3) if t1 > t0 else None
     # end to end through the public API (host tables built + uploaded each step)
     e2e = None
     if not args.no_e2e:
@@ -382,13 +458,6 @@ def run_b200(args, world, rank, local):
                "d2h_bytes_per_step": ncells * (4 + 1) * 8 + (4 * ncells if world > 1 else 0),
                "api": "paper_1305_6738_b200.build_table" if world == 1 else "paper_1305_6738_b200.parallel.build_table"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        workers = os.cpu_count() or 1
-        v, reps, dt = cpu_sample_run(args.cpu_replicates, workers)
-        cpu = {"value": v, "unit": "replicates/s", "cores": workers, "kind": "port",
-               "sample": cpu_sample_desc(args.cpu_replicates) + f"; {reps} replicates in {dt:.1f} s"}
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "replicates/s", "n_gpus": world, "steps": args.steps,
@@ -399,6 +468,9 @@ def run_b200(args, world, rank, local):
                        "repetitions": 1, "base_seed": 1, "parallelism": f"dp{world}",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": roof,
+            "per_n_replicates_per_s": per_n,
+            "per_gamma_n": "every (gamma, n) cell of a row runs at its row's rate (one stream per replicate, "
+                           "counted for all 21 gammas in the same launches)",
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": timed_launches,

@@ -13,7 +13,7 @@ from ._build import LIB
 ZKS_OK, ZKS_EINVAL, ZKS_ECUDA = 0, 1, 2
 STATUS_OK, STATUS_RETRIED, STATUS_FAILED = 0, 1, 2
 MLE_TABLE, MLE_DIRECT = 0, 1
-KERNEL_KINDS = ("stage", "draw", "fit", "retry", "batch", "single", "select", "other")  # ZKS_KERNEL_*
+KERNEL_KINDS = ("row", "draw", "fit", "retry", "batch", "single", "select", "other")  # ZKS_KERNEL_*
 ABI_VERSION = 3
 
 # every symbol include/zipfks_b200.h declares

@@ -102,7 +102,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
   const int lane = threadIdx.x & 31;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
-  unsigned long long shi = 0, slo = 0;  // exact log-sum (the row kernels' arithmetic)
+  double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0;
   for (int b = 0; b < nb; ++b) {
     const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
@@ -114,7 +114,7 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       if (vb[w]) {
-        add128(shi, slo, 0ull, log_fixed(a.logs, x[w]));
+        ls += __ldg(a.logs + x[w]);
         mn = min(mn, x[w]);
         mx = max(mx, x[w]);
         if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
@@ -123,68 +123,10 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
     *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
   }
   DrawStats s;
-  s.log_sum = fixed_to_double(shi, slo);
+  s.log_sum = ls;
   s.vmin = mn;
   s.vmax = mx;
   return s;
-}
-
-// The same draws by one lane from its staged row of 32-bit words t = x >> 32 (sweeps): values
-// 1..4 by the exact cut tests t < a.tcut[j] (u > cdf[j]), larger ones by the guide + cdf search
-// on the word's largest u, accepted when the cdf entry below lies under its smallest u.  Returns
-// false when some word leaves its value undecided (the caller redraws from Philox).
-__device__ __forceinline__ bool draw_sample_lane_staged(const ReplicateArgs& a, const uint32_t* __restrict__ row,
-                                                        const uint16_t* __restrict__ guide, uint16_t* v, uint8_t* lh,
-                                                        DrawStats& st) {
-  const int lane = threadIdx.x & 31;
-  const int n = static_cast<int>(a.n);
-  const int nb = (n + 3) >> 2;
-  double ls = 0.0;
-  uint32_t mn = 0xffffffffu, mx = 0, amb = 0;
-  for (int b = 0; b < nb; ++b) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(row) + b);
-    const uint32_t t4[4] = {q.x, q.y, q.z, q.w};
-    bool vb[4], big[4];
-    double uu[4];
-    uint32_t x[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t t = t4[w];
-      uint32_t val = 1;
-      inc_if_lt(val, t, a.tcut[0]);
-      inc_if_lt(val, t, a.tcut[1]);
-      inc_if_lt(val, t, a.tcut[2]);
-      inc_if_lt(val, t, a.tcut[3]);
-      vb[w] = 4 * b + w < n;
-      if (vb[w]) flag_if_any_eq(amb, t, a.tcut[0], a.tcut[1], a.tcut[2], a.tcut[3]);
-      big[w] = vb[w] && val == 5u;
-      x[w] = val;
-      uu[w] = 1.0 - static_cast<double>(t) * 0x1p-32;  // the word's largest u
-    }
-    uint32_t s[4];
-    draw_block_u(uu, big, guide, a, s);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      if (big[w]) {
-        const double ulo = uu[w] - (0x1p-32 - 0x1p-53);  // its smallest u
-        if (s[w] >= 2u && __ldg(a.cdf + s[w] - 2) >= ulo) amb = 1u;
-        x[w] = s[w];
-      }
-      if (vb[w]) {
-        ls += __ldg(a.logs + x[w]);
-        mn = min(mn, x[w]);
-        mx = max(mx, x[w]);
-        if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
-      } else {
-        x[w] = 0u;
-      }
-    }
-    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
-  }
-  st.log_sum = ls;
-  st.vmin = mn;
-  st.vmax = mx;
-  return amb == 0u;
 }
 
 __device__ __forceinline__ double fit_target(double log_sum, uint32_t vmin, int K, double dn) {
@@ -415,15 +357,8 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     // 1-2. stream key and sample of this lane's replicate
     uint16_t* mv = vals + lane * a.vals_stride;
     DrawStats st{0.0, 0u, 0u};
-    bool drawn = false;
     uint8_t* lh = reinterpret_cast<uint8_t*>(hist);  // lane histograms, zero between batches
-    if (active && a.ubuf) {  // sweeps: the row's staged words, shared by every gamma of the row
-      drawn = draw_sample_lane_staged(a, a.ubuf + (a.first + r0 + lane - a.ubuf_first) * a.ubuf_stride, guide, mv, lh,
-                                      st);
-      if (!drawn)
-        for (int v = 0; v <= static_cast<int>(kKsHead); ++v) lh[v * 32 + lane] = 0;
-    }
-    if (active && !drawn) {
+    if (active) {
       uint64_t k0, k1;
       stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
       st = draw_sample_lane(a, k0, k1, guide, mv, lh);
@@ -431,9 +366,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     __syncwarp();
     if (kCount) {
       wk.attempts += nrep;
-      const unsigned long long d = a.n, nd = __popc(__ballot_sync(0xffffffffu, active && !drawn));
-      wk.draws += nd * d;
-      if (a.ubuf) wk.staged += static_cast<unsigned long long>(nrep) * d;
+      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
     }
 
     // 3. exponent fits, one replicate per lane
@@ -721,64 +654,29 @@ __global__ void __launch_bounds__(kThreads) retry_kernel(ReplicateArgs a, const 
   }
 }
 
-// Staged draw words of replicate indices [first, first + count) of stream (seed, rep, .): row i
-// holds, for the n draws of index first + i (padded to `stride`), the top 32 bits t = x >> 32 of
-// each Philox word x -- u = 1 - (x >> 11) 2^-53 lies in [1 - (t+1) 2^-32 + 2^-53, 1 - t 2^-32].
-// One warp per replicate.  Shared by every cell of a sweep with the same (n, base_seed,
-// repetition): build_table reuses base_seed for all cells (montecarlo.py:276-277), so they
-// consume identical streams.  Half the bytes of staged doubles; the rare draw whose 32 bits do
-// not decide its value sends its replicate back to the exact Philox path (draw_stats_kernel).
-__global__ void __launch_bounds__(256) stage_uniforms_kernel(uint64_t seed, uint64_t rep, uint64_t first,
-                                                             uint64_t count, int64_t n, int64_t stride, uint32_t* out,
-                                                             unsigned long long* counters) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t nb = (n + 3) >> 2;
-  unsigned long long made = 0;
-  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < count; i += warps) {
-    uint64_t k0, k1;
-    stream_key(seed, rep, first + i, k0, k1);
-    uint32_t* row = out + i * stride;
-    for (int64_t b = lane; b < nb; b += 32) {
-      const Block4 r = philox4x64_10(static_cast<uint64_t>(b) + 1ull, k0, k1);
-      uint4 q;
-      q.x = static_cast<uint32_t>(r.w[0] >> 32);
-      q.y = static_cast<uint32_t>(r.w[1] >> 32);
-      q.z = static_cast<uint32_t>(r.w[2] >> 32);
-      q.w = static_cast<uint32_t>(r.w[3] >> 32);
-      __stcs(reinterpret_cast<uint4*>(row + 4 * b), q);
-    }
-    made += 4 * nb;
-  }
-  if (counters && lane == 0 && made) atomicAdd(counters + kWorkFields, made);
-}
-
 // The draw phase on its own, at high occupancy: one warp per replicate of [first, first+count)
 // draws its sample and writes what the fit and the KS scan need -- log-sum, min, max, the counts
 // of the values 1..kKsHead and the list of values above it -- so fit_ks_kernel never touches the
-// n draws again.  Draws from Philox, or from a staged sweep buffer of 32-bit words (a.ubuf).
+// n draws again (n above the row kernel's range: kRowMaxN < n <= kPreMaxN, zks_rows.cuh).
 //
 // Values 1..4 are counted without a search: with h = cdf[0..3] and the exact cuts T_j of the
-// 32-bit words (u > h_j <=> t < T_j, t = x >> 32 for staged and Philox words alike; h_j = +inf
+// 32-bit words (u > h_j <=> t < T_j, t = x >> 32 of the Philox word; h_j = +inf
 // from L-1 on clamps to L, distribution.py:200-201), a per-block table indexed by a word's top
 // 10 bits holds the count increment of the value every word of that 2^22-wide range takes, or
 // 0 when the range holds a cut or lies above h_3.  Those words -- 5 % of them at gamma = 2.5,
 // 36 % at 1.5, plus the rare ranges with a cut -- are pushed onto a warp queue and resolved 32 at
-// a time by the guide + cdf search with every lane busy, so divergence costs nothing; a staged
-// word is searched with its largest u and accepted when the cdf entry below lies under its
-// smallest u.  A replicate with an undecided staged word is redrawn from Philox (exact), about
-// one in 200 at n = 1000.
+// a time by the guide + cdf search with every lane busy, so divergence costs nothing.
 constexpr int kDrawQueue = 160;  // entries per warp: < 32 left over + 4 x 32 pushed per step
-constexpr int kCutTabBits = 10;  // the cut table: one entry per 2^22-wide range of staged words
+constexpr int kCutTabBits = 10;  // the cut table: one entry per 2^22-wide range of 32-bit words
 
 // The cut table of a sampling table: entry i covers the words t in [i 2^22, (i+1) 2^22).  With
 // the exact cuts T_j (u > cdf[j] <=> t < T_j, t = T_j undecided), a range holding no cut decides
 // the value 1 + #{j : T_j > t} of all its words: the entry is the count increment 1 << 8(v-1)
 // for v <= 4.  A range above h_3 whose extreme uniforms (u_max = 1 - i 2^-10 and u_min =
-// 1 - (i+1) 2^-10 + 2^-53, the bounds of u for a staged word or a Philox draw whose top 32 bits
-// lie in the range) see the same count c of the first 64 cdf entries below them decides the value
-// v = c + 1 <= 64 of all its words (no cdf entry lies in [u_min, u_max), so no staged word of it
-// is undecided either): the entry is kDirect | v, counted straight into the lane's bin.  Any
+// 1 - (i+1) 2^-10 + 2^-53, the bounds of u for a Philox draw whose top 32 bits lie in the range)
+// see the same count c of the first 64 cdf entries below them decides the value v = c + 1 <= 64
+// of all its words (no cdf entry lies in [u_min, u_max)): the entry is kDirect | v, counted
+// straight into the lane's bin.  Any
 // other range is 0: queued for the exact search.  head64 = cdf[0..63] (+inf from L-1 on).
 constexpr uint32_t kDirect = 0x80000000u;
 __device__ __forceinline__ uint32_t count_below(const double* head64, double u) {
@@ -824,36 +722,24 @@ struct DrawRowOut {
   uint32_t mn, mx, m;
 };
 
-// One replicate row (warp-cooperative).  kStaged: 32-bit staged words (returns false when some
-// word was undecided: the caller redraws the row with kStaged = false).
-template <bool kStaged, typename BinT>
-__device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, const uint32_t* __restrict__ urow,
-                                         const uint16_t* __restrict__ guide, const uint32_t* __restrict__ ctab,
-                                         BinT* bins, void* qmem, uint32_t* dense, uint16_t* tail, uint16_t* head,
-                                         DrawRowOut& o, int lane) {
-  using Q = typename std::conditional<kStaged, uint32_t, double>::type;
-  Q* queue = reinterpret_cast<Q*>(qmem);
+// One replicate row (warp-cooperative).
+template <typename BinT>
+__device__ __forceinline__ void draw_row(const ReplicateArgs& a, uint64_t idx, const uint16_t* __restrict__ guide,
+                                         const uint32_t* __restrict__ ctab, BinT* bins, double* queue,
+                                         uint32_t* dense, uint16_t* tail, uint16_t* head, DrawRowOut& o, int lane) {
   const bool two = a.guide_levels == 2;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   const unsigned lt = (1u << lane) - 1u;
   uint64_t k0 = 0, k1 = 0;
-  if (!kStaged) stream_key(a.seed, a.rep, idx, k0, k1);
+  stream_key(a.seed, a.rep, idx, k0, k1);
   double ls = 0.0;
   uint32_t mn = 0xffffffffu, mx = 0, m = 0;
   uint32_t acc = 0;          // this lane's counts of the values 1..4, 8-bit fields (flushed below)
   uint32_t acc02 = 0, acc13 = 0;  // ... accumulated in 16-bit fields
-  uint32_t amb = 0;                         // staged: some word undecided
   int qn = 0;                               // queued draws (warp-uniform)
   // one queued draw per lane: value by guide + search, then bin / tail
-  auto resolve = [&](Q q, bool ok) {
-    double ur, ulo = 0.0;
-    if (kStaged) {
-      ur = 1.0 - static_cast<double>(q) * 0x1p-32;  // largest u of the word (exact)
-      ulo = ur - (0x1p-32 - 0x1p-53);                // smallest u (exact)
-    } else {
-      ur = q;
-    }
+  auto resolve = [&](double ur, bool ok) {
     uint32_t lo, hi;
     guide_bracket_fine(ur, guide, a.guide_fine, two, lo, hi);
     if (!ok) hi = lo;
@@ -864,7 +750,6 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
       else
         lo = mid + 1;
     }
-    if (kStaged && ok && lo > 0u && __ldg(a.cdf + lo - 1) >= ulo) amb = 1u;
     const uint32_t v = min(lo + 1, a.L);
     if (ok) {
       mn = min(mn, v);
@@ -882,30 +767,17 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     }
     m += __popc(bm);
   };
-  // staged rows: the next block's 16-byte load is issued before this block is used
-  uint4 p = make_uint4(0u, 0u, 0u, 0u);
-  if (kStaged && lane < nb) p = __ldcs(reinterpret_cast<const uint4*>(urow) + lane);
   // one step: lane b's block of 4 draws.  A word's top 10 bits index ctab: the count increment
   // of its value 1..4 (1 << 8(v-1)), or 0 = queue it (value above 4, or a cut inside the bin);
   // kMasked for the last step (words past n count nowhere)
   auto step = [&](int b, auto masked) {
     uint32_t t4[4];
-    Q w4[4];
-    if (kStaged) {
-      t4[0] = p.x;
-      t4[1] = p.y;
-      t4[2] = p.z;
-      t4[3] = p.w;
+    double w4[4];
+    const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
 #pragma unroll
-      for (int w = 0; w < 4; ++w) w4[w] = t4[w];
-      p = b + 32 < nb ? __ldcs(reinterpret_cast<const uint4*>(urow) + b + 32) : make_uint4(0u, 0u, 0u, 0u);
-    } else {
-      const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        t4[w] = static_cast<uint32_t>(r.w[w] >> 32);
-        w4[w] = uniform_open_closed(r.w[w]);
-      }
+    for (int w = 0; w < 4; ++w) {
+      t4[w] = static_cast<uint32_t>(r.w[w] >> 32);
+      w4[w] = uniform_open_closed(r.w[w]);
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -927,7 +799,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
     __syncwarp();
     while (qn >= 32) {
       qn -= 32;
-      const Q q = queue[qn + lane];
+      const double q = queue[qn + lane];
       __syncwarp();
       resolve(q, true);
     }
@@ -950,7 +822,7 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   flush();
   if (qn) {
     const bool ok = lane < qn;
-    const Q q = ok ? queue[lane] : Q(0);
+    const double q = ok ? queue[lane] : 0.0;
     __syncwarp();
     resolve(q, ok);
   }
@@ -978,20 +850,17 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   if (lane < 4) hc0 += ((lane & 1) ? c13 : c02) >> (16 * (lane >> 1)) & 0xffffu;
   for (int i = lane; i < kKsHead * 8 * static_cast<int>(sizeof(BinT)); i += 32)
     reinterpret_cast<uint32_t*>(bins + 32)[i] = 0u;
-  const bool undecided = kStaged && __any_sync(0xffffffffu, amb);
   if (dense) {  // counts of kKsHead+1..K into the row's tail slot (u32), the warp histogram reset
     __syncwarp();
     uint32_t* out = reinterpret_cast<uint32_t*>(tail);
     for (int i = lane; i < a.dense_words; i += 32) {
-      if (!undecided) out[i] = dense[i];
+      out[i] = dense[i];
       dense[i] = 0u;
     }
     __syncwarp();
   }
-  if (!undecided) {
-    head[lane] = static_cast<uint16_t>(hc0);  // n <= kPreMaxN: u16 counts
-    head[lane + 32] = static_cast<uint16_t>(hc1);
-  }
+  head[lane] = static_cast<uint16_t>(hc0);  // n <= kPreMaxN: u16 counts
+  head[lane + 32] = static_cast<uint16_t>(hc1);
   mn = min(mn, hc0 ? lane + 1u : (hc1 ? lane + 33u : 0xffffffffu));
   mx = max(mx, hc1 ? lane + 33u : (hc0 ? lane + 1u : 0u));
   o.mn = warp_min_u32(mn);
@@ -1000,7 +869,6 @@ __device__ __forceinline__ bool draw_row(const ReplicateArgs& a, uint64_t idx, c
   ls += static_cast<double>(hc0) * __ldg(a.logs + lane + 1) + static_cast<double>(hc1) * __ldg(a.logs + lane + 33);
   o.ls = warp_sum(ls);
   o.m = m;
-  return !undecided;
 }
 
 template <bool kCount, bool kWide>
@@ -1018,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   // most one queued draw per pop and there are <= n/32 + 1 pops, plus its direct draws (<= 4 per
   // step of its <= n/128 + 1 steps): u8 up to kNarrowBinsMaxN
   BinT* bins = reinterpret_cast<BinT*>(wbase);
-  void* queue = wbase + (kKsHead + 1) * 32 * sizeof(BinT);
+  double* queue = reinterpret_cast<double*>(wbase + (kKsHead + 1) * 32 * sizeof(BinT));
   uint32_t* dense = a.dense_words ? reinterpret_cast<uint32_t*>(wbase + draw_warp_bytes(kWide)) : nullptr;
   for (int i = lane; i < a.dense_words; i += 32) dense[i] = 0u;
   load_guide(guide, a.guide, 1);
@@ -1030,29 +898,13 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
   for (int v = 0; v <= static_cast<int>(kKsHead); ++v) bins[v * 32 + lane] = 0;
   __syncthreads();
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  unsigned long long philox = 0, staged = 0, redrawn = 0, rows = 0, tails = 0;
+  unsigned long long rows = 0, tails = 0;
   for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.count; i += warps) {
     const uint64_t idx = a.first + i;
     uint16_t* tail = tail_out + i * a.vals_stride;
     uint16_t* head = head_out + i * kKsHead;
     DrawRowOut o;
-    bool done = false;
-    if (a.ubuf) {
-      // the warp's next row into L2 while this one is drawn (its loads then wait on L2, not HBM)
-      if (i + warps < a.count) {
-        const char* next = reinterpret_cast<const char*>(a.ubuf + (idx + warps - a.ubuf_first) * a.ubuf_stride);
-        for (int64_t off = 128 * lane; off < a.n * 4; off += 128 * 32)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(next + off));
-      }
-      done = draw_row<true>(a, idx, a.ubuf + (idx - a.ubuf_first) * a.ubuf_stride, guide, ctab, bins, queue, dense,
-                            tail, head, o, lane);
-      staged += a.n;
-      redrawn += !done;
-    }
-    if (!done) {
-      draw_row<false>(a, idx, nullptr, guide, ctab, bins, queue, dense, tail, head, o, lane);
-      philox += a.n;
-    }
+    draw_row(a, idx, guide, ctab, bins, queue, dense, tail, head, o, lane);
     if (lane == 0) {
       ls_out[i] = o.ls;
       min_out[i] = o.mn;
@@ -1063,11 +915,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_DRAW_MINB) draw_stats_kernel(Rep
     tails += o.m;
   }
   if (kCount && lane == 0) {
-    if (philox) atomicAdd(a.counters + 1, philox);
-    if (staged) atomicAdd(a.counters + 8, staged);
-    if (redrawn) atomicAdd(a.counters + kWorkFields + 1, redrawn);
-    if (rows) atomicAdd(a.counters + kWorkFields + 2, rows);
-    if (tails) atomicAdd(a.counters + kWorkFields + 3, tails);
+    if (rows) atomicAdd(a.counters + 1, rows * static_cast<unsigned long long>(a.n));  // Philox draws
+    if (rows) atomicAdd(a.counters + kWorkFields + 1, rows);
+    if (tails) atomicAdd(a.counters + kWorkFields + 2, tails);
   }
 }
 

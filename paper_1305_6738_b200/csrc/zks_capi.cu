@@ -97,10 +97,10 @@ struct zks_engine {
 
 namespace {
 
-// Staged words t = x >> 32 of Philox words x, u = 1 - (x >> 11) 2^-53 (stream.py:57-63):
+// Top words t = x >> 32 of Philox words x, u = 1 - (x >> 11) 2^-53 (stream.py:57-63):
 // u > h <=> m = x >> 11 < M(h), M(h) = #{m : 1 - m 2^-53 > h} (exact, by bisection on m).
 // Hence t < M >> 21 decides u > h, t > M >> 21 decides u <= h, and t == M >> 21 is undecided.
-uint32_t staged_cut(double h) {
+uint32_t word_cut(double h) {
   uint64_t lo = 0, hi = uint64_t(1) << 53;  // smallest m with 1 - m 2^-53 <= h in [lo, hi]
   while (lo < hi) {
     const uint64_t mid = (lo + hi) / 2;
@@ -351,7 +351,7 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   for (int j = 0; j < 4; ++j) {
     t->head[j] = j + 1 < len ? cdf_host[j] : __builtin_huge_val();
     t->tail_mass = len > 64 ? std::max(0.0, 1.0 - cdf_host[63]) : 0.0;
-    t->tcut[j] = staged_cut(t->head[j]);
+    t->tcut[j] = word_cut(t->head[j]);
   }
   // one stream-ordered allocation (cdf then guide): no device-wide synchronisation
   void* mem = nullptr;

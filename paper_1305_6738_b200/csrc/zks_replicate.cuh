@@ -61,11 +61,6 @@ struct ReplicateArgs {
   int batch;                     // replicates per warp batch (replicate_batch_kernel)
   int vals_stride;               // u16 sample slots per replicate in the batch store
   int guide_levels;              // 1, or 2 for long tables (L > 4096)
-  // staged uniforms (shared by the cells of a sweep with equal n and seed): u of replicate
-  // index i, draw j at ubuf[(i - ubuf_first) * ubuf_stride + j]; NULL = generate (Philox)
-  const uint32_t* ubuf;
-  int64_t ubuf_stride;
-  uint64_t ubuf_first;
   // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: u16 counts of
   // the values 1..kKsHead at pre_head[i * kKsHead] (128-byte rows), the m = pre_m[i] values
   // above kKsHead at pre_tail[i * vals_stride], log-sum / min / max.  pre_tail is consumed:
@@ -82,7 +77,7 @@ struct ReplicateArgs {
   int dense_words;
   double inv_n;  // 1 / n
   int rng;       // kRngNumpy (bit-exact with the reference) or kRngPhilox4x32 (opt-in fast stream)
-  uint32_t tcut[4];     // staged words: u > cdf_head[j] <=> t < tcut[j] (undecided at equality)
+  uint32_t tcut[4];     // top 32 bits t of a Philox word: u > cdf_head[j] <=> t < tcut[j] (undecided at equality)
   double cdf_head[4];  // cdf[0..3]; +inf from index L-1 on (every u above it draws L)
 };
 

@@ -359,9 +359,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
     if (threadIdx.x == 0 && rows) {
       atomicAdd(a.counters + 1, rows * static_cast<unsigned long long>(n));  // Philox draws
       atomicAdd(a.counters + kWorkFields, rows * static_cast<unsigned long long>(n));  // keys bucketed
-      atomicAdd(a.counters + kWorkFields + 2, rows * static_cast<unsigned long long>(a.ncells));
+      atomicAdd(a.counters + kWorkFields + 1, rows * static_cast<unsigned long long>(a.ncells));
     }
-    if (tails) atomicAdd(a.counters + kWorkFields + 3, tails);
+    if (tails) atomicAdd(a.counters + kWorkFields + 2, tails);
   }
 }
 
