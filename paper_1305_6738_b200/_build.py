@@ -49,5 +49,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+DEBUG_LIB = os.path.join(HERE, "libzks_b200_debug.so")
+
+
+def build_debug_bounds() -> str:
+    """The bounds-checked variant (-DZKS_DEBUG_BOUNDS: violated indices trap), loaded instead of the
+    product library with ZKS_LIB=<path>; for tests only."""
+    tmp = DEBUG_LIB + ".tmp"
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-DZKS_DEBUG_BOUNDS", "-o", tmp, *SOURCES], check=True)
+    os.replace(tmp, DEBUG_LIB)
+    return DEBUG_LIB
+
+
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+
+    print(build_debug_bounds() if "--debug-bounds" in sys.argv else build(force=True, verbose=True))

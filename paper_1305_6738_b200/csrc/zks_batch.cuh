@@ -754,15 +754,19 @@ __device__ __forceinline__ void draw_row(const ReplicateArgs& a, uint64_t idx, c
     if (ok) {
       mn = min(mn, v);
       mx = max(mx, v);
+      ZKS_CHECK(v >= 1u && v <= a.L);
       if (v <= kKsHead) ++bins[v * 32 + lane];
     }
     const bool big = ok && v > kKsHead;
     const unsigned bm = __ballot_sync(0xffffffffu, big);
     if (big) {
-      if (dense)
+      if (dense) {
+        ZKS_CHECK(static_cast<int>(v - kKsHead) <= a.dense_words);
         atomicAdd(dense + (v - kKsHead - 1), 1u);
-      else
+      } else {
+        ZKS_CHECK(m + __popc(bm & lt) < static_cast<uint32_t>(a.vals_stride));
         tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+      }
       ls += __ldg(a.logs + v);
     }
     m += __popc(bm);

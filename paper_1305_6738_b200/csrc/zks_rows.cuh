@@ -159,7 +159,10 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
       if (lane == 0) up = prev;
       const uint32_t cnt = up - P;  // count of value j + 1
       const int k = j + 1;
-      if (k <= static_cast<int>(C.L) && k - kKsHead - 1 < a.dense_words) out[k - kKsHead - 1] = cnt;
+      if (k <= static_cast<int>(C.L) && k - kKsHead - 1 < a.dense_words) {
+        ZKS_CHECK(2 * (k - kKsHead) <= a.vals_stride);
+        out[k - kKsHead - 1] = cnt;
+      }
       if (cnt) {
         const unsigned long long lk = log_fixed(a.logs, static_cast<uint32_t>(k));
         add128(shi, slo, __umul64hi(cnt, lk), static_cast<unsigned long long>(cnt) * lk);
@@ -181,6 +184,7 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
     const unsigned lt = (1u << lane) - 1u;
     uint16_t* tail = C.tail + i * a.vals_stride;
     uint32_t m = 0;
+    ZKS_CHECK(E <= static_cast<uint32_t>(n));
     for (uint32_t t0 = 0; t0 < E; t0 += 32) {
       const uint32_t t = t0 + lane;
       const unsigned long long key = t < E ? keys[t] : ~0ull;
@@ -204,10 +208,13 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
       }
       const unsigned bm = __ballot_sync(0xffffffffu, in);
       if (in) {
-        if (a.dense_words)
+        if (a.dense_words) {
+          ZKS_CHECK(v > kKsHead && static_cast<int>(v - kKsHead) <= a.dense_words);
           atomicAdd(dense + (v - kKsHead - 1), 1u);
-        else
+        } else {
+          ZKS_CHECK(m + __popc(bm & lt) < static_cast<uint32_t>(a.vals_stride));
           tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+        }
       }
       m += __popc(bm);
     }
@@ -328,7 +335,10 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
     if (parked) {
       for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const unsigned long long m = raw[j];
-        keys[atomicAdd(bend + (m >> shift), 1u)] = m;
+        ZKS_CHECK((m >> shift) < static_cast<unsigned long long>(nbk));
+        const uint32_t at = atomicAdd(bend + (m >> shift), 1u);
+        ZKS_CHECK(at < static_cast<uint32_t>(n));
+        keys[at] = m;
       }
     } else {
       for (int b = threadIdx.x; b < nb; b += blockDim.x) {
@@ -336,7 +346,11 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const unsigned long long m = x.w[w] >> 11;
-          if (4 * b + w < n) keys[atomicAdd(bend + (m >> shift), 1u)] = m;
+          if (4 * b + w < n) {
+            const uint32_t at = atomicAdd(bend + (m >> shift), 1u);
+            ZKS_CHECK(at < static_cast<uint32_t>(n));
+            keys[at] = m;
+          }
         }
       }
     }

@@ -264,7 +264,10 @@ __device__ __forceinline__ void sel_compact(const SelectBatch& B, SelectState* s
           unsigned long long at = 0;
           if (lane == 0) at = atomicAdd(&st->cand_n[a], static_cast<unsigned long long>(__popc(m)));
           at = __shfl_sync(0xffffffffu, at, 0);
-          if (hit) cand[at + __popc(m & ((1u << lane) - 1u))] = kk[u];
+          if (hit) {
+            ZKS_CHECK(at + __popc(m & ((1u << lane) - 1u)) < static_cast<unsigned long long>(n));
+            cand[at + __popc(m & ((1u << lane) - 1u))] = kk[u];
+          }
         }
       }
     }

@@ -9,6 +9,20 @@
 #pragma once
 #include <cstdint>
 
+// Bounds checks of the debug build (python -m paper_1305_6738_b200._build --debug-bounds, i.e.
+// -DZKS_DEBUG_BOUNDS): a violated index traps the kernel (the launch fails loudly); compiled out
+// otherwise.  compute-sanitizer is closed on the GPU pool this engine was built on.
+#ifdef ZKS_DEBUG_BOUNDS
+#define ZKS_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define ZKS_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace zks {
 
 constexpr uint64_t kPhiloxM0 = 0xD2E7470EE14C6C93ull;
