@@ -453,8 +453,24 @@ static_assert(2 * kHeadRowWords >= static_cast<int>(kFitLaneTailMax), "a short t
 // fits them lane-parallel, walks each head k <= kKsHead lane by lane from the counts, and
 // scores the tails that outlive the head warp-cooperatively from the tail lists.  First-attempt
 // failures go to retry_list (count at [0], row offsets after) for retry_kernel.
+// Rows whose tails outlive the register sort (m > kOverCap: page passes) are not scored by the
+// warp that fitted them -- one such tail takes the warp for tens of page passes while its other
+// 31 rows wait, and a heavy-tailed launch (gamma ~ 1.25, n ~ 5 x 10^4) then fills a fraction of
+// the GPU.  fit_ks_kernel lists them with their head state instead (the retry list's pattern);
+// long_tail_kernel scores them one warp per row, with the same function on the same inputs.
+struct TailList {
+  uint32_t* list;  // [0] = count, then row offsets in the chunk
+  double* S;       // head state at k = kKsHead per listed row (ks_lane_walk's S, C, D)
+  double* D;
+  double* g;       // fitted exponent and normaliser
+  double* norm;
+  uint32_t* C;
+  uint32_t* kmax;
+};
+
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(ReplicateArgs a, uint32_t* retry_list) {
+__global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(ReplicateArgs a, uint32_t* retry_list,
+                                                                       TailList tl) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* heads = reinterpret_cast<uint32_t*>(smem) + warp * kFitWarpWords;
@@ -537,6 +553,20 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
     if (kCount) wk.ks_tails += warp_sum_u32(ends);
     __syncwarp();
     unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail);
+    if (!a.dense_words) {  // paged tails to long_tail_kernel, with the lane's head state
+      const bool defer = tail && !short_tail && my_m > kOverCap;
+      if (defer) {
+        const uint32_t at = atomicAdd(tl.list, 1u);
+        tl.list[1 + at] = static_cast<uint32_t>(r0 + lane);
+        tl.S[at] = hS;
+        tl.D[at] = hD;
+        tl.g[at] = g;
+        tl.norm[at] = norm;
+        tl.C[at] = hC;
+        tl.kmax[at] = vmax;
+      }
+      need &= ~__ballot_sync(0xffffffffu, defer);
+    }
     if (a.dense_words) {  // dense finite support (K <= kDenseMaxK): the head walk continues
       // lane by lane over the row's counts of kKsHead+1..kmax, the reference's cumulative
       // form (gof.py:60-70) in the head's arithmetic; no endpoint formulas, no warp scans
@@ -602,6 +632,35 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
       a.gh_out[r0 + lane] = g;
       a.st_out[r0 + lane] = ok ? 0 : 2;
     }
+  }
+  if (kCount && lane == 0) {
+    const unsigned long long* f = &wk.attempts;
+    for (int i = 0; i < kWorkFields; ++i)
+      if (f[i]) atomicAdd(a.counters + i, f[i]);
+  }
+}
+
+// The listed long tails (fit_ks_kernel), one warp per row: page passes over the row's tail
+// values (compacted in place, ks_scan<..., kCompact>) from the row's head state -- exactly the
+// call fit_ks_kernel would have made, with the same page and histogram sizes.
+template <bool kCount>
+__global__ void __launch_bounds__(kThreads) long_tail_kernel(ReplicateArgs a, const TailList tl) {
+  const uint32_t cnt = *tl.list;
+  if (cnt == 0) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * (kFitHistWords + kKsQueueWords);
+  uint32_t* queue = hist + kFitHistWords;
+  Work wk{};
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t j = blockIdx.x * (blockDim.x >> 5) + warp; j < cnt; j += warps) {
+    const uint32_t rel = tl.list[1 + j];
+    const uint64_t row = a.first + rel - a.pre_first;
+    uint16_t* over = a.pre_tail + row * a.vals_stride;
+    const KsOut ko = ks_tail_from_head(a, 0, tl.g[j], tl.norm[j], tl.kmax[j], tl.S[j], tl.C[j], tl.D[j], hist,
+                                       kFitHistWords, kFitHistWords, queue, over, a.pre_m[row], lane, wk);
+    if (lane == 0) a.ks_out[rel] = ko.D;
+    __syncwarp();
   }
   if (kCount && lane == 0) {
     const unsigned long long* f = &wk.attempts;

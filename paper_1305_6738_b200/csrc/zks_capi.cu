@@ -541,11 +541,12 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   const bool counting = e->counters != nullptr;
   const size_t guide_bytes = zks::round_up(args[0].guide_levels * zks::kGuideLevel * 2, 16);
   // per row and cell: u16 head counts (128 B), log-sum, min / max / m, the tail slot, a
-  // retry-list slot; per cell region 256-byte aligned
-  const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(vals_stride) * 2 + 4;
+  // retry-list slot, a long-tail-list slot with its head state (44 B); per cell region 256-byte
+  // aligned
+  const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(vals_stride) * 2 + 4 + 48;
   const uint64_t chunk =
       std::max<uint64_t>(1, std::min<uint64_t>(c0.count, e->pre_cap / (row_bytes * uint64_t(ncells))));
-  const size_t region = (size_t(chunk) * row_bytes + 16 + 255) & ~size_t(255);
+  const size_t region = (size_t(chunk) * row_bytes + 64 + 255) & ~size_t(255);
   const size_t need = region * size_t(ncells);
   if (need > sc->pre_bytes) {
     if (sc->pre) ZKS_CUDA(cudaFreeAsync(sc->pre, e->stream));
@@ -560,6 +561,7 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     uint32_t *mn, *mx, *m;
     uint16_t* tail;
     uint32_t* retry;
+    zks::TailList tl;
   };
   std::vector<Pre> pre(ncells);
   for (int j = 0; j < ncells; ++j) {
@@ -572,6 +574,14 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     p.m = p.mx + chunk;
     p.tail = reinterpret_cast<uint16_t*>(p.m + chunk);
     p.retry = reinterpret_cast<uint32_t*>(p.tail + chunk * vals_stride);  // vals_stride % 4 == 0
+    double* st = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p.retry + chunk + 1) + 7) & ~uintptr_t(7));
+    p.tl.S = st;
+    p.tl.D = st + chunk;
+    p.tl.g = st + 2 * chunk;
+    p.tl.norm = st + 3 * chunk;
+    p.tl.C = reinterpret_cast<uint32_t*>(st + 4 * chunk);
+    p.tl.kmax = p.tl.C + chunk;
+    p.tl.list = p.tl.kmax + chunk;
   }
   // the retry kernel's per-warp sample store grows with n: fewer warps per block for large n
   const int rwarps = static_cast<int>(std::max<size_t>(
@@ -579,10 +589,13 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
                                            size_t(zks::retry_warp_bytes(hist_words, vals_stride)))));
   auto fit = counting ? zks::fit_ks_kernel<true> : zks::fit_ks_kernel<false>;
   auto again = counting ? zks::retry_kernel<true> : zks::retry_kernel<false>;
+  auto longk = counting ? zks::long_tail_kernel<true> : zks::long_tail_kernel<false>;
   const size_t fsmem = size_t(zks::kWarps) * zks::kFitWarpWords * 4;
+  const size_t lsmem = size_t(zks::kWarps) * (zks::kFitHistWords + zks::kKsQueueWords) * 4;
   const size_t rsmem = guide_bytes + size_t(rwarps) * zks::retry_warp_bytes(hist_words, vals_stride);
-  int fper = 0, rper = 0;
+  int fper = 0, rper = 0, lper = 0;
   if (int rc = occupancy_of(e, reinterpret_cast<const void*>(fit), fsmem, zks::kThreads, &fper)) return rc;
+  if (int rc = occupancy_of(e, reinterpret_cast<const void*>(longk), lsmem, zks::kThreads, &lper)) return rc;
   if (int rc = occupancy_of(e, reinterpret_cast<const void*>(again), rsmem, 32 * rwarps, &rper)) return rc;
   // draw phase
   const bool wide = c0.n > zks::kNarrowBinsMaxN;
@@ -700,9 +713,15 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     for (int j = 0; j < ncells; ++j) {
       ZKS_CUDA(cudaMemsetAsync(sub[j].work, 0, sizeof(unsigned long long), e->stream));
       ZKS_CUDA(cudaMemsetAsync(pre[j].retry, 0, sizeof(uint32_t), e->stream));
+      ZKS_CUDA(cudaMemsetAsync(pre[j].tl.list, 0, sizeof(uint32_t), e->stream));
       {
         Timed tm(e, ZKS_KERNEL_FIT);
-        fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub[j], pre[j].retry);
+        fit<<<(unsigned)fblocks, zks::kThreads, fsmem, e->stream>>>(sub[j], pre[j].retry, pre[j].tl);
+        ZKS_CUDA(launched(e));
+      }
+      if (!dense_words) {  // the listed paged tails, one warp each (exits at once on an empty list)
+        Timed tm(e, ZKS_KERNEL_FIT);
+        longk<<<(unsigned)(e->sms * lper), zks::kThreads, lsmem, e->stream>>>(sub[j], pre[j].tl);
         ZKS_CUDA(launched(e));
       }
       {
