@@ -40,7 +40,7 @@ constexpr int kRowMaxN = 16384;      // keys (8 B each) + buckets of one row in 
 constexpr int kRowStageMaxN = 2048;  // up to here the draw pass parks the keys in shared memory for
                                      // the scatter pass; above it the scatter pass regenerates them
 #ifndef ZKS_ROW_MINB
-#define ZKS_ROW_MINB 3
+#define ZKS_ROW_MINB 4
 #endif
 
 // Exact 53-bit cut of a cdf entry h: the smallest m <= 2^53 with 1 - m 2^-53 <= h (so u > h
@@ -107,11 +107,11 @@ __host__ __device__ constexpr int row_bucket_bits(int n) {
 }
 constexpr int kRowKeyPad = 2;  // sentinel keys (all ones) after the row: pair loads past a bucket's end
 // shared memory of one block of `warps` warps: keys + sentinels (+ the parked draw pass), bucket
-// starts and ends, and (dense supports, n <= kRowDenseHistMaxN) per-warp histograms of 65..K
+// starts, ends and counts, and (dense supports, n <= kRowDenseHistMaxN) per-warp histograms of 65..K
 constexpr int kRowDenseHistMaxN = 4096;
 __host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps) {
   return size_t(round_up(n + kRowKeyPad, 2)) * 8 + (n <= kRowStageMaxN ? size_t(round_up(n, 2)) * 8 : 0) +
-         (size_t(1) << row_bucket_bits(n)) * 8 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
+         (size_t(1) << row_bucket_bits(n)) * 12 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
 }
 
 
@@ -131,7 +131,10 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
     const uint32_t p = bstart[bk], e = bend[bk];
     const unsigned long long x0 = keys[p], x1 = keys[p + 1];
     uint32_t r = p + (p < e && x0 < M) + (p + 1 < e && x1 < M);
-    for (uint32_t s = p + 2; s < e; ++s) r += keys[s] < M;
+    if (e > p + 2) {
+#pragma unroll 1
+      for (uint32_t s = p + 2; s < e; ++s) r += keys[s] < M;
+    }
     return r;
   };
   const unsigned long long Ma = __ldg(C.mcut + lane), Mb = __ldg(C.mcut + 32 + lane);
@@ -269,10 +272,12 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
   const int nbk = 1 << a.bucket_bits;
   const int shift = 53 - a.bucket_bits;
   uint32_t* bstart = reinterpret_cast<uint32_t*>(raw + (parked ? round_up(n, 2) : 0));
-  uint32_t* bend = bstart + nbk;  // counts, then running scatter positions = bucket ends
+  uint32_t* bend = bstart + nbk;  // running scatter positions = bucket ends
+  uint32_t* cnt = bend + nbk;     // bucket sizes of the row being drawn (zeroed by the scan that reads them)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
-  uint32_t* dense = (a.dense_words && n <= kRowDenseHistMaxN) ? bend + nbk + warp * a.dense_words : nullptr;
+  uint32_t* dense = (a.dense_words && n <= kRowDenseHistMaxN) ? cnt + nbk + warp * a.dense_words : nullptr;
+  for (int b = threadIdx.x; b < nbk; b += blockDim.x) cnt[b] = 0u;
   if (dense)
     for (int k = lane; k < a.dense_words; k += 32) dense[k] = 0u;
   __shared__ unsigned long long key_sh[2][2];  // this row's and the next row's stream keys
@@ -288,31 +293,30 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
       key_sh[0][1] = k1;
     }
   }
+  __syncthreads();
   int kb = 0;  // key_sh slot of the current row
   for (uint64_t i = blockIdx.x; i < a.count; i += gridDim.x, kb ^= 1) {
-    // 1. zeroed bucket counts (the stream key was derived during the previous row)
-    for (int b = threadIdx.x; b < nbk; b += blockDim.x) bend[b] = 0u;
-    __syncthreads();
+    // 1. draw pass: bucket sizes (and the keys parked in stream order); the stream key was
+    // derived during the previous row, the counts zeroed by its scan
     const uint64_t k0 = key_sh[kb][0], k1 = key_sh[kb][1];
-    // 2. draw pass: bucket sizes (and the keys parked in stream order)
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
       const Block4 x = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         if (4 * b + w < n) {
           const unsigned long long m = x.w[w] >> 11;
-          atomicAdd(bend + (m >> shift), 1u);
+          atomicAdd(cnt + (m >> shift), 1u);
           if (parked) raw[4 * b + w] = m;
         }
       }
     }
     __syncthreads();
-    // 3. exclusive scan of the bucket sizes (each thread a contiguous segment)
+    // 2. exclusive scan of the bucket sizes (each thread a contiguous segment)
     {
       const int seg = (nbk + blockDim.x - 1) / blockDim.x;
       const int b0 = min(nbk, static_cast<int>(threadIdx.x) * seg), b1 = min(nbk, b0 + seg);
       uint32_t s = 0;
-      for (int b = b0; b < b1; ++b) s += bend[b];
+      for (int b = b0; b < b1; ++b) s += cnt[b];
       uint32_t incl = s;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -324,14 +328,15 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
       uint32_t run = incl - s;
       for (int w = 0; w < warp; ++w) run += wsum[w];
       for (int b = b0; b < b1; ++b) {
-        const uint32_t c = bend[b];
+        const uint32_t c = cnt[b];
+        cnt[b] = 0u;  // ready for the next row's draw pass
         bstart[b] = run;
         bend[b] = run;
         run += c;
       }
     }
     __syncthreads();
-    // 4. scatter pass (bend[b] ends as the end of bucket b)
+    // 3. scatter pass (bend[b] ends as the end of bucket b)
     if (parked) {
       for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const unsigned long long m = raw[j];
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_ROW_MINB) row_draw_kernel(const 
       }
     }
     __syncthreads();
-    // 5. the row's cells by the schedule; the last warp also derives the next row's stream key
+    // 4. the row's cells by the schedule; the last warp also derives the next row's stream key
     for (int c = a.wbeg[warp]; c < a.wbeg[warp + 1]; ++c)
       row_cell<kCount>(a, a.cell[a.order[c]], i, keys, bstart, bend, dense, lane, tails);
     if (warp == warps - 1 && i + gridDim.x < a.count) {
