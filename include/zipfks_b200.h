@@ -174,8 +174,9 @@ int zks_stream_uniforms(zks_engine* engine, uint64_t seed, uint64_t repetition, 
  * always numpy's. */
 int zks_engine_set_rng(zks_engine* engine, int rng);
 
-/* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (default 16 GiB,
- * 0 restores it): a cell whose rows exceed it runs chunk by chunk.  Results do not depend on it. */
+/* Memory budget (bytes) of one chunk of pre-drawn rows on the two-kernel path (0, the default: 40 %
+ * of the free device memory, at most 48 GiB): a cell whose rows exceed it runs chunk by chunk.
+ * Results do not depend on it. */
 int zks_engine_set_chunk_bytes(zks_engine* engine, uint64_t bytes);
 
 int zks_stream_uniforms_key(zks_engine* engine, uint64_t k0, uint64_t k1, int64_t count, double* out_dev);

@@ -46,7 +46,8 @@ constexpr int64_t kLogsLen = 65537;                   // ln k for k = 0..65536
 constexpr size_t kSlabBudget = size_t(4) << 30;       // overflow-slab memory cap (bytes)
 constexpr int kStagingSlots = 8;                      // pinned staging slots for table uploads
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
-constexpr uint64_t kPreBytes = uint64_t(16) << 30;    // pre-drawn rows per chunk (bytes)
+constexpr uint64_t kPreBytes = uint64_t(48) << 30;    // pre-drawn rows per chunk (bytes), at most
+constexpr double kPreFreeFrac = 0.4;                  // ... and at most this share of the free memory
 constexpr uint32_t kBatchHist = 512;                  // batch / retry histogram bins above K = 1024
 
 }  // namespace
@@ -64,7 +65,7 @@ struct zks_engine {
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
   int mle_mode = ZKS_MLE_TABLE;
   int rng = ZKS_RNG_NUMPY;  // replicate streams: numpy's (bit-exact) or the opt-in fast one
-  uint64_t pre_cap = kPreBytes;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes)
+  uint64_t pre_cap = 0;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes; 0 = from the free memory)
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::tuple<const void*, size_t, int>, int> occupancy;  // (kernel, smem, threads) -> blocks per SM
   // per-stream scratch: everything a launch writes besides its caller-owned outputs (the work
@@ -295,7 +296,7 @@ int zks_engine_sync(zks_engine* e) {
 
 int zks_engine_set_chunk_bytes(zks_engine* e, uint64_t bytes) {
   if (!e) return fail(ZKS_EINVAL, "engine is NULL");
-  e->pre_cap = bytes ? bytes : kPreBytes;
+  e->pre_cap = bytes;
   return ZKS_OK;
 }
 
@@ -480,6 +481,15 @@ int cell_args(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_d
   return ZKS_OK;
 }
 
+// the chunk budget of pre-drawn rows: the caller's, else min(kPreBytes, kPreFreeFrac of the free
+// memory + what this stream's buffer already holds) -- larger chunks mean fewer, fuller launches
+uint64_t pre_budget(zks_engine* e, const zks_engine::Scratch* sc) {
+  if (e->pre_cap) return e->pre_cap;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return uint64_t(4) << 30;
+  return std::min<uint64_t>(kPreBytes, uint64_t(kPreFreeFrac * double(free_b + sc->pre_bytes)));
+}
+
 // blocks per SM of a kernel at a dynamic shared-memory size (cached; sets the opt-in ceiling)
 int occupancy_of(zks_engine* e, const void* kernel, size_t smem, int threads, int* per) {
   const auto key = std::make_tuple(kernel, smem, threads);
@@ -545,7 +555,7 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   // aligned
   const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(vals_stride) * 2 + 4 + 48;
   const uint64_t chunk =
-      std::max<uint64_t>(1, std::min<uint64_t>(c0.count, e->pre_cap / (row_bytes * uint64_t(ncells))));
+      std::max<uint64_t>(1, std::min<uint64_t>(c0.count, pre_budget(e, sc) / (row_bytes * uint64_t(ncells))));
   const size_t region = (size_t(chunk) * row_bytes + 64 + 255) & ~size_t(255);
   const size_t need = region * size_t(ncells);
   if (need > sc->pre_bytes) {

@@ -256,7 +256,8 @@ class Engine:
         self.rng = kind
 
     def set_chunk_bytes(self, nbytes: int = 0) -> None:
-        """Budget of one chunk of pre-drawn rows (0 = the default 16 GiB); results never depend on it."""
+        """Budget of one chunk of pre-drawn rows (0 = 40 % of the free device memory, at most 48 GiB);
+        results never depend on it."""
         _native.check(self.lib.zks_engine_set_chunk_bytes(self.handle, int(nbytes)))
 
     def uniforms_key(self, k0: int, k1: int, count: int, out) -> None:
