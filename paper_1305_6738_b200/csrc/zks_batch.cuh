@@ -48,6 +48,7 @@ __device__ __forceinline__ void add_lane_work(Work& wk, const Work& lw) {
 struct DrawStats {
   double log_sum;
   uint32_t vmin, vmax;
+  uint32_t m;  // draws above kKsHead (draw_sample_lane)
 };
 
 // g += (t < T), as one compare and one predicated add
@@ -95,15 +96,18 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   return s;
 }
 
-// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle); the
-// values <= kKsHead are also counted into the lane's column of the u8 histogram lh ([v][lane]).
+// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle): the
+// values <= kKsHead counted into the lane's column of the u8 histogram lh ([v][lane]), the values
+// above it kept in the lane's tail buffer t (the first `cap`; a longer tail is scored from a
+// warp-cooperative redraw of the sample, so the lane never stores its whole sample).
 __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
-                                                      const uint16_t* __restrict__ guide, uint16_t* v, uint8_t* lh) {
+                                                      const uint16_t* __restrict__ guide, uint16_t* t, uint32_t cap,
+                                                      uint8_t* lh) {
   const int lane = threadIdx.x & 31;
   const int n = static_cast<int>(a.n);
   const int nb = (n + 3) >> 2;
   double ls = 0.0;
-  uint32_t mn = 0xffffffffu, mx = 0;
+  uint32_t mn = 0xffffffffu, mx = 0, m = 0;
   for (int b = 0; b < nb; ++b) {
     const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
     bool vb[4];
@@ -117,15 +121,20 @@ __device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, ui
         ls += __ldg(a.logs + x[w]);
         mn = min(mn, x[w]);
         mx = max(mx, x[w]);
-        if (x[w] <= kKsHead) ++lh[x[w] * 32 + lane];
+        if (x[w] <= kKsHead) {
+          ++lh[x[w] * 32 + lane];
+        } else {
+          if (m < cap) t[m] = static_cast<uint16_t>(x[w]);
+          ++m;
+        }
       }
     }
-    *reinterpret_cast<uint2*>(v + 4 * b) = make_uint2(x[0] | (x[1] << 16), x[2] | (x[3] << 16));
   }
   DrawStats s;
   s.log_sum = ls;
   s.vmin = mn;
   s.vmax = mx;
+  s.m = m;
   return s;
 }
 
@@ -276,19 +285,6 @@ __device__ __forceinline__ double ks_tail_lane(const ReplicateArgs& a, double g,
   return D;
 }
 
-// The same for a whole stored sample v[0..n) (n < kLaneDrawMaxN): its values above the head
-// are first compacted to the front of v (overwritten).
-__device__ __forceinline__ double ks_tail_lane_sample(const ReplicateArgs& a, double g, double norm, double S,
-                                                      uint32_t C, double D, uint16_t* v, uint32_t& endpoints) {
-  const int n = static_cast<int>(a.n);
-  int m = 0;
-  for (int i = 0; i < n; ++i) {
-    const uint16_t x = v[i];
-    if (x > kKsHead) v[m++] = x;
-  }
-  return ks_tail_lane(a, g, norm, S, C, D, v, m, endpoints);
-}
-
 // One replicate's second attempt on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative:
 // draw into v, fit, score.  Returns the status (1 retried, 2 failed twice).
 template <bool kCount>
@@ -312,10 +308,10 @@ __device__ __forceinline__ uint8_t retry_replicate(const ReplicateArgs& a, const
   return ok2 ? 1 : 2;
 }
 
-// per-warp shared memory of replicate_batch_kernel: histogram, queue, 32 samples (16-byte
-// aligned); sized to n so that small n leaves L1 room for the fit tables
-__host__ __device__ constexpr int batch_warp_bytes(int hist_words, int vals_stride) {
-  return round_up(hist_words * 4 + kKsQueueWords * 4 + 32 * vals_stride * 2, 16);
+// per-warp shared memory of replicate_batch_kernel: histogram, queue, 32 lane tail buffers of
+// vals_stride values, one staging row of n values (long-tail redraws, retries); 16-byte aligned
+__host__ __device__ constexpr int batch_warp_bytes(int hist_words, int vals_stride, int n) {
+  return round_up(hist_words * 4 + kKsQueueWords * 4 + 32 * vals_stride * 2 + round_up(n, 4) * 2, 16);
 }
 
 // Small samples (n < kLaneDrawMaxN): a warp takes B = 32 consecutive replicate indices;
@@ -328,11 +324,12 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
   uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
   const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int warp_bytes = batch_warp_bytes(a.hist_words, a.vals_stride);
+  const int warp_bytes = batch_warp_bytes(a.hist_words, a.vals_stride, static_cast<int>(a.n));
   unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
   uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
   uint32_t* queue = hist + a.hist_words;
-  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);
+  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);  // lane tails
+  uint16_t* stage = vals + 32 * a.vals_stride;  // one sample of n values (8-byte aligned: vals_stride % 4 == 0)
   load_guide(guide, a.guide, a.guide_levels);
   clear_hist(hist, a.hist_words, lane);
   __syncthreads();
@@ -361,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     if (active) {
       uint64_t k0, k1;
       stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
-      st = draw_sample_lane(a, k0, k1, guide, mv, lh);
+      st = draw_sample_lane(a, k0, k1, guide, mv, static_cast<uint32_t>(a.vals_stride), lh);
     }
     __syncwarp();
     if (kCount) {
@@ -394,9 +391,9 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     clear_hist(hist, kLaneHistWords, lane);
     // short tails lane by lane (insertion sort: quadratic in the tail length), long ones by the warp
     const bool tail = active && ok && !scored;
-    const bool short_tail = tail && static_cast<uint32_t>(a.n) - hC <= kLaneTailMax;
+    const bool short_tail = tail && st.m <= kLaneTailMax;  // (then st.m <= vals_stride: all kept)
     uint32_t ends = 0;
-    if (short_tail) my_ks = ks_tail_lane_sample(a, g, norm, hS, hC, hD, mv, ends);
+    if (short_tail) my_ks = ks_tail_lane(a, g, norm, hS, hC, hD, mv, static_cast<int>(st.m), ends);
     if (kCount) wk.ks_tails += warp_sum_u32(ends);
     __syncwarp();
     for (unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail); need; need &= need - 1) {
@@ -404,9 +401,15 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
       const double gr = __shfl_sync(0xffffffffu, g, r);
       const double nr = __shfl_sync(0xffffffffu, norm, r);
       const uint32_t kmax = __shfl_sync(0xffffffffu, st.vmax, r);
-      // n < kOverCap: the values above the head always fit the register sort (no pages)
-      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, a.hist_words, 0u, queue,
-                                         vals + r * a.vals_stride, static_cast<uint32_t>(a.n), lane, wk);
+      // the sample of replicate r redrawn by the warp into the staging row (its values <= kKsHead
+      // are ignored by the scan); n < kOverCap: the tail fits the register sort (no pages)
+      uint64_t q0, q1;
+      stream_key(a.seed, a.rep, a.first + r0 + r, q0, q1);
+      draw_sample(a, q0, q1, guide, stage, lane);
+      __syncwarp();
+      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, a.hist_words, 0u, queue, stage,
+                                         static_cast<uint32_t>(a.n), lane, wk);
+      __syncwarp();
       if (lane == r) my_ks = ko.D;
     }
 
@@ -415,8 +418,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kern
     for (unsigned fails = __ballot_sync(0xffffffffu, active && !ok); fails; fails &= fails - 1) {
       const int r = __ffs(fails) - 1;
       double ks2, g2;
-      const uint8_t s2 = retry_replicate<kCount>(a, M, r0 + r, guide, vals + r * a.vals_stride, hist, queue, lane, ks2,
-                                                 g2, wk);
+      const uint8_t s2 = retry_replicate<kCount>(a, M, r0 + r, guide, stage, hist, queue, lane, ks2, g2, wk);
       if (lane == r) {
         status = s2;
         my_ks = ks2;

@@ -770,10 +770,11 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
     // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
     a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
     a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
-    a.vals_stride = zks::round_up(static_cast<int>(c->n), 4);
+    // a lane's tail buffer: every tail a lane scores itself (kLaneTailMax values)
+    a.vals_stride = std::min(zks::round_up(static_cast<int>(c->n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
     a.batch = 32;  // one replicate per lane
     kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride);
+    smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride, int(c->n));
     per_block = int64_t(zks::kWarps) * a.batch;
   } else {
     a.batch = 1;
