@@ -219,8 +219,11 @@ __device__ __forceinline__ void row_cell(const RowArgs& a, const RowCell& C, uin
           ZKS_CHECK(v > kKsHead && static_cast<int>(v - kKsHead) <= a.dense_words);
           atomicAdd(dense + (v - kKsHead - 1), 1u);
         } else {
-          ZKS_CHECK(m + __popc(bm & lt) < static_cast<uint32_t>(a.vals_stride));
-          tail[m + __popc(bm & lt)] = static_cast<uint16_t>(v);
+          // keys ascend bucket by bucket, so values descend: stored back to front, the list comes
+          // out ascending up to the order inside a bucket -- the fit kernel's insertion sort of a
+          // short tail is then linear instead of quadratic
+          ZKS_CHECK(m + __popc(bm & lt) < T && T <= static_cast<uint32_t>(a.vals_stride));
+          tail[T - 1u - (m + __popc(bm & lt))] = static_cast<uint16_t>(v);
         }
       }
       m += __popc(bm);
