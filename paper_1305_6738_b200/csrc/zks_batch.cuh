@@ -646,7 +646,10 @@ __global__ void __launch_bounds__(kThreads, ZKS_FIT_MINB) fit_ks_kernel(Replicat
 // values (compacted in place, ks_scan<..., kCompact>) from the row's head state -- exactly the
 // call fit_ks_kernel would have made, with the same page and histogram sizes.
 template <bool kCount>
-__global__ void __launch_bounds__(kThreads) long_tail_kernel(ReplicateArgs a, const TailList tl) {
+#ifndef ZKS_LONG_MINB
+#define ZKS_LONG_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, ZKS_LONG_MINB) long_tail_kernel(ReplicateArgs a, const TailList tl) {
   const uint32_t cnt = *tl.list;
   if (cnt == 0) return;
   extern __shared__ __align__(16) unsigned char smem[];
