@@ -390,6 +390,7 @@ def run_b200(args, world, rank, local):
     # timed region; every engine kernel launch is bracketed by CUDA events on its stream
     stream = torch.cuda.current_stream()
     total_ms = 0.0
+    host_s = 0.0  # host time to enqueue the sweeps (the device must not wait on it)
     plans = None
     launches0 = eng.launches
     eng.set_timing(True)
@@ -401,7 +402,9 @@ def run_b200(args, world, rank, local):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
+            h0 = time.perf_counter()
             plans = sweep()
+            host_s += time.perf_counter() - h0
             e1.record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -474,6 +477,7 @@ def run_b200(args, world, rank, local):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": timed_launches,
+            "host_enqueue_ms_per_step": host_s / args.steps * 1e3,
             "clocks": clock,
             "cutoffs_sample": {f"{g},{n}": rows[(g, n)] for g, n in ((1.5, 10), (2.5, 100), (3.5, 1000))},
         }

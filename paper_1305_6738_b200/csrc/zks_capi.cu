@@ -485,6 +485,7 @@ int cell_args(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_d
 // memory + what this stream's buffer already holds) -- larger chunks mean fewer, fuller launches
 uint64_t pre_budget(zks_engine* e, const zks_engine::Scratch* sc) {
   if (e->pre_cap) return e->pre_cap;
+  if (sc->pre_bytes >= kPreBytes) return kPreBytes;  // already holds the most it may use: no driver query
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return uint64_t(4) << 30;
   return std::min<uint64_t>(kPreBytes, uint64_t(kPreFreeFrac * double(free_b + sc->pre_bytes)));
