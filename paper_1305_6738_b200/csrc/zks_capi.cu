@@ -65,7 +65,8 @@ struct zks_engine {
   unsigned long long* counters = nullptr;  // optional work counters (diagnostics)
   int mle_mode = ZKS_MLE_TABLE;
   int rng = ZKS_RNG_NUMPY;  // replicate streams: numpy's (bit-exact) or the opt-in fast one
-  uint64_t pre_cap = 0;  // pre-drawn rows per chunk (zks_engine_set_chunk_bytes; 0 = from the free memory)
+  uint64_t pre_cap = 0;   // pre-drawn rows per chunk (zks_engine_set_chunk_bytes; 0 = from the free memory)
+  uint64_t pre_auto = 0;  // ... that budget, measured at the first use
   std::map<int, zks::FitTable> fit_tables;  // per support K (0 = unbounded)
   std::map<std::tuple<const void*, size_t, int>, int> occupancy;  // (kernel, smem, threads) -> blocks per SM
   // per-stream scratch: everything a launch writes besides its caller-owned outputs (the work
@@ -483,12 +484,17 @@ int cell_args(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_d
 
 // the chunk budget of pre-drawn rows: the caller's, else min(kPreBytes, kPreFreeFrac of the free
 // memory + what this stream's buffer already holds) -- larger chunks mean fewer, fuller launches
+// memory once per engine (the driver query stalls the enqueue; repeated per call it let the device
+// idle: sweep times varied 90-108 ms)
 uint64_t pre_budget(zks_engine* e, const zks_engine::Scratch* sc) {
   if (e->pre_cap) return e->pre_cap;
-  if (sc->pre_bytes >= kPreBytes) return kPreBytes;  // already holds the most it may use: no driver query
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return uint64_t(4) << 30;
-  return std::min<uint64_t>(kPreBytes, uint64_t(kPreFreeFrac * double(free_b + sc->pre_bytes)));
+  if (!e->pre_auto) {
+    size_t free_b = 0, total_b = 0;
+    e->pre_auto = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess
+                      ? std::min<uint64_t>(kPreBytes, uint64_t(kPreFreeFrac * double(free_b + sc->pre_bytes)))
+                      : uint64_t(4) << 30;
+  }
+  return e->pre_auto;
 }
 
 // blocks per SM of a kernel at a dynamic shared-memory size (cached; sets the opt-in ceiling)
