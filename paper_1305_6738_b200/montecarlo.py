@@ -317,7 +317,8 @@ def _stage_key(cfg: SimulationConfig):
     return (cfg.support.k, cfg.n, cfg.base_seed, cfg.replicates, cfg.repetitions, cfg.quantiles)
 
 
-_ROW_CELLS = 32  # cells per zks_run_cells call
+_ROW_CELLS = 32   # cells per zks_run_cells call
+_ROW_MIN_N = 128  # rows below this n run cell by cell (the lane kernel; kLaneDrawMaxN in zks_batch.cuh)
 
 
 def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
@@ -352,14 +353,21 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
         plan.finished = torch.cuda.Event(enable_timing=True)
         plan.started.record(stream)
         outs.append(_Slab(eng, max(total, 1)))
-    tables = [_table(eng, p.config) for p in plans]
+    # below the row kernel's range the cells run one launch each: fetch each cell's draw table just
+    # before its launch, so the first cells run while the host still builds the others (e2e)
+    per_cell = n < _ROW_MIN_N
+    tables = [None] * len(plans) if per_cell else [_table(eng, p.config) for p in plans]
     for rep in range(cfg0.repetitions):
         if stop > first:
             if kernel_events is not None:  # bench.py: the row's replicate kernels
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(stream)
-            for j0 in range(0, len(plans), _ROW_CELLS):
-                part = slice(j0, j0 + _ROW_CELLS)
+            step = 1 if per_cell else _ROW_CELLS
+            for j0 in range(0, len(plans), step):
+                part = slice(j0, j0 + step)
+                for j in range(j0, min(j0 + step, len(plans))):
+                    if tables[j] is None:
+                        tables[j] = _table(eng, plans[j].config)
                 eng.run_cells(tables[part], cfg0.support.k, [p.config.gamma for p in plans[part]], n, cfg0.base_seed,
                               rep, first, stop - first,
                               [(o.ks[first:], o.gh[first:], o.st[first:]) for o in outs[part]])
