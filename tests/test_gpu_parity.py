@@ -596,3 +596,28 @@ def test_small_row_kernel_matches_cells(zk, K, n, gammas):
             np.testing.assert_array_equal(a, b)
     if -30.0 in gammas:
         assert (rows[-30.0][2] == 2).any()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_build_table_matches_single_process(zk, world):
+    # real ranks (torchrun, one process each) sharing the one GPU, gloo collectives: shards, the
+    # distributed selection's histogram all-reduces, the all-reduced statuses and the agreed
+    # failure message -- equal to the single-process results bit for bit
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", f"--nproc-per-node={world}",
+                          "--master-addr=127.0.0.1", f"--master-port={port}",
+                          os.path.join(root, "tools", "multirank_check.py")],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["world"] == world
+    assert all(line["tables_bit_identical"]), line
+    assert line["error_equal"] and "failed twice" in line["error"], line
