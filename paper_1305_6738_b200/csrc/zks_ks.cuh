@@ -315,10 +315,11 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
     // above the head: endpoints of the observed values
     int q = 0;
     ks_sparse_tiles<kArg>(s, c, q, kKsHead + 1, kmax < H ? kmax : H, hist, 0u, lane, wk);
-    bool paged = true;
-    if (!s.done && kmax > H) {
-      // Values above H are few unless the tail is very heavy: with at most kOverCap of them,
-      // take them in increasing order by repeated warp minimum over registers (no pages).
+    // Values above `above` (all of over_vals' values above it) in increasing order: with at most
+    // kOverCap of them, sorted in registers and scored run by run (no pages).  Returns false
+    // (nothing consumed) when there are more.  Used first above H and, on compacting scans,
+    // again whenever a page pass leaves few values above its page.
+    auto reg_tail = [&](uint64_t above) -> bool {
       if (q) {
         ks_flush<kArg>(s, c, q, lane, wk);  // the emptied queue stages the values
         q = 0;
@@ -330,15 +331,15 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       for (uint32_t i0 = 0; i0 < over_n; i0 += 32) {
         const uint32_t i = i0 + lane;
         const uint64_t v = i < over_n ? static_cast<uint64_t>(over_vals[i]) : 0ull;
-        const bool big = v > H;
+        const bool big = v > above;
         const unsigned b = __ballot_sync(0xffffffffu, big);
         const uint32_t slot = m + __popc(b & lt);
         if (big && slot < kOverCap) queue[slot] = static_cast<uint32_t>(v);
         m += __popc(b);
       }
       __syncwarp();
-      if (m <= kOverCap) {
-        paged = false;
+      if (m > kOverCap) return false;
+      {
         constexpr int kSlots = kOverCap / 32;
         const int size = m <= 32u ? 32 : m <= 64u ? 64 : 128;  // sort only the occupied slots
         uint32_t r[kSlots];  // element i = slot * 32 + lane
@@ -414,7 +415,10 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
         ks_flush<kArg>(s, c, ne, lane, wk);
         s.Cb += m;
       }
-    }
+      return true;
+    };
+    bool paged = !s.done && kmax > H;
+    if (paged && reg_tail(H)) paged = false;
     uint64_t pa = H + 1;
     while (paged && !s.done && pa <= kmax) {
       out.used_pages = true;
@@ -456,6 +460,9 @@ __device__ KsOut ks_scan(const KsParams& p, double g, double norm, uint64_t kmax
       ks_sparse_tiles<kArg>(s, c, q, pa, pb, hist, pa, lane, wk);
       pa = pb + 1;
       if (next != ~0ull && next > pa) pa = next;  // no observations in between: no endpoints
+      // compacted: the values left are exactly those above pb -- once few, one register pass
+      // scores them all instead of a page pass per sparse cluster
+      if (kCompact && !s.done && over_n <= kOverCap && reg_tail(pb)) break;
     }
     ks_flush<kArg>(s, c, q, lane, wk);
   }
