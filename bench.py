@@ -331,7 +331,7 @@ def roofline(work, ktimes, peaks, args, world, shard, R, ncells, total_ms, sm_mh
 
 
 KERNEL_NAMES = {"row": "row_draw_kernel", "draw": "draw_stats_kernel", "fit": "fit_ks_kernel",
-                "retry": "retry_kernel", "batch": "replicate_batch_kernel", "single": "replicate_kernel",
+                "retry": "retry_kernel", "batch": "lane_row_kernel", "single": "replicate_kernel",
                 "select": "select_kernel", "other": "other"}
 
 

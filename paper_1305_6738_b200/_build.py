@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = [os.path.join(HERE, "csrc", "zks_capi.cu")]
 HEADERS = [
     os.path.join(HERE, "csrc", f)
-    for f in ("zks_stream.cuh", "zks_series.cuh", "zks_replicate.cuh", "zks_select.cuh", "zks_probe.cuh", "zks_fit.cuh", "zks_batch.cuh", "zks_ks.cuh", "zks_samples.cuh", "zks_rows.cuh")
+    for f in ("zks_stream.cuh", "zks_series.cuh", "zks_replicate.cuh", "zks_select.cuh", "zks_probe.cuh", "zks_fit.cuh", "zks_batch.cuh", "zks_ks.cuh", "zks_samples.cuh", "zks_rows.cuh", "zks_lanes.cuh")
 ] + [os.path.join(os.path.dirname(HERE), "include", "zipfks_b200.h")]
 LIB = os.environ.get("ZKS_LIB") or os.path.join(HERE, "libzks_b200.so")
 

@@ -1,16 +1,16 @@
-// Batched replicate kernels for n <= 1024 (table-mode MLE).
+// Replicate kernels for small and medium n (table-mode MLE): the shared lane / warp pieces and
+// the two-kernel path.
 //
 // Same per-replicate pipeline as replicate_kernel (montecarlo.py:89-116), re-phased so that no
 // phase is serial on a warp:
-//   * n < kLaneDrawMaxN (replicate_batch_kernel): a warp takes 32 consecutive replicate
-//     indices; each lane derives its stream key, draws its sample into shared memory (u16),
-//     fits it (Newton/bisection on the fit tables) and walks its KS head k <= kKsHead; the tails
-//     that outlive the head are scored warp-cooperatively; NoRootError replicates are retried
-//     on stream idx + 2^32 warp-cooperatively;
-//   * kLaneDrawMaxN <= n <= 1024: draw_stats_kernel draws (one warp per replicate, at high
-//     occupancy) and keeps only head counts, the tail values, log-sum / min / max; then
-//     fit_ks_kernel fits and scores 32 rows per warp the same way, and retry_kernel takes the
-//     listed first-attempt failures.
+//   * n < kLaneDrawMaxN (lane_row_kernel, zks_lanes.cuh): a warp takes 32 consecutive replicate
+//     indices, one lane each; each lane fits its replicate (Newton/bisection on the fit tables)
+//     and walks its KS head k <= kKsHead (ks_lane_walk); short tails are scored lane by lane
+//     (ks_tail_lane), long ones and NoRootError retries on stream idx + 2^32 warp-cooperatively;
+//   * kLaneDrawMaxN <= n <= kPreMaxN: the draw phase (row_draw_kernel or draw_stats_kernel)
+//     keeps only head counts, the tail values, log-sum / min / max; then fit_ks_kernel fits and
+//     scores 32 rows per warp the same way, and retry_kernel takes the listed first-attempt
+//     failures.
 #pragma once
 #include <type_traits>
 
@@ -18,9 +18,6 @@
 
 namespace zks {
 
-#ifndef ZKS_BATCH_MINB
-#define ZKS_BATCH_MINB 3
-#endif
 #ifndef ZKS_DRAW_MINB
 #define ZKS_DRAW_MINB 4
 #endif
@@ -48,7 +45,6 @@ __device__ __forceinline__ void add_lane_work(Work& wk, const Work& lw) {
 struct DrawStats {
   double log_sum;
   uint32_t vmin, vmax;
-  uint32_t m;  // draws above kKsHead (draw_sample_lane)
 };
 
 // g += (t < T), as one compare and one predicated add
@@ -93,48 +89,6 @@ __device__ __forceinline__ DrawStats draw_sample(const ReplicateArgs& a, uint64_
   s.log_sum = warp_sum(ls);
   s.vmin = warp_min_u32(mn);
   s.vmax = warp_max_u32(mx);
-  return s;
-}
-
-// The same draws by one lane alone (small n: a warp-wide pass would leave most lanes idle): the
-// values <= kKsHead counted into the lane's column of the u8 histogram lh ([v][lane]), the values
-// above it kept in the lane's tail buffer t (the first `cap`; a longer tail is scored from a
-// warp-cooperative redraw of the sample, so the lane never stores its whole sample).
-__device__ __forceinline__ DrawStats draw_sample_lane(const ReplicateArgs& a, uint64_t k0, uint64_t k1,
-                                                      const uint16_t* __restrict__ guide, uint16_t* t, uint32_t cap,
-                                                      uint8_t* lh) {
-  const int lane = threadIdx.x & 31;
-  const int n = static_cast<int>(a.n);
-  const int nb = (n + 3) >> 2;
-  double ls = 0.0;
-  uint32_t mn = 0xffffffffu, mx = 0, m = 0;
-  for (int b = 0; b < nb; ++b) {
-    const Block4 r = rng_block(static_cast<uint64_t>(b) + 1ull, k0, k1, a.rng);
-    bool vb[4];
-    uint32_t x[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) vb[w] = 4 * b + w < n;
-    draw_block(r, vb, guide, a, x);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      if (vb[w]) {
-        ls += __ldg(a.logs + x[w]);
-        mn = min(mn, x[w]);
-        mx = max(mx, x[w]);
-        if (x[w] <= kKsHead) {
-          ++lh[x[w] * 32 + lane];
-        } else {
-          if (m < cap) t[m] = static_cast<uint16_t>(x[w]);
-          ++m;
-        }
-      }
-    }
-  }
-  DrawStats s;
-  s.log_sum = ls;
-  s.vmin = mn;
-  s.vmax = mx;
-  s.m = m;
   return s;
 }
 
@@ -308,136 +262,12 @@ __device__ __forceinline__ uint8_t retry_replicate(const ReplicateArgs& a, const
   return ok2 ? 1 : 2;
 }
 
-// per-warp shared memory of replicate_batch_kernel: histogram, queue, 32 lane tail buffers of
-// vals_stride values, one staging row of n values (long-tail redraws, retries); 16-byte aligned
+// per-warp shared memory of lane_row_kernel (zks_lanes.cuh): histogram, queue, 32 lane tail
+// buffers of vals_stride values, one staging row of n values (long-tail redraws, retries); 16-byte aligned
 __host__ __device__ constexpr int batch_warp_bytes(int hist_words, int vals_stride, int n) {
   return round_up(hist_words * 4 + kKsQueueWords * 4 + 32 * vals_stride * 2 + round_up(n, 4) * 2, 16);
 }
 
-// Small samples (n < kLaneDrawMaxN): a warp takes B = 32 consecutive replicate indices;
-// each lane draws, fits and scores the head of its own replicate; tails that outlive the head
-// are scored from the lane's head state, lane by lane when short (ks_tail_lane), else
-// warp-cooperatively.
-template <bool kCount>
-__global__ void __launch_bounds__(kThreads, ZKS_BATCH_MINB) replicate_batch_kernel(ReplicateArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint16_t* guide = reinterpret_cast<uint16_t*>(smem);
-  const int guide_bytes = round_up(a.guide_levels * kGuideLevel * 2, 16);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int warp_bytes = batch_warp_bytes(a.hist_words, a.vals_stride, static_cast<int>(a.n));
-  unsigned char* mine = smem + guide_bytes + warp * warp_bytes;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(mine);
-  uint32_t* queue = hist + a.hist_words;
-  uint16_t* vals = reinterpret_cast<uint16_t*>(mine + a.hist_words * 4 + 3 * kKsQueue * 4);  // lane tails
-  uint16_t* stage = vals + 32 * a.vals_stride;  // one sample of n values (8-byte aligned: vals_stride % 4 == 0)
-  load_guide(guide, a.guide, a.guide_levels);
-  clear_hist(hist, a.hist_words, lane);
-  __syncthreads();
-
-  const int K = a.K;
-  const double dn = static_cast<double>(a.n);
-  const int B = a.batch;
-  const uint64_t nbatches = (a.count + B - 1) / B;
-  Work wk{};
-  const ModelFns M{K, a.logs, a.fit, true};
-
-  for (;;) {
-    unsigned long long bid = 0;
-    if (lane == 0) bid = atomicAdd(a.work, 1ull);
-    bid = __shfl_sync(0xffffffffu, bid, 0);
-    if (bid >= nbatches) break;
-    const uint64_t r0 = bid * B;
-    const uint64_t left = a.count - r0;
-    const int nrep = left < static_cast<uint64_t>(B) ? static_cast<int>(left) : B;
-    const bool active = lane < nrep;
-
-    // 1-2. stream key and sample of this lane's replicate
-    uint16_t* mv = vals + lane * a.vals_stride;
-    DrawStats st{0.0, 0u, 0u};
-    uint8_t* lh = reinterpret_cast<uint8_t*>(hist);  // lane histograms, zero between batches
-    if (active) {
-      uint64_t k0, k1;
-      stream_key(a.seed, a.rep, a.first + r0 + lane, k0, k1);
-      st = draw_sample_lane(a, k0, k1, guide, mv, static_cast<uint32_t>(a.vals_stride), lh);
-    }
-    __syncwarp();
-    if (kCount) {
-      wk.attempts += nrep;
-      wk.draws += static_cast<unsigned long long>(nrep) * a.n;
-    }
-
-    // 3. exponent fits, one replicate per lane
-    double g = 0.0, norm = 1.0;
-    bool ok = false;
-    Work lw{};
-    if (active) {
-      const double target = fit_target(st.log_sum, st.vmin, K, dn);
-      ok = fit_exponent(M, target, lane, g, lw);
-      if (ok) norm = fit_norm(a.fit, g);
-      if (!ok) g = target;
-      if (kCount && ok) {  // the reference's normaliser and KS terms (min(kmax, 4096), gof.py:49-105)
-        lw.norm_terms += ref_norm_terms(a.fit, g);
-        lw.ks_terms += min(st.vmax, static_cast<uint32_t>(kSeam));
-      }
-    }
-    if (kCount) add_lane_work(wk, lw);
-
-    // 4. KS: the head lane by lane, then the tails
-    double my_ks = __longlong_as_double(0x7ff8000000000000ll);
-    double hS, hD;
-    uint32_t hC;
-    const bool scored = ks_lane_head(a, ok && active, g, norm, st.vmax, lh, my_ks,
-                                     hS, hC, hD);
-    clear_hist(hist, kLaneHistWords, lane);
-    // short tails lane by lane (insertion sort: quadratic in the tail length), long ones by the warp
-    const bool tail = active && ok && !scored;
-    const bool short_tail = tail && st.m <= kLaneTailMax;  // (then st.m <= vals_stride: all kept)
-    uint32_t ends = 0;
-    if (short_tail) my_ks = ks_tail_lane(a, g, norm, hS, hC, hD, mv, static_cast<int>(st.m), ends);
-    if (kCount) wk.ks_tails += warp_sum_u32(ends);
-    __syncwarp();
-    for (unsigned need = __ballot_sync(0xffffffffu, tail && !short_tail); need; need &= need - 1) {
-      const int r = __ffs(need) - 1;
-      const double gr = __shfl_sync(0xffffffffu, g, r);
-      const double nr = __shfl_sync(0xffffffffu, norm, r);
-      const uint32_t kmax = __shfl_sync(0xffffffffu, st.vmax, r);
-      // the sample of replicate r redrawn by the warp into the staging row (its values <= kKsHead
-      // are ignored by the scan); n < kOverCap: the tail fits the register sort (no pages)
-      uint64_t q0, q1;
-      stream_key(a.seed, a.rep, a.first + r0 + r, q0, q1);
-      draw_sample(a, q0, q1, guide, stage, lane);
-      __syncwarp();
-      const KsOut ko = ks_tail_from_head(a, r, gr, nr, kmax, hS, hC, hD, hist, a.hist_words, 0u, queue, stage,
-                                         static_cast<uint32_t>(a.n), lane, wk);
-      __syncwarp();
-      if (lane == r) my_ks = ko.D;
-    }
-
-    // 5. retries on stream idx + 2^32 (montecarlo.py:106-115), warp-cooperative
-    uint8_t status = ok ? 0 : 2;
-    for (unsigned fails = __ballot_sync(0xffffffffu, active && !ok); fails; fails &= fails - 1) {
-      const int r = __ffs(fails) - 1;
-      double ks2, g2;
-      const uint8_t s2 = retry_replicate<kCount>(a, M, r0 + r, guide, stage, hist, queue, lane, ks2, g2, wk);
-      if (lane == r) {
-        status = s2;
-        my_ks = ks2;
-        g = g2;
-      }
-    }
-
-    if (active) {
-      a.ks_out[r0 + lane] = my_ks;
-      a.gh_out[r0 + lane] = g;
-      a.st_out[r0 + lane] = status;
-    }
-  }
-  if (kCount && lane == 0) {
-    const unsigned long long* f = &wk.attempts;
-    for (int i = 0; i < kWorkFields; ++i)
-      if (f[i]) atomicAdd(a.counters + i, f[i]);
-  }
-}
 
 constexpr int kHeadRowWords = kKsHead / 2 + 1;        // u16 counts of 1..kKsHead + pad: conflict-free columns
 constexpr int kFitHistWords = 32 * kHeadRowWords;      // the head rows, reused as page histogram

@@ -14,6 +14,7 @@
 #include "zks_replicate.cuh"
 #include "zks_batch.cuh"
 #include "zks_rows.cuh"
+#include "zks_lanes.cuh"
 #include "zks_samples.cuh"
 #include "zks_select.cuh"
 #include "zks_probe.cuh"
@@ -83,6 +84,8 @@ struct zks_engine {
     double* sel_out = nullptr;
     void* cand = nullptr;  // selection candidates (keys matching a 16-bit prefix)
     size_t cand_bytes = 0;
+    uint32_t* words = nullptr;  // lane_row_kernel: per resident warp n x 32 top words
+    size_t words_bytes = 0;
   };
   std::map<cudaStream_t, Scratch> scratch;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
@@ -201,6 +204,7 @@ struct zks_table {
   double tail_mass = 0.0;          // P(X > 64) = 1 - cdf[63]: the row kernel's cost estimate
   uint32_t tcut[4] = {0, 0, 0, 0};  // the same tests on the top 32 bits of Philox words
   unsigned long long* mcut = nullptr;  // exact 53-bit cuts of cdf[0..kCutMax) (row_draw_kernel)
+  zks::LaneCut* lanecut = nullptr;     // top-32-bit head cuts + bucket brackets (lane_row_kernel)
   // stream ordering: the upload (and guide build) runs on `home`; another stream's first use
   // waits on `ready`; the free waits on every stream that used the table
   cudaStream_t home = nullptr;
@@ -268,6 +272,7 @@ void zks_engine_destroy(zks_engine* e) {
     cudaFree(sc.sel);
     cudaFree(sc.sel_out);
     if (sc.cand) cudaFree(sc.cand);
+    if (sc.words) cudaFree(sc.words);
   }
   for (auto& kv : e->fit_tables) cudaFree(const_cast<double*>(kv.second.coef));
   if (e->staging) cudaFreeHost(e->staging);
@@ -360,12 +365,15 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
   const int64_t cdf_slots = (len + 1) & ~int64_t(1);  // guide 16-byte aligned (vector copies)
   const size_t guide_bytes = (size_t(zks::kGuideEntries) * sizeof(uint16_t) + 15) & ~size_t(15);
   cudaError_t err =
-      cudaMallocAsync(&mem, cdf_slots * sizeof(double) + guide_bytes + zks::kCutMax * sizeof(unsigned long long),
+      cudaMallocAsync(&mem,
+                      cdf_slots * sizeof(double) + guide_bytes + zks::kCutMax * sizeof(unsigned long long) +
+                          sizeof(zks::LaneCut),
                       e->stream);
   if (err == cudaSuccess) {
     t->cdf = static_cast<double*>(mem);
     t->guide = reinterpret_cast<uint16_t*>(t->cdf + cdf_slots);
     t->mcut = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(t->guide) + guide_bytes);
+    t->lanecut = reinterpret_cast<zks::LaneCut*>(t->mcut + zks::kCutMax);
   }
   if (err == cudaSuccess) {
     // stage through a pinned slot so the copy never waits for kernels already queued
@@ -388,6 +396,11 @@ int zks_table_create(zks_engine* e, const double* cdf_host, int64_t len, zks_tab
     if (err == cudaSuccess) {
       Timed tm(e, ZKS_KERNEL_OTHER);
       zks::cut_kernel<<<zks::kCutMax / 256, 256, 0, e->stream>>>(t->cdf, t->len, t->mcut);
+      err = launched(e);
+    }
+    if (err == cudaSuccess) {
+      Timed tm(e, ZKS_KERNEL_OTHER);
+      zks::lane_cut_kernel<<<16, 256, 0, e->stream>>>(t->mcut, t->lanecut);
       err = launched(e);
     }
   }
@@ -751,6 +764,68 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   return ZKS_OK;
 }
 
+// Small samples (n < kLaneDrawMaxN, table MLE) for ncells cells of one row (equal n, support,
+// seed, repetition and replicate range; gammas differ): one lane_row_kernel launch, each replicate
+// stream drawn once per work item for the cells of its group.  A single cell runs through here
+// too (ncells = 1), so a cell's results do not depend on whether it was computed alone or in a row.
+int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                  double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+  const zks_cell& c0 = cells[0];
+  zks_engine::Scratch* sc = nullptr;
+  ZKS_CUDA(scratch_for(e, &sc));
+  thread_local zks::LaneArgs la;  // 18 KB: kept off the host stack
+  std::memset(&la, 0, sizeof la);
+  const uint32_t L = tables[0]->len;
+  const int H = static_cast<int>(L <= 1024u ? L : kBatchHist);
+  for (int j = 0; j < ncells; ++j) {
+    ZKS_CUDA(table_use(e, tables[j]));
+    zks::ReplicateArgs& a = la.cell[j];
+    if (int rc = cell_args(e, tables[j], &cells[j], ks_dev[j], gh_dev[j], st_dev[j], sc, a)) return rc;
+    // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
+    a.H = H;
+    a.hist_words = std::max(zks::round_up(std::max(H, 4) + 1, 4), zks::kLaneHistWords);
+    // a lane's tail buffer: every tail a lane scores itself (kLaneTailMax values)
+    a.vals_stride = std::min(zks::round_up(static_cast<int>(c0.n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
+    a.batch = 32;
+    a.slab = nullptr;
+    a.slab_cap = 0;
+    la.cut[j] = tables[j]->lanecut;
+  }
+  la.ncells = ncells;
+  const bool counting = e->counters != nullptr;
+  auto kernel = counting ? zks::lane_row_kernel<true> : zks::lane_row_kernel<false>;
+  const zks::ReplicateArgs& a0 = la.cell[0];
+  const size_t smem = zks::kLaneLnBytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a0.hist_words, a0.vals_stride,
+                                                                                       int(c0.n));
+  int per_sm = 0;
+  if (int rc = occupancy_of(e, reinterpret_cast<const void*>(kernel), smem, zks::kThreads, &per_sm)) return rc;
+  const int64_t tiles = (c0.count + 31) / 32;
+  int64_t blocks = std::min<int64_t>(int64_t(e->sms) * per_sm, (tiles + zks::kWarps - 1) / zks::kWarps);
+  // enough work items for about two per resident warp: short launches split the cells into
+  // groups (each group redraws its tiles)
+  const int64_t warps = int64_t(e->sms) * per_sm * zks::kWarps;
+  int groups = static_cast<int>(std::min<int64_t>(ncells, std::max<int64_t>(1, (2 * warps + tiles - 1) / tiles)));
+  la.per_group = (ncells + groups - 1) / groups;
+  la.groups = (ncells + la.per_group - 1) / la.per_group;
+  blocks = std::min<int64_t>(int64_t(e->sms) * per_sm, (tiles * la.groups + zks::kWarps - 1) / zks::kWarps);
+  const size_t need = size_t(blocks) * zks::kWarps * size_t(c0.n) * 32 * sizeof(uint32_t);
+  if (need > sc->words_bytes) {
+    if (sc->words) ZKS_CUDA(cudaFreeAsync(sc->words, e->stream));
+    sc->words = nullptr;
+    sc->words_bytes = 0;
+    ZKS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc->words), need, e->stream));
+    sc->words_bytes = need;
+  }
+  la.words = sc->words;
+  ZKS_CUDA(cudaMemsetAsync(a0.work, 0, sizeof(unsigned long long), e->stream));
+  {
+    Timed tm(e, ZKS_KERNEL_BATCH);
+    kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(la);
+    ZKS_CUDA(launched(e));
+  }
+  return ZKS_OK;
+}
+
 int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
                         uint8_t* st_dev) {
   if (!e) return fail(ZKS_EINVAL, "engine is NULL");
@@ -761,6 +836,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   const bool table_mode = e->mle_mode == ZKS_MLE_TABLE;
   if (table_mode && c->n >= zks::kLaneDrawMaxN && c->n <= zks::kPreMaxN)
     return run_pre_rows(e, 1, &t, c, &ks_dev, &gh_dev, &st_dev);
+  if (table_mode && c->n < zks::kLaneDrawMaxN) return run_lane_rows(e, 1, &t, c, &ks_dev, &gh_dev, &st_dev);
   ZKS_CUDA(table_use(e, t));
   zks_engine::Scratch* sc = nullptr;
   ZKS_CUDA(scratch_for(e, &sc));
@@ -768,36 +844,21 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   if (int rc = cell_args(e, t, c, ks_dev, gh_dev, st_dev, sc, a)) return rc;
   const uint32_t L = t->len;
   const bool counting = e->counters != nullptr;
-  const bool batched = table_mode && c->n < zks::kLaneDrawMaxN;
+  // replicate_kernel: direct-sum MLE at any n, table MLE above kPreMaxN (one warp per replicate)
   const size_t guide_bytes = zks::round_up(a.guide_levels * zks::kGuideLevel * 2, 16);
-  void (*kernel)(zks::ReplicateArgs);
-  size_t smem;
-  int64_t per_block;  // replicates one block takes per work item round
-  if (batched) {
-    // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
-    a.H = static_cast<int32_t>(L <= 1024u ? L : kBatchHist);
-    a.hist_words = std::max(zks::round_up(std::max(a.H, 4) + 1, 4), zks::kLaneHistWords);
-    // a lane's tail buffer: every tail a lane scores itself (kLaneTailMax values)
-    a.vals_stride = std::min(zks::round_up(static_cast<int>(c->n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
-    a.batch = 32;  // one replicate per lane
-    kernel = counting ? zks::replicate_batch_kernel<true> : zks::replicate_batch_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a.hist_words, a.vals_stride, int(c->n));
-    per_block = int64_t(zks::kWarps) * a.batch;
-  } else {
-    a.batch = 1;
-    a.vals_stride = 0;
-    kernel = counting ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
-    smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words + 3 * zks::kKsQueue) * 4;
-    per_block = zks::kWarps;
-  }
+  a.batch = 1;
+  a.vals_stride = 0;
+  auto kernel = counting ? zks::replicate_kernel<true> : zks::replicate_kernel<false>;
+  const size_t smem = guide_bytes + size_t(zks::kWarps) * (a.hist_words + 3 * zks::kKsQueue) * 4;
+  const int64_t per_block = zks::kWarps;  // replicates one block takes per work item round
   int per_sm = 0;
   if (int rc = occupancy_of(e, reinterpret_cast<const void*>(kernel), smem, zks::kThreads, &per_sm)) return rc;
   int64_t blocks = int64_t(e->sms) * std::max(per_sm, 1);
   blocks = std::min<int64_t>(blocks, (int64_t)((c->count + per_block - 1) / per_block));
   a.slab = nullptr;
   a.slab_cap = 0;
-  if (!batched && L > static_cast<uint32_t>(a.H)) {
-    // replicate_kernel: worst case every draw of a replicate lands above the histogram, so
+  if (L > static_cast<uint32_t>(a.H)) {
+    // worst case every draw of a replicate lands above the histogram, so
     // capacity n per warp
     const size_t per_warp = size_t(c->n) * sizeof(uint16_t);
     int64_t max_blocks = int64_t(kSlabBudget / (per_warp * zks::kWarps));
@@ -816,7 +877,7 @@ int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, do
   }
   ZKS_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), e->stream));
   {
-    Timed tm(e, batched ? ZKS_KERNEL_BATCH : ZKS_KERNEL_SINGLE);
+    Timed tm(e, ZKS_KERNEL_SINGLE);
     kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(a);
     ZKS_CUDA(launched(e));
   }
@@ -850,6 +911,8 @@ int zks_run_cells(zks_engine* e, int32_t ncells, const zks_table* const* tables,
   ZKS_CUDA(cudaSetDevice(e->device));
   if (e->mle_mode == ZKS_MLE_TABLE && c0.n >= zks::kLaneDrawMaxN && c0.n <= zks::kRowMaxN)
     return run_pre_rows(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
+  if (e->mle_mode == ZKS_MLE_TABLE && c0.n < zks::kLaneDrawMaxN)
+    return run_lane_rows(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
   for (int j = 0; j < ncells; ++j)  // other sizes: cell by cell (independent streams per launch)
     if (int rc = run_replicates_impl(e, tables[j], &cells[j], ks_dev[j], gh_dev[j], st_dev[j])) return rc;
   return ZKS_OK;

@@ -318,7 +318,6 @@ def _stage_key(cfg: SimulationConfig):
 
 
 _ROW_CELLS = 32   # cells per zks_run_cells call
-_ROW_MIN_N = 128  # rows below this n run cell by cell (the lane kernel; kLaneDrawMaxN in zks_batch.cuh)
 
 
 def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
@@ -326,7 +325,7 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
 
     build_table seeds every cell with the same base_seed (montecarlo.py:276-277), so cells with
     equal n draw from identical uniforms: zks_run_cells draws each replicate's stream once for
-    all of them (128 <= n <= 16384; other sizes run cell by cell inside the same call).  The
+    all of them (n <= 16384 in table mode; other sizes run cell by cell inside the same call).  The
     cells' order statistics are selected in batched launches.  Results are identical to running
     the cells one by one.
     """
@@ -353,21 +352,14 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
         plan.finished = torch.cuda.Event(enable_timing=True)
         plan.started.record(stream)
         outs.append(_Slab(eng, max(total, 1)))
-    # below the row kernel's range the cells run one launch each: fetch each cell's draw table just
-    # before its launch, so the first cells run while the host still builds the others (e2e)
-    per_cell = n < _ROW_MIN_N
-    tables = [None] * len(plans) if per_cell else [_table(eng, p.config) for p in plans]
+    tables = [_table(eng, p.config) for p in plans]
     for rep in range(cfg0.repetitions):
         if stop > first:
             if kernel_events is not None:  # bench.py: the row's replicate kernels
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(stream)
-            step = 1 if per_cell else _ROW_CELLS
-            for j0 in range(0, len(plans), step):
-                part = slice(j0, j0 + step)
-                for j in range(j0, min(j0 + step, len(plans))):
-                    if tables[j] is None:
-                        tables[j] = _table(eng, plans[j].config)
+            for j0 in range(0, len(plans), _ROW_CELLS):
+                part = slice(j0, j0 + _ROW_CELLS)
                 eng.run_cells(tables[part], cfg0.support.k, [p.config.gamma for p in plans[part]], n, cfg0.base_seed,
                               rep, first, stop - first,
                               [(o.ks[first:], o.gh[first:], o.st[first:]) for o in outs[part]])

@@ -621,3 +621,91 @@ def test_multirank_build_table_matches_single_process(zk, world):
     assert line["world"] == world
     assert all(line["tables_bit_identical"]), line
     assert line["error_equal"] and "failed twice" in line["error"], line
+
+
+def _run_table(table, K, n, seed, rep, first, count):
+    import torch
+
+    from paper_1305_6738_b200 import engine
+
+    eng = engine.get_engine()
+    dev = f"cuda:{eng.device}"
+    ks = torch.empty(count, dtype=torch.float64, device=dev)
+    gh = torch.empty(count, dtype=torch.float64, device=dev)
+    st = torch.empty(count, dtype=torch.uint8, device=dev)
+    eng.run_replicates(table, K, 1.3, n, seed, rep, first, count, ks, gh, st)
+    return ks.cpu().numpy(), gh.cpu().numpy(), st.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [100, 300])
+def test_words_on_cuts_resolve_exactly(zk, n):
+    # The small-n kernel classifies each stored word by its top 32 bits against top-32-bit cuts
+    # and resolves the undecided words (a cut inside the word's 2^21-wide key range) from their
+    # Philox block.  A sampling table with entries placed exactly on, and just beside, chosen
+    # words' uniforms -- in the head (value <= 64) and in the tail -- makes those words
+    # undecided; every replicate must still equal the oracle on the same table (the row kernel,
+    # n = 300, compares full 53-bit keys: the same table checks its cut positions at equality).
+    from oracle import port
+
+    from paper_1305_6738_b200 import engine
+
+    seed, rep, count = 11, 0, 64
+    cdf = port.sampling_cdf(1.3, None).copy()
+    us = [port.stream_uniforms(seed, rep, i, n, False) for i in range(count)]
+    ulp = 2.0 ** -53
+    edits = {}
+    for i, u in enumerate(us):
+        v = port.draw(cdf, u)
+        mode = i % 4
+        head = np.flatnonzero((v >= 2) & (v <= 64))
+        tail = np.flatnonzero(v > 70)
+        if mode in (0, 1) and head.size:
+            j = head[0]
+            k = int(v[j]) - 1 if mode == 0 else int(v[j]) - 2  # on the value's own cut / the one below
+            edits.setdefault(k, u[j])
+        elif mode in (2, 3) and tail.size:
+            j = tail[0]
+            k = int(v[j]) - 2  # the cut just below the word: inside its 2^-32 range, or on it
+            edits.setdefault(k, u[j] - (3 * ulp if mode == 2 else 0.0))
+    for k, x in edits.items():
+        cdf[k] = x
+    cdf = np.maximum.accumulate(cdf)
+    assert len(edits) >= count // 2
+    eng = engine.get_engine()
+    table = engine.DrawTable(eng, cdf)
+    try:
+        ks, gh, st = _run_table(table, None, n, seed, rep, 0, count)
+    finally:
+        table.close()
+    for i, u in enumerate(us):
+        obs = port.draw(cdf, u)
+        want_gh = port.fit_exponent(obs, None)
+        want_ks = port.ks_distance(obs, want_gh, None)
+        assert st[i] == 0
+        assert close(gh[i], want_gh), (i, gh[i], want_gh)
+        assert close(ks[i], want_ks), (i, ks[i], want_ks)
+
+
+@pytest.mark.parametrize("K", [None, 20, 1000])
+def test_small_n_rows_match_cells(zk, K):
+    # n < 128 sweep rows draw each stream once for all cells (lane_row_kernel); with enough
+    # replicates a work item covers every cell of the row, with few the cells split into groups
+    # -- both must equal each cell run alone, bit for bit
+    import torch
+
+    from paper_1305_6738_b200 import engine
+    from paper_1305_6738_b200.distribution import Support, sampling_cdf
+
+    eng = engine.get_engine()
+    gammas = (0.25, 1.2, 2.0, 3.1) if K else (1.1, 1.6, 2.4, 3.5)
+    dev = f"cuda:{eng.device}"
+    for n, count in ((10, 300_000), (57, 2_000), (100, 240_000)):
+        tables = [eng.table(g, K, lambda g=g: sampling_cdf(g, Support(K))) for g in gammas]
+        outs = [(torch.empty(count, dtype=torch.float64, device=dev), torch.empty(count, dtype=torch.float64, device=dev),
+                 torch.empty(count, dtype=torch.uint8, device=dev)) for _ in gammas]
+        eng.run_cells(tables, K, gammas, n, 4, 1, 17, count, outs)
+        for g, o in zip(gammas, outs):
+            ks, gh, st = run_cell(K, g, n, 4, 1, 17, count)
+            np.testing.assert_array_equal(o[0].cpu().numpy(), ks)
+            np.testing.assert_array_equal(o[1].cpu().numpy(), gh)
+            np.testing.assert_array_equal(o[2].cpu().numpy(), st)

@@ -17,7 +17,7 @@ import json
 import sys
 
 KINDS = {"row_draw_kernel": "row", "draw_stats_kernel": "draw", "fit_ks_kernel": "fit", "long_tail_kernel": "fit", "retry_kernel": "retry",
-         "replicate_batch_kernel": "batch", "replicate_kernel": "single", "select_kernel": "select"}
+         "lane_row_kernel": "batch", "replicate_kernel": "single", "select_kernel": "select"}
 SCALE_T = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
 SCALE_B = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
