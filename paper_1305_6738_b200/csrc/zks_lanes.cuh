@@ -218,10 +218,18 @@ __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const
       if (active) {
         const uint32_t cap = static_cast<uint32_t>(b.vals_stride);
         int j = 0;
+        // words stream from L2 (__ldcs: L1 keeps the tables); the next group is in flight while
+        // this one is classified
+        uint32_t nx[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) nx[w] = w < n ? __ldcs(words + w * 32 + lane) : 0u;
         for (; j + 4 <= n; j += 4) {
           uint32_t t[4];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) t[w] = __ldcs(words + (j + w) * 32 + lane);  // streamed: L1 keeps the tables
+          for (int w = 0; w < 4; ++w) {
+            t[w] = nx[w];
+            nx[w] = j + 4 + w < n ? __ldcs(words + (j + 4 + w) * 32 + lane) : 0u;
+          }
           uint32_t br[4];
 #pragma unroll
           for (int w = 0; w < 4; ++w) br[w] = __ldg(lc->br + lane_bucket(t[w]));
@@ -241,9 +249,11 @@ __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const
             }
           }
         }
-        for (; j < n; ++j) {
-          const uint32_t t = __ldcs(words + j * 32 + lane);
-          const uint32_t v = lane_value(a, lc, t, __ldg(lc->br + lane_bucket(t)), idx, j);
+#pragma unroll
+        for (int w = 0; w < 3; ++w) {  // the last n % 4 words (already in nx)
+          if (j + w >= n) break;
+          const uint32_t t = nx[w];
+          const uint32_t v = lane_value(a, lc, t, __ldg(lc->br + lane_bucket(t)), idx, j + w);
           ZKS_CHECK(v >= 1u && v <= a.L);
           vmin = min(vmin, v);
           vmax = max(vmax, v);
