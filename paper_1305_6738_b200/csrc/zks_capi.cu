@@ -89,7 +89,9 @@ struct zks_engine {
   };
   std::map<cudaStream_t, Scratch> scratch;
   unsigned long long launches = 0;  // kernels enqueued by this engine (zks_engine_launches)
-  int select_blocks = 0;            // resident grid of the cooperative selection kernel
+  int select_blocks = 0;
+  int l2_persist_max = -1;  // cudaDevAttrMaxPersistingL2CacheSize (queried at the first lane launch)
+  int l2_window_max = 0;    // cudaDevAttrMaxAccessPolicyWindowSize            // resident grid of the cooperative selection kernel
   zks::SelectBatch dist{};          // the distributed selection in progress (zks_select_dist_*)
   zks::SelectState* dist_sel = nullptr;  // ... and the state it works in (its stream's scratch)
   bool dist_active = false;
@@ -820,7 +822,34 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
   ZKS_CUDA(cudaMemsetAsync(a0.work, 0, sizeof(unsigned long long), e->stream));
   {
     Timed tm(e, ZKS_KERNEL_BATCH);
-    kernel<<<(unsigned)blocks, zks::kThreads, smem, e->stream>>>(la);
+    // the words are re-read once per cell: keep them in L2 as persisting lines (an access-policy
+    // window on this launch; the device's persisting set-aside is raised once per engine)
+    if (e->l2_persist_max < 0) {
+      int maxp = 0, maxw = 0;
+      ZKS_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, e->device));
+      ZKS_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, e->device));
+      if (maxp > 0) ZKS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(maxp)));
+      e->l2_persist_max = maxp;
+      e->l2_window_max = maxw;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(zks::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = e->stream;
+    cudaLaunchAttribute at[1];
+    if (e->l2_persist_max > 0 && e->l2_window_max > 0) {
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = sc->words;
+      at[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(need, size_t(e->l2_window_max));
+      at[0].val.accessPolicyWindow.hitRatio =
+          std::min(1.0f, float(e->l2_persist_max) / float(at[0].val.accessPolicyWindow.num_bytes));
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
+    ZKS_CUDA(cudaLaunchKernelEx(&cfg, kernel, la));
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
