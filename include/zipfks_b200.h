@@ -83,7 +83,7 @@ enum {
   ZKS_KERNEL_DRAW = 1,   /* draw_stats_kernel: samples -> head counts, tail values, log-sums */
   ZKS_KERNEL_FIT = 2,    /* fit_ks_kernel: exponent fits + KS of pre-drawn rows */
   ZKS_KERNEL_RETRY = 3,  /* retry_kernel: second attempts */
-  ZKS_KERNEL_BATCH = 4,  /* replicate_batch_kernel: n < 128, one replicate per lane */
+  ZKS_KERNEL_BATCH = 4,  /* lane_row_kernel: n < 128, one replicate per lane, all cells of a row */
   ZKS_KERNEL_SINGLE = 5, /* replicate_kernel: n > 1024 or direct-sum MLE, one warp per replicate */
   ZKS_KERNEL_SELECT = 6, /* radix selection of order statistics */
   ZKS_KERNEL_OTHER = 7,  /* tables, user-sample fits, series, draws */
@@ -111,10 +111,11 @@ int zks_run_replicates(zks_engine* engine, const zks_table* table, const zks_cel
  * the same n and repetition consume identical uniform streams.  One call runs replicates
  * [first, first+count) of ncells (<= 32) such cells -- cells[j] must differ only in gamma, with
  * tables[j] its sampling table and ks_dev[j] / gamma_hat_dev[j] / status_dev[j] its outputs as
- * in zks_run_replicates.  For 128 <= n <= 16384 each replicate's stream is drawn and its 53-bit
- * keys sorted ONCE on chip, and every cell's counts come from where its cdf cuts fall among
- * them; other sizes run cell by cell.  Results equal zks_run_replicates per cell bit for bit
- * (single cells of that size take the same kernel).  Replaces build_table's per-cell
+ * in zks_run_replicates.  In table-MLE mode for n <= 16384 each replicate's stream is drawn
+ * ONCE for all the cells (n >= 128: its 53-bit keys bucketed on chip, every cell's counts from
+ * where its cdf cuts fall among them; n < 128: the words' top 32 bits kept per lane and
+ * classified against each cell's cuts); other sizes run cell by cell.  Results equal
+ * zks_run_replicates per cell bit for bit (single cells of these sizes take the same kernels).  Replaces build_table's per-cell
  * run_simulation loop (montecarlo.py:263-314, 194-212) for one row.  Asynchronous. */
 int zks_run_cells(zks_engine* engine, int32_t ncells, const zks_table* const* tables, const zks_cell* cells,
                   double* const* ks_dev, double* const* gamma_hat_dev, uint8_t* const* status_dev);

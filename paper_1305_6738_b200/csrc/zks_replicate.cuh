@@ -58,7 +58,7 @@ struct ReplicateArgs {
   unsigned long long* counters;  // optional Work totals (kWorkFields), NULL = off
   FitTable fit;                  // exponent-fit table of this support
   int use_table;                 // 1: table-driven model functions, 0: direct sums
-  int batch;                     // replicates per warp batch (replicate_batch_kernel)
+  int batch;                     // replicates per warp batch (lane_row_kernel)
   int vals_stride;               // u16 sample slots per replicate in the batch store
   int guide_levels;              // 1, or 2 for long tables (L > 4096)
   // pre-drawn samples (draw_stats_kernel), row i = replicate index pre_first + i: u16 counts of

@@ -4,7 +4,7 @@
     compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_cases.py
 
 row_draw_kernel (list tails, dense per-draw and all-cut counts), fit_ks_kernel with page
-compaction, retry_kernel, replicate_batch_kernel (lane tails, warp tails, retries, double
+compaction, retry_kernel, lane_row_kernel (lane tails, warp tails, retries, double
 failures), draw_stats_kernel (16384 < n <= 65535), replicate_kernel (overflow slab, direct-sum
 MLE), the cooperative selection and the distributed selection steps, user-sample fits, series,
 solves, uniforms, draws, the fast stream.
