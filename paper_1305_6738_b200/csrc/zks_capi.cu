@@ -638,20 +638,21 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   auto rowk = counting ? zks::row_draw_kernel<true> : zks::row_draw_kernel<false>;
   // warps per row block (the cells are spread over them by the schedule below)
   int row_warps = std::max(4, std::min(zks::kWarps, ncells));
-  if (rows && row_warps > 4 && c0.n <= 512) {
+  int row_bits = zks::row_bucket_bits(static_cast<int>(c0.n));
+  if (rows && row_warps > 4 && c0.n <= 1024) {
     // blocks of 4 warps when they keep as many warps resident: more, smaller blocks per SM leave
-    // fewer warps idle at a row's barriers (measured, 21-cell rows: n = 128..500 7-8 % faster;
-    // n = 700 2 % and n = 1000 5 % slower, where a row's longer cell lists favour 8 warps)
+    // fewer warps idle at a row's barriers (measured, 21-cell rows: n = 128..1000 5-8 % faster,
+    // with 512 buckets for 512 < n <= 1024 so that 8 such blocks fit; n = 1500..3000: no gain)
     int p8 = 0, p4 = 0;
     const int n = static_cast<int>(c0.n);
-    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), zks::row_smem_bytes(n, dense_words, row_warps),
+    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), zks::row_smem_bytes(n, dense_words, row_warps, row_bits),
                               32 * row_warps, &p8))
       return rc;
-    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), zks::row_smem_bytes(n, dense_words, 4), 128, &p4))
+    if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), zks::row_smem_bytes(n, dense_words, 4, row_bits), 128, &p4))
       return rc;
     if (p4 * 4 >= p8 * row_warps) row_warps = 4;
   }
-  const size_t rsmem_row = zks::row_smem_bytes(static_cast<int>(c0.n), dense_words, row_warps);
+  const size_t rsmem_row = zks::row_smem_bytes(static_cast<int>(c0.n), dense_words, row_warps, row_bits);
   int dper = 0;
   if (rows) {
     if (int rc = occupancy_of(e, reinterpret_cast<const void*>(rowk), rsmem_row, 32 * row_warps, &dper)) return rc;
@@ -666,7 +667,7 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
     ra.vals_stride = vals_stride;
     ra.dense_words = dense_words;
     ra.ncells = ncells;
-    ra.bucket_bits = zks::row_bucket_bits(ra.n);
+    ra.bucket_bits = row_bits;
     ra.logs = e->logs;
     ra.counters = e->counters;
     ra.rng = e->rng;

@@ -103,9 +103,10 @@ struct RowArgs {
 __host__ __device__ constexpr int row_bucket_bits(int n) {
   int b = 0;
   while ((1 << b) < n) ++b;  // ceil(log2 n): about one key per bucket
-  // larger rows: 2 (n <= 2048, keys parked) and 4 to 8 keys per bucket, so the 12 B per bucket do
-  // not cost a resident block beside the keys' 8-16 n B (measured: n = 2000 -8 %, n = 5000 -43 %)
-  if (n > 1024) b -= 1;
+  // larger rows: 2 (512 < n <= 2048, keys parked) and 4 to 8 keys per bucket, so the 12 B per
+  // bucket do not cost a resident block beside the keys' 8-16 n B (measured: n = 700 -7 %,
+  // n = 1000 -5 % with 4-warp blocks, n = 2000 -8 %, n = 5000 -43 %)
+  if (n > 512) b -= 1;
   if (n > kRowStageMaxN) b -= 2;
   return b < 4 ? 4 : (b > 12 ? 12 : b);  // <= 4096 buckets
 }
@@ -113,9 +114,9 @@ constexpr int kRowKeyPad = 2;  // sentinel keys (all ones) after the row: pair l
 // shared memory of one block of `warps` warps: keys + sentinels (+ the parked draw pass), bucket
 // starts, ends and counts, and (dense supports, n <= kRowDenseHistMaxN) per-warp histograms of 65..K
 constexpr int kRowDenseHistMaxN = 4096;
-__host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps) {
+__host__ __device__ constexpr size_t row_smem_bytes(int n, int dense_words, int warps, int bits) {
   return size_t(round_up(n + kRowKeyPad, 2)) * 8 + (n <= kRowStageMaxN ? size_t(round_up(n, 2)) * 8 : 0) +
-         (size_t(1) << row_bucket_bits(n)) * 12 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
+         (size_t(1) << bits) * 12 + (n <= kRowDenseHistMaxN ? size_t(warps) * dense_words * 4 : 0);
 }
 
 
