@@ -49,6 +49,9 @@ constexpr int kStagingSlots = 8;                      // pinned staging slots fo
 constexpr int64_t kStagingLen = 65536;                // doubles per slot
 constexpr uint64_t kPreBytes = uint64_t(48) << 30;    // pre-drawn rows per chunk (bytes), at most
 constexpr double kPreFreeFrac = 0.4;                  // ... and at most this share of the free memory
+constexpr uint64_t kPreMaxRows = uint64_t(1) << 20;   // ... and at most this many rows per cell: 8.8 fit-kernel
+                                                      // waves; larger chunks only cost allocation time
+constexpr int kLaneL2SetAside = 24 << 20;             // persisting L2 for lane_row_kernel's words (bytes)
 constexpr uint32_t kBatchHist = 512;                  // batch / retry histogram bins above K = 1024
 
 }  // namespace
@@ -254,6 +257,17 @@ int zks_engine_create(int device, const double* logs_host, int64_t logs_len, zks
   if (err != cudaSuccess) {
     zks_engine_destroy(e);
     return fail(ZKS_ECUDA, "engine allocation failed: %s", cudaGetErrorString(err));
+  }
+  // the engine's scratch (pre-drawn rows: tens of GB for large rows) comes from the device's
+  // default memory pool; keep freed blocks mapped in the pool instead of returning them to the
+  // driver at every synchronisation, so that a chunk buffer regrown for a larger row reuses them
+  // (re-mapping tens of GB stalled the enqueue for seconds, e.g. config 5's K = inf grid)
+  {
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
   }
   e->stream = e->own;
   *out = e;
@@ -576,8 +590,8 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
   // retry-list slot, a long-tail-list slot with its head state (44 B); per cell region 256-byte
   // aligned
   const uint64_t row_bytes = zks::kKsHead * 2 + 8 + 12 + uint64_t(vals_stride) * 2 + 4 + 48;
-  const uint64_t chunk =
-      std::max<uint64_t>(1, std::min<uint64_t>(c0.count, pre_budget(e, sc) / (row_bytes * uint64_t(ncells))));
+  const uint64_t chunk = std::max<uint64_t>(
+      1, std::min<uint64_t>(std::min<uint64_t>(c0.count, kPreMaxRows), pre_budget(e, sc) / (row_bytes * uint64_t(ncells))));
   const size_t region = (size_t(chunk) * row_bytes + 64 + 255) & ~size_t(255);
   const size_t need = region * size_t(ncells);
   if (need > sc->pre_bytes) {
@@ -793,6 +807,15 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
   std::memset(&la, 0, sizeof la);
   const uint32_t L = tables[0]->len;
   const int H = static_cast<int>(L <= 1024u ? L : kBatchHist);
+  // a lane's tail buffer: the tails a lane scores itself (ks_tail_lane), longer ones go to the
+  // warp.  kLaneTailMax values, or the whole sample when a cell of the row expects long tails
+  // (n P(X > 64) > kLaneTailMax / 2: K = 500 / 1000 at n = 100, gamma < 1) -- then one warp-
+  // serial tail per replicate would cost more than a resident block less
+  double tail_max = 0.0;
+  for (int j = 0; j < ncells; ++j) tail_max = std::max(tail_max, double(c0.n) * tables[j]->tail_mass);
+  const int vals_stride = tail_max > 0.5 * zks::kLaneTailMax
+                              ? zks::round_up(static_cast<int>(c0.n), 4)
+                              : std::min(zks::round_up(static_cast<int>(c0.n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
   for (int j = 0; j < ncells; ++j) {
     ZKS_CUDA(table_use(e, tables[j]));
     zks::ReplicateArgs& a = la.cell[j];
@@ -800,8 +823,7 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
     // finite supports up to 1024 fit the histogram whole; otherwise 512 bins + ordered overflow
     a.H = H;
     a.hist_words = std::max(zks::round_up(std::max(H, 4) + 1, 4), zks::kLaneHistWords);
-    // a lane's tail buffer: every tail a lane scores itself (kLaneTailMax values)
-    a.vals_stride = std::min(zks::round_up(static_cast<int>(c0.n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
+    a.vals_stride = vals_stride;
     a.batch = 32;
     a.slab = nullptr;
     a.slab_cap = 0;
@@ -842,6 +864,10 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
       int maxp = 0, maxw = 0;
       ZKS_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, e->device));
       ZKS_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, e->device));
+      // a set-aside of 24 MB of the 79 MB allowed: larger ones cost the row and fit kernels of
+      // the larger rows L2 they need (config 3: 2.61 s at 24 MB, 2.66 s at 79 MB; config 2 best
+      // at 24-48 MB, 1 % slower without)
+      maxp = std::min(maxp, kLaneL2SetAside);
       if (maxp > 0) ZKS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(maxp)));
       e->l2_persist_max = maxp;
       e->l2_window_max = maxw;
@@ -864,6 +890,11 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
       cfg.numAttrs = 1;
     }
     ZKS_CUDA(cudaLaunchKernelEx(&cfg, kernel, la));
+    ZKS_CUDA(launched(e));
+  }
+  {  // the words are dropped from L2 (no write-back of scratch)
+    Timed tm(e, ZKS_KERNEL_OTHER);
+    zks::lane_release_kernel<<<(unsigned)e->sms, 256, 0, e->stream>>>(sc->words, need & ~size_t(127));
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;

@@ -150,6 +150,15 @@ __device__ __forceinline__ uint32_t lane_value(const ReplicateArgs& a, const Lan
   return lane_exact_value(a, idx, j);
 }
 
+// After a lane_row_kernel launch: its words (scratch, rewritten by the next launch) are dropped
+// from L2 without a write-back -- they would otherwise hold persisting lines through the kernels
+// that follow and be written to HBM when evicted
+__global__ void lane_release_kernel(uint32_t* words, size_t bytes) {
+  const size_t lines = bytes / 128;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < lines; i += size_t(gridDim.x) * blockDim.x)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(words) + i * 128) : "memory");
+}
+
 template <bool kCount>
 __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const __grid_constant__ LaneArgs la) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const
       clear_hist(hist, kLaneHistWords, lane);
       // short tails lane by lane (insertion sort: quadratic in the tail length), long ones by the warp
       const bool tail = active && ok && !scored;
-      const bool short_tail = tail && m <= kLaneTailMax;  // (then m <= vals_stride: all kept)
+      const bool short_tail = tail && m <= static_cast<uint32_t>(b.vals_stride);  // all kept by the lane
       uint32_t ends = 0;
       if (short_tail) my_ks = ks_tail_lane(b, g, norm, hS, hC, hD, mv, static_cast<int>(m), ends);
       if (kCount) wk.ks_tails += warp_sum_u32(ends);

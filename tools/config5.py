@@ -107,6 +107,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--paper-seed", type=int, default=2)
     ap.add_argument("--skip-paper", action="store_true")
+    ap.add_argument("--no-warmup", action="store_true")
     args = ap.parse_args()
 
     import paper_1305_6738_b200 as zk
@@ -118,6 +119,14 @@ def main() -> None:
     total_cells = total_reps = 0
     dev_total = wall_total = 0.0
     mc._engine()
+    if not args.no_warmup:
+        # untimed: the engine's scratch at its largest (the pre-drawn-row chunk of the largest row,
+        # the small-n words), so the timed grid measures the steady state, not first-touch
+        # allocation of tens of GB
+        zk.build_table((max(ns),), cli.REFERENCE_GAMMAS_FINITE, zk.Support.finite(1000), base_seed=99,
+                       replicates=400_000, repetitions=1)
+        zk.build_table((min(100, max(ns)),), cli.REFERENCE_GAMMAS_FINITE, zk.Support.finite(1000), base_seed=99,
+                       replicates=1_000_000, repetitions=1)
     with Clocks() as clk:
         for label in args.supports.split(","):
             support = zk.Support.unbounded() if label == "inf" else zk.Support.finite(int(label))
