@@ -892,7 +892,7 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
     ZKS_CUDA(cudaLaunchKernelEx(&cfg, kernel, la));
     ZKS_CUDA(launched(e));
   }
-  {  // the words are dropped from L2 (no write-back of scratch)
+  if (need >= (size_t(16) << 20)) {  // large word buffers are dropped from L2 (no write-back of scratch)
     Timed tm(e, ZKS_KERNEL_OTHER);
     zks::lane_release_kernel<<<(unsigned)e->sms, 256, 0, e->stream>>>(sc->words, need & ~size_t(127));
     ZKS_CUDA(launched(e));
