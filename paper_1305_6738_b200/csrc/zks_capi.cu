@@ -809,11 +809,12 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
   const int H = static_cast<int>(L <= 1024u ? L : kBatchHist);
   // a lane's tail buffer: the tails a lane scores itself (ks_tail_lane), longer ones go to the
   // warp.  kLaneTailMax values, or the whole sample when a cell of the row expects long tails
-  // (n P(X > 64) > kLaneTailMax / 2: K = 500 / 1000 at n = 100, gamma < 1) -- then one warp-
-  // serial tail per replicate would cost more than a resident block less
+  // (n P(X > 64) > 40: K = 500 / 1000 at n = 100, gamma < 1) -- then one warp-serial tail per
+  // replicate would cost more than a resident block less (measured: K = 1000, n = 100, 31 cells
+  // 95 -> 85 ms; at n = 50 the same rule cost 13 %)
   double tail_max = 0.0;
   for (int j = 0; j < ncells; ++j) tail_max = std::max(tail_max, double(c0.n) * tables[j]->tail_mass);
-  const int vals_stride = tail_max > 0.5 * zks::kLaneTailMax
+  const int vals_stride = tail_max > 40.0
                               ? zks::round_up(static_cast<int>(c0.n), 4)
                               : std::min(zks::round_up(static_cast<int>(c0.n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
   for (int j = 0; j < ncells; ++j) {
