@@ -318,6 +318,7 @@ def _stage_key(cfg: SimulationConfig):
 
 
 _ROW_CELLS = 32   # cells per zks_run_cells call
+_EARLY_CELLS = 6  # cells of a sweep's first row launched ahead of the other tables
 
 
 def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_events=None, keep=None) -> None:
@@ -352,14 +353,23 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
         plan.finished = torch.cuda.Event(enable_timing=True)
         plan.started.record(stream)
         outs.append(_Slab(eng, max(total, 1)))
-    tables = [_table(eng, p.config) for p in plans]
+    # while the host still builds draw tables (the first row of a sweep), the first few cells go
+    # ahead in a launch of their own, so the device starts after _EARLY_CELLS tables instead of
+    # after all of them (results do not depend on how a row's cells are grouped)
+    pending = any((eng.device, float(p.config.gamma), p.config.support.k) in _PENDING for p in plans)
+    tables = [None] * len(plans)
     for rep in range(cfg0.repetitions):
         if stop > first:
             if kernel_events is not None:  # bench.py: the row's replicate kernels
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(stream)
-            for j0 in range(0, len(plans), _ROW_CELLS):
-                part = slice(j0, j0 + _ROW_CELLS)
+            lead = _EARLY_CELLS if rep == 0 and pending and len(plans) > 2 * _EARLY_CELLS else 0
+            bounds = ([0] if lead else []) + list(range(lead, len(plans), _ROW_CELLS)) + [len(plans)]
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                for j in range(a, b):
+                    if tables[j] is None:
+                        tables[j] = _table(eng, plans[j].config)
+                part = slice(a, b)
                 eng.run_cells(tables[part], cfg0.support.k, [p.config.gamma for p in plans[part]], n, cfg0.base_seed,
                               rep, first, stop - first,
                               [(o.ks[first:], o.gh[first:], o.st[first:]) for o in outs[part]])
