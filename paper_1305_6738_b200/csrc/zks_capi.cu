@@ -862,14 +862,17 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
     // the words are re-read once per cell: keep them in L2 as persisting lines (an access-policy
     // window on this launch; the device's persisting set-aside is raised once per engine)
     if (e->l2_persist_max < 0) {
-      int maxp = 0, maxw = 0;
-      ZKS_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, e->device));
-      ZKS_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, e->device));
       // a set-aside of 24 MB of the 79 MB allowed: larger ones cost the row and fit kernels of
       // the larger rows L2 they need (config 3: 2.61 s at 24 MB, 2.66 s at 79 MB; config 2 best
-      // at 24-48 MB, 1 % slower without)
+      // at 24-48 MB, 1 % slower without).  A performance hint only: where the device refuses it
+      // (queries or the limit fail), the launch goes without the window
+      int maxp = 0, maxw = 0;
+      if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, e->device) != cudaSuccess ||
+          cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, e->device) != cudaSuccess)
+        maxp = maxw = 0;
       maxp = std::min(maxp, kLaneL2SetAside);
-      if (maxp > 0) ZKS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(maxp)));
+      if (maxp > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(maxp)) != cudaSuccess) maxp = 0;
+      cudaGetLastError();  // clear a refused hint
       e->l2_persist_max = maxp;
       e->l2_window_max = maxw;
     }
