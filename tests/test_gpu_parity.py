@@ -709,3 +709,23 @@ def test_small_n_rows_match_cells(zk, K):
             np.testing.assert_array_equal(o[0].cpu().numpy(), ks)
             np.testing.assert_array_equal(o[1].cpu().numpy(), gh)
             np.testing.assert_array_equal(o[2].cpu().numpy(), st)
+
+
+def test_small_n_warp_tails_match_oracle(zk):
+    # n < 128 with a 48-value lane tail buffer (the row's expected tail n P(X > 64) = 39 <= 40):
+    # the replicates whose tails are longer are scored by the warp from an exact redraw -- the
+    # one lane-kernel path the heavier rows (whole-sample lane buffers) no longer take
+    from oracle import port
+
+    gamma, n, seed, count = 1.15, 102, 4, 320
+    ks, gh, st = run_cell(None, gamma, n, seed, 0, 0, count)
+    cdf = port.sampling_cdf(gamma, None)
+    long_tails = 0
+    for j in range(count):
+        obs = port.draw(cdf, port.stream_uniforms(seed, 0, j, n, False))
+        long_tails += int((obs > 64).sum() > 48)
+        want_ks, want_gh, want_st = port.replicate(gamma, None, n, seed, j, 0)
+        assert st[j] == want_st
+        assert close(ks[j], want_ks), (j, ks[j], want_ks)
+        assert close(gh[j], want_gh), (j, gh[j], want_gh)
+    assert long_tails >= 2
