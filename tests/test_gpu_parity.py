@@ -151,6 +151,8 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (None, 1.05, 120, 3, 0, 96),  # the heaviest unbounded tail at n < 128
         (None, 1.6, 800, 2, 0, 96),  # two-kernel path, tail lists around kFitLaneTailMax (lane + warp)
         (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
+        (2, 1.0, 70, 6, 0, 64),  # ... at n < 128 (lane kernel: cuts of 0 from L - 1 on)
+        (3, 0.7, 50, 6, 1, 64),
         (5, 2.0, 300, 7, 1, 64),
     ],
 )
