@@ -52,6 +52,7 @@ constexpr double kPreFreeFrac = 0.4;                  // ... and at most this sh
 constexpr uint64_t kPreMaxRows = uint64_t(1) << 20;   // ... and at most this many rows per cell: 8.8 fit-kernel
                                                       // waves; larger chunks only cost allocation time
 constexpr int kLaneL2SetAside = 24 << 20;             // persisting L2 for lane_row_kernel's words (bytes)
+constexpr double kLaneHeavyTail = 40.0;                // expected values above 64 that make a lane row cell "heavy"
 constexpr uint32_t kBatchHist = 512;                  // batch / retry histogram bins above K = 1024
 
 }  // namespace
@@ -798,8 +799,8 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
 // seed, repetition and replicate range; gammas differ): one lane_row_kernel launch, each replicate
 // stream drawn once per work item for the cells of its group.  A single cell runs through here
 // too (ncells = 1), so a cell's results do not depend on whether it was computed alone or in a row.
-int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
-                  double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+int run_lane_launch(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                    double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
   const zks_cell& c0 = cells[0];
   zks_engine::Scratch* sc = nullptr;
   ZKS_CUDA(scratch_for(e, &sc));
@@ -814,7 +815,7 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
   // 95 -> 85 ms; at n = 50 the same rule cost 13 %)
   double tail_max = 0.0;
   for (int j = 0; j < ncells; ++j) tail_max = std::max(tail_max, double(c0.n) * tables[j]->tail_mass);
-  const int vals_stride = tail_max > 40.0
+  const int vals_stride = tail_max > kLaneHeavyTail
                               ? zks::round_up(static_cast<int>(c0.n), 4)
                               : std::min(zks::round_up(static_cast<int>(c0.n), 4), zks::round_up(int(zks::kLaneTailMax), 4));
   for (int j = 0; j < ncells; ++j) {
@@ -902,6 +903,37 @@ int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, con
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
+}
+
+// The row's cells that expect long tails (n P(X > 64) > kLaneHeavyTail) run one launch each,
+// the others together: heavy cells spend most of their time in warp-scored tails and long KS
+// scans, and mixed with light cells in one launch the warps' phases and tables thrash the
+// instruction cache and L1 (K = 1000, n = 100, 31 cells: 84 ms in one launch, 69 ms split;
+// K = 500: 63 -> 53 ms).  Results do not depend on the grouping.
+int run_lane_rows(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                  double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+  std::vector<int> light;
+  for (int j = 0; j < ncells; ++j) {
+    if (ncells > 1 && double(cells[j].n) * tables[j]->tail_mass > kLaneHeavyTail) {
+      if (int rc = run_lane_launch(e, 1, tables + j, cells + j, ks_dev + j, gh_dev + j, st_dev + j)) return rc;
+    } else {
+      light.push_back(j);
+    }
+  }
+  if (light.empty()) return ZKS_OK;
+  if (int(light.size()) == ncells) return run_lane_launch(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
+  std::vector<const zks_table*> t;
+  std::vector<zks_cell> c;
+  std::vector<double*> k, g;
+  std::vector<uint8_t*> st;
+  for (int j : light) {
+    t.push_back(tables[j]);
+    c.push_back(cells[j]);
+    k.push_back(ks_dev[j]);
+    g.push_back(gh_dev[j]);
+    st.push_back(st_dev[j]);
+  }
+  return run_lane_launch(e, int(light.size()), t.data(), c.data(), k.data(), g.data(), st.data());
 }
 
 int run_replicates_impl(zks_engine* e, const zks_table* t, const zks_cell* c, double* ks_dev, double* gh_dev,
