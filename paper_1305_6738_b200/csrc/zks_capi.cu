@@ -799,12 +799,13 @@ int run_pre_rows(zks_engine* e, int ncells, const zks_table* const* tables, cons
 // seed, repetition and replicate range; gammas differ): one lane_row_kernel launch, each replicate
 // stream drawn once per work item for the cells of its group.  A single cell runs through here
 // too (ncells = 1), so a cell's results do not depend on whether it was computed alone or in a row.
-int run_lane_launch(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
-                    double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+template <int C>
+int run_lane_launch_t(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                      double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
   const zks_cell& c0 = cells[0];
   zks_engine::Scratch* sc = nullptr;
   ZKS_CUDA(scratch_for(e, &sc));
-  thread_local zks::LaneArgs la;  // 18 KB: kept off the host stack
+  thread_local zks::LaneArgsT<C> la;  // up to 18 KB: kept off the host stack
   std::memset(&la, 0, sizeof la);
   const uint32_t L = tables[0]->len;
   const int H = static_cast<int>(L <= 1024u ? L : kBatchHist);
@@ -833,7 +834,7 @@ int run_lane_launch(zks_engine* e, int ncells, const zks_table* const* tables, c
   }
   la.ncells = ncells;
   const bool counting = e->counters != nullptr;
-  auto kernel = counting ? zks::lane_row_kernel<true> : zks::lane_row_kernel<false>;
+  auto kernel = counting ? zks::lane_row_kernel<true, C> : zks::lane_row_kernel<false, C>;
   const zks::ReplicateArgs& a0 = la.cell[0];
   const size_t smem = zks::kLaneLnBytes + size_t(zks::kWarps) * zks::batch_warp_bytes(a0.hist_words, a0.vals_stride,
                                                                                        int(c0.n));
@@ -903,6 +904,12 @@ int run_lane_launch(zks_engine* e, int ncells, const zks_table* const* tables, c
     ZKS_CUDA(launched(e));
   }
   return ZKS_OK;
+}
+
+int run_lane_launch(zks_engine* e, int ncells, const zks_table* const* tables, const zks_cell* cells,
+                    double* const* ks_dev, double* const* gh_dev, uint8_t* const* st_dev) {
+  if (ncells == 1) return run_lane_launch_t<1>(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
+  return run_lane_launch_t<zks::kLaneMaxCells>(e, ncells, tables, cells, ks_dev, gh_dev, st_dev);
 }
 
 // The row's cells that expect long tails (n P(X > 64) > kLaneHeavyTail) run one launch each,

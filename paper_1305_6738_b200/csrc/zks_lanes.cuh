@@ -89,9 +89,12 @@ __global__ void lane_cut_kernel(const unsigned long long* __restrict__ mcut, Lan
   }
 }
 
-struct LaneArgs {
-  ReplicateArgs cell[kLaneMaxCells];  // the row's cells (equal n, support, seed, rep, range)
-  const LaneCut* cut[kLaneMaxCells];
+// C: the parameter block's cell capacity (kLaneMaxCells, or 1 for single cells: a 0.6 KB
+// instead of an 18 KB kernel parameter, ~10 us less per launch where launches dominate)
+template <int C>
+struct LaneArgsT {
+  ReplicateArgs cell[C];  // the row's cells (equal n, support, seed, rep, range)
+  const LaneCut* cut[C];
   uint32_t* words;  // per resident warp: n x 32 top words, [j][lane]
   int ncells;
   int groups;     // work items = tiles of 32 replicates x cell groups (more items than warps
@@ -159,8 +162,8 @@ __global__ void lane_release_kernel(uint32_t* words, size_t bytes) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<char*>(words) + i * 128) : "memory");
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const __grid_constant__ LaneArgs la) {
+template <bool kCount, int C>
+__global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const __grid_constant__ LaneArgsT<C> la) {
   extern __shared__ __align__(16) unsigned char smem[];
   const ReplicateArgs& b = la.cell[0];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
