@@ -32,6 +32,10 @@ namespace zks {
 #ifndef ZKS_LANE_MINB
 #define ZKS_LANE_MINB 3
 #endif
+#ifndef ZKS_LANE_GROUP
+#define ZKS_LANE_GROUP 4
+#endif
+constexpr int kLaneGroup = ZKS_LANE_GROUP;  // words classified per step (their loads in flight together)
 constexpr int kLaneMaxCells = 32;
 // Head cuts are bracketed by a log-scale bucket of the word: the distance x of t to the nearer end
 // of the word range (cuts crowd towards both ends -- the tail cuts of a Zipf law near t = 0, the
@@ -232,21 +236,21 @@ __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const
         int j = 0;
         // words stream from L2 (__ldcs: L1 keeps the tables); the next group is in flight while
         // this one is classified
-        uint32_t nx[4];
+        uint32_t nx[kLaneGroup];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) nx[w] = w < n ? __ldcs(words + w * 32 + lane) : 0u;
-        for (; j + 4 <= n; j += 4) {
-          uint32_t t[4];
+        for (int w = 0; w < kLaneGroup; ++w) nx[w] = w < n ? __ldcs(words + w * 32 + lane) : 0u;
+        for (; j + kLaneGroup <= n; j += kLaneGroup) {
+          uint32_t t[kLaneGroup];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < kLaneGroup; ++w) {
             t[w] = nx[w];
-            nx[w] = j + 4 + w < n ? __ldcs(words + (j + 4 + w) * 32 + lane) : 0u;
+            nx[w] = j + kLaneGroup + w < n ? __ldcs(words + (j + kLaneGroup + w) * 32 + lane) : 0u;
           }
-          uint32_t br[4];
+          uint32_t br[kLaneGroup];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) br[w] = __ldg(lc->br + lane_bucket(t[w]));
+          for (int w = 0; w < kLaneGroup; ++w) br[w] = __ldg(lc->br + lane_bucket(t[w]));
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < kLaneGroup; ++w) {
             const uint32_t v = lane_value(a, lc, t[w], br[w], idx, j + w);
             ZKS_CHECK(v >= 1u && v <= a.L);
             vmin = min(vmin, v);
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, ZKS_LANE_MINB) lane_row_kernel(const
           }
         }
 #pragma unroll
-        for (int w = 0; w < 3; ++w) {  // the last n % 4 words (already in nx)
+        for (int w = 0; w < kLaneGroup - 1; ++w) {  // the last n % kLaneGroup words (already in nx)
           if (j + w >= n) break;
           const uint32_t t = nx[w];
           const uint32_t v = lane_value(a, lc, t, __ldg(lc->br + lane_bucket(t)), idx, j + w);
