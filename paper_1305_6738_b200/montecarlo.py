@@ -363,7 +363,8 @@ def _enqueue_group(eng, plans: list[_CellPlan], shard=None, reduce=None, kernel_
             if kernel_events is not None:  # bench.py: the row's replicate kernels
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(stream)
-            lead = _EARLY_CELLS if rep == 0 and pending and len(plans) > 2 * _EARLY_CELLS else 0
+            # (small-n rows only: their extra stream draw is cheap beside the cells' work)
+            lead = _EARLY_CELLS if rep == 0 and pending and n < 128 and len(plans) > 2 * _EARLY_CELLS else 0
             bounds = ([0] if lead else []) + list(range(lead, len(plans), _ROW_CELLS)) + [len(plans)]
             for a, b in zip(bounds[:-1], bounds[1:]):
                 for j in range(a, b):
