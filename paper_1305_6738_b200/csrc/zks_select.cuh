@@ -26,7 +26,7 @@ namespace zks {
 constexpr int kMaxRanks = 16;
 constexpr int kSelMaxArrays = 24;
 #ifndef ZKS_SEL_UNROLL
-#define ZKS_SEL_UNROLL 8
+#define ZKS_SEL_UNROLL 16
 #endif
 constexpr int kSelUnroll = ZKS_SEL_UNROLL;  // key loads in flight per thread
 constexpr int kSelectPasses = 8;
