@@ -152,6 +152,9 @@ def test_replicates_match_reference_golden(zk, golden, mle_mode):
         (None, 1.6, 800, 2, 0, 96),  # two-kernel path, tail lists around kFitLaneTailMax (lane + warp)
         (3, 0.7, 200, 6, 0, 64),  # supports shorter than the four counted values (cut table)
         (2, 1.0, 70, 6, 0, 64),  # ... at n < 128 (lane kernel: cuts of 0 from L - 1 on)
+        (None, 1.3, 127, 8, 0, 96),  # the largest lane-kernel n (n % 4 = 3 words after the groups)
+        (None, 2.0, 1, 3, 0, 64),  # one observation per sample
+        (20, 1.0, 1, 3, 0, 64),
         (3, 0.7, 50, 6, 1, 64),
         (5, 2.0, 300, 7, 1, 64),
     ],
